@@ -1,0 +1,141 @@
+/*
+ * cp.h -- C ABI of libcp.so, the B200 (sm_100a) hot path of the multigrid CP method of
+ * De Sterck & Miller, arXiv 1111.6091 ("P:n" = line n of the paper's LaTeX source).
+ *
+ * The library computes, on one GPU, in IEEE fp64:
+ *   cp_mttkrp        M = Z_(n) Phi^(n)                       eq:gradEqn, eq:Phi
+ *   cp_als_sweep     one ALS / BNGS iteration (with optional   P:121, eq:relaxinnersolve P:356-358
+ *                    FAS right-hand side F) and the functional f  eq:CPfunctional P:38-42
+ *   cp_mode_product  X = Z x_n U (restriction U = Phat^T,      P:74-78, eq:ctensor_transformed
+ *                    interpolation on a 2-way factor matrix)
+ *   cp_fit           f (direct), g and ||G^(n)||^2              eq:gradConv P:454-456
+ *   cp_norm2         ||Z||^2
+ *
+ * ---------------------------------------------------------------------------------------
+ * Conventions
+ *   - Every pointer is DEVICE memory unless marked [host].  The caller owns every buffer,
+ *     the workspace included; the library allocates nothing and frees nothing.
+ *   - Tensor layout: Z of size I_1 x ... x I_N is dense, mode 1 fastest:
+ *       linear index = sum_n i_n * prod_{k<n} I_k        (0-based i_n; Kolda-Bader order,
+ *     consistent with the reversed Khatri-Rao order of Phi^(n)).
+ *   - Matrix layout: A^(n), M, F, G (I_n x R) and U (J x I_n) are column-major:
+ *       entry (i, r) at i + rows * r.
+ *   - Modes are 0-based in this ABI (mode 0 = the paper's mode 1).
+ *   - Limits: 1 <= N <= CP_MAX_N (cp_mode_product; N >= 2 for the others),
+ *     1 <= R <= CP_MAX_R, every I_n >= 1, prod I_n < 2^62.
+ *   - Inputs are never modified, except A in cp_als_sweep.  Outputs must not alias inputs.
+ *   - Nothing synchronizes the host: all work is enqueued on `stream` (a cudaStream_t;
+ *     NULL = legacy default stream), so whole sweeps can be captured in a CUDA graph.
+ *     A workspace may be used by one stream at a time.
+ *   - Results are deterministic: no atomics in any reduction, fixed summation order, so two
+ *     runs on the same inputs are bitwise identical.
+ *
+ * Errors
+ *   - Argument / shape errors return synchronously, before anything is enqueued:
+ *       CP_EINVAL  null pointer, N or R out of range, mode out of range, J < 1
+ *       CP_EDIM    a dimension < 1 or the element count overflows
+ *       CP_EWORKSPACE  ws_bytes smaller than the matching *_workspace_bytes()
+ *   - CP_ECUDA: a launch failed (cudaGetLastError after enqueueing).
+ *   - Numeric failures are asynchronous: a non-positive Cholesky pivot (Gamma singular, e.g.
+ *     a zero factor column -- the Keller condition of P:362) is written into the device
+ *     `out` status word as CP_ENOTSPD together with the failing mode; the factors are then
+ *     unspecified.
+ */
+#ifndef CP_H
+#define CP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CP_MAX_N 8
+#define CP_MAX_R 32
+#define CP_VERSION 1
+
+enum {
+    CP_OK = 0,
+    CP_EINVAL = -1,
+    CP_EDIM = -2,
+    CP_ENOTSPD = -3,
+    CP_ECUDA = -4,
+    CP_EWORKSPACE = -5
+};
+
+/* a cudaStream_t (struct CUstream_st*), spelled without including the CUDA headers */
+typedef struct CUstream_st *cp_stream_t;
+
+/* [host] problem shape: order N, rank R, sizes dims[0..N-1] (= I_1..I_N) */
+typedef struct {
+    int32_t N;
+    int32_t R;
+    int64_t dims[CP_MAX_N];
+} cp_shape;
+
+/* Workspace bytes needed by cp_norm2 / cp_mttkrp / cp_als_sweep / cp_fit for shape s on the
+ * current device (depends on the SM count).  0 on an invalid shape. */
+size_t cp_workspace_bytes(const cp_shape *s);
+
+/* ||Z||^2 -> out[0] (device).  The squared Frobenius norm of eq:CPfunctional. */
+int cp_norm2(const cp_shape *s, const double *Z, double *out, void *ws, size_t ws_bytes,
+             cp_stream_t stream);
+
+/* MTTKRP  M = Z_(mode) Phi^(mode)   (eq:gradEqn P:104-107, eq:Phi P:109-111)
+ *   A    [host] array of N device pointers to I_k x R factors (A[mode] is not read and may be
+ *        NULL);  M: I_mode x R, column-major, overwritten.
+ *   M(i,r) = sum over all other indices of z * prod_{k != mode} A^(k)(i_k, r).  The Khatri-
+ *   Rao product Phi is never materialized; Z is streamed from HBM exactly once. */
+int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_t mode,
+              double *M, void *ws, size_t ws_bytes, cp_stream_t stream);
+
+/* One ALS / block nonlinear Gauss-Seidel sweep -- with a right-hand side, the BNGS
+ * relaxation of the FAS solve phase (eq:relaxinnersolve P:356-358):
+ *   for n = 0..N-1 (ascending; each update uses the freshest factors):
+ *       M = Z_(n) Phi^(n);  Gamma = *_{k != n} A^(k)^T A^(k)   (eq:Gamma P:113-116)
+ *       A^(n) <- (M + F^(n)) Gamma^{-1}   via Gamma = L L^T, L lower, no pivoting.
+ *   Z       tensor (the finest tensor or a coarse-level tensor, eq:cfunc P:181-185)
+ *   normZ2  device pointer to ||Z||^2 (from cp_norm2)
+ *   A       [host] N device pointers, I_n x R each, updated in place
+ *   F       [host] NULL (all zero) or N device pointers, each NULL (= 0) or I_n x R
+ *   out     device, 4 doubles: f, f_tilde, status (CP_OK or CP_ENOTSPD), failed mode or -1
+ *           f       = 1/2 ||Z - [[A]]||^2 after the sweep, evaluated without another pass as
+ *                     1/2||Z||^2 - <M^(N),A^(N)> + 1/2 sum_{r,s} prod_k (A^(k)^T A^(k))_{rs}
+ *           f_tilde = f - sum_n <F^(n), A^(n)>  (the functional minimized block-wise when F != 0)
+ *   No normalization or sorting (the driver does that on the finest level only). */
+int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
+                 const double *const *F, double *out, void *ws, size_t ws_bytes,
+                 cp_stream_t stream);
+
+/* n-mode product X = Z x_mode U  (X_(n) = U Z_(n))
+ *   dims [host] N sizes of Z;  U: J x dims[mode], column-major;  X: dims with dims[mode] -> J.
+ *   Restriction (coarse tensor, Alg. 1 step 7 P:273): U = Phat^T;  interpolation A = Phat A_c
+ *   (eq:CGC P:191): N = 2, dims = {I_c, R}, mode 0, U = Phat.
+ *   ws may be NULL when cp_mode_product_workspace_bytes() returns 0. */
+size_t cp_mode_product_workspace_bytes(int32_t N, const int64_t *dims, int32_t mode, int64_t J);
+int cp_mode_product(int32_t N, const int64_t *dims, const double *Z, int32_t mode,
+                    const double *U, int64_t J, double *X, void *ws, size_t ws_bytes,
+                    cp_stream_t stream);
+
+/* Fit and stopping quantity at one iterate (eq:gradConv P:454-456):
+ *   out  device, 2 + N doubles: f (direct, one residual pass over Z), g, ||G^(n)||^2 (n < N)
+ *        G^(n) = -Z_(n)Phi^(n) + A^(n)Gamma^(n) [- F^(n)]  (eq:gradEqn; with F the FAS residual
+ *        H^(n)(A) - F^(n), eq:FASop P:326-328);  g = (sum_n ||G^(n)||^2)^{1/2} / ||Z||
+ *   F    [host] NULL or N device pointers (entries may be NULL)
+ *   G    [host] NULL or N device pointers (entries may be NULL) receiving G^(n), I_n x R. */
+int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const double *const *A,
+           const double *const *F, double *out, double *const *G, void *ws, size_t ws_bytes,
+           cp_stream_t stream);
+
+/* Number of kernel launches the last successful call on this thread enqueued (for the
+ * benchmark's gpu_launches count). */
+int cp_last_launch_count(void);
+
+const char *cp_status_string(int code);
+int cp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CP_H */

@@ -1,0 +1,210 @@
+"""paper_1111_6091_b200 -- B200 (sm_100a) hot path of the multigrid CP method of
+De Sterck & Miller, arXiv 1111.6091: MTTKRP, the ALS / BNGS sweep with Cholesky solve and the
+functional f, the n-mode products (restriction / interpolation) and f/g evaluation.
+
+This module is a thin ctypes binding over ``lib/libcp.so`` (C ABI: ``include/cp.h``).  It only
+marshals arguments: every arithmetic step runs in the library's CUDA kernels.  There is no CPU
+fallback -- importing works without a GPU, but every call raises if the CUDA library or a CUDA
+device is missing.
+
+Tensor conventions:
+  * Z: float64 CUDA tensor, contiguous, shape (I_N, ..., I_1)  (mode 1 fastest);
+  * factor matrices A^(n), F^(n), G^(n) (I_n x R) and operators U (J x I_n): float64 CUDA
+    tensors of that shape stored column-major, i.e. ``t.stride() == (1, rows)``; use
+    :func:`colmajor` to convert.
+  * modes are 0-based (mode 0 = the paper's mode 1).
+"""
+import ctypes
+import os
+
+import torch
+
+from ._lib import (CP_ECUDA, CP_EDIM, CP_EINVAL, CP_ENOTSPD, CP_EWORKSPACE, CP_MAX_N, CP_MAX_R,
+                   CP_OK, CPError, lib, lib_path)
+
+__all__ = ["colmajor", "empty_factor", "Workspace", "norm2", "mttkrp", "als_sweep",
+           "mode_product", "fit", "workspace_bytes", "lib", "lib_path", "last_launch_count",
+           "CPError", "CP_OK", "CP_EINVAL", "CP_EDIM", "CP_ENOTSPD", "CP_ECUDA", "CP_EWORKSPACE"]
+
+
+class _Shape(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int32), ("R", ctypes.c_int32), ("dims", ctypes.c_int64 * CP_MAX_N)]
+
+
+def _shape(dims, R):
+    s = _Shape()
+    s.N = len(dims)
+    s.R = int(R)
+    for i, d in enumerate(dims):
+        s.dims[i] = int(d)
+    return s
+
+
+def colmajor(t):
+    """Column-major (Fortran-order) copy/view of a 2-D tensor: stride (1, rows)."""
+    if t.dim() != 2:
+        raise ValueError("expected a 2-D tensor")
+    if t.stride(0) == 1 and (t.stride(1) == t.shape[0] or t.shape[1] == 1):
+        return t
+    return t.t().contiguous().t()
+
+
+def empty_factor(rows, cols, device="cuda", dtype=torch.float64):
+    return torch.empty((cols, rows), device=device, dtype=dtype).t()
+
+
+def _check_cm(t, rows, cols, name):
+    if t.dtype != torch.float64 or not t.is_cuda:
+        raise TypeError(f"{name}: expected a float64 CUDA tensor")
+    if tuple(t.shape) != (rows, cols):
+        raise ValueError(f"{name}: expected shape {(rows, cols)}, got {tuple(t.shape)}")
+    if rows > 1 and cols > 1 and not (t.stride(0) == 1 and t.stride(1) == rows):
+        raise ValueError(f"{name}: must be column-major (use colmajor())")
+
+
+def _check_Z(Z, dims):
+    if Z.dtype != torch.float64 or not Z.is_cuda or not Z.is_contiguous():
+        raise TypeError("Z: expected a contiguous float64 CUDA tensor")
+    n = 1
+    for d in dims:
+        n *= int(d)
+    if Z.numel() != n:
+        raise ValueError(f"Z: {Z.numel()} elements, dims {tuple(dims)} need {n}")
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p()
+
+
+def _ptr_array(ts):
+    arr = (ctypes.c_void_p * len(ts))()
+    for i, t in enumerate(ts):
+        arr[i] = t.data_ptr() if t is not None else None
+    return arr
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(code, what):
+    if code != CP_OK:
+        raise CPError(code, what)
+
+
+def workspace_bytes(dims, R):
+    lib()
+    return int(lib().cp_workspace_bytes(ctypes.byref(_shape(dims, R))))
+
+
+class Workspace:
+    """Caller-owned device workspace (the library allocates nothing)."""
+
+    def __init__(self, dims, R, device="cuda"):
+        self.dims = tuple(int(d) for d in dims)
+        self.R = int(R)
+        self.nbytes = max(256, workspace_bytes(self.dims, self.R))
+        self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+
+    def fits(self, dims, R):
+        return workspace_bytes(dims, R) <= self.nbytes
+
+
+def _ws(ws, dims, R, device):
+    if ws is None:
+        ws = Workspace(dims, R, device)
+    elif not ws.fits(dims, R):
+        raise CPError(CP_EWORKSPACE, "workspace too small")
+    return ws
+
+
+def last_launch_count():
+    return int(lib().cp_last_launch_count())
+
+
+def norm2(Z, dims, out=None, ws=None, stream=None):
+    """||Z||^2 as a 1-element float64 CUDA tensor (cp_norm2)."""
+    _check_Z(Z, dims)
+    out = torch.empty(1, dtype=torch.float64, device=Z.device) if out is None else out
+    ws = _ws(ws, dims, 1, Z.device)
+    _check(lib().cp_norm2(ctypes.byref(_shape(dims, 1)), _ptr(Z), _ptr(out), _ptr(ws.buf),
+                          ctypes.c_size_t(ws.nbytes), _stream(stream)), "cp_norm2")
+    return out
+
+
+def mttkrp(Z, dims, A, mode, M=None, ws=None, stream=None):
+    """M = Z_(mode) Phi^(mode)  (I_mode x R, column-major)   (cp_mttkrp)."""
+    _check_Z(Z, dims)
+    R = next(a for k, a in enumerate(A) if k != mode).shape[1]
+    for k, a in enumerate(A):
+        if k != mode:
+            _check_cm(a, dims[k], R, f"A[{k}]")
+    M = empty_factor(dims[mode], R, Z.device) if M is None else M
+    _check_cm(M, dims[mode], R, "M")
+    ws = _ws(ws, dims, R, Z.device)
+    _check(lib().cp_mttkrp(ctypes.byref(_shape(dims, R)), _ptr(Z),
+                           _ptr_array([a if k != mode else None for k, a in enumerate(A)]),
+                           ctypes.c_int32(mode), _ptr(M), _ptr(ws.buf), ctypes.c_size_t(ws.nbytes),
+                           _stream(stream)), "cp_mttkrp")
+    return M
+
+
+def als_sweep(Z, dims, A, normZ2, F=None, out=None, ws=None, stream=None):
+    """One ALS/BNGS sweep, A updated in place.  Returns the device tensor
+    out = [f, f_tilde, status, failed_mode]   (cp_als_sweep)."""
+    _check_Z(Z, dims)
+    R = A[0].shape[1]
+    for k, a in enumerate(A):
+        _check_cm(a, dims[k], R, f"A[{k}]")
+    Fp = None
+    if F is not None:
+        for k, f in enumerate(F):
+            if f is not None:
+                _check_cm(f, dims[k], R, f"F[{k}]")
+        Fp = _ptr_array(list(F))
+    out = torch.empty(4, dtype=torch.float64, device=Z.device) if out is None else out
+    ws = _ws(ws, dims, R, Z.device)
+    _check(lib().cp_als_sweep(ctypes.byref(_shape(dims, R)), _ptr(Z), _ptr(normZ2), _ptr_array(A),
+                              Fp, _ptr(out), _ptr(ws.buf), ctypes.c_size_t(ws.nbytes),
+                              _stream(stream)), "cp_als_sweep")
+    return out
+
+
+def mode_product(Z, dims, mode, U, X=None, stream=None):
+    """X = Z x_mode U with U (J x I_mode, column-major).  Returns (X, new dims)."""
+    _check_Z(Z, dims)
+    J = U.shape[0]
+    _check_cm(U, J, dims[mode], "U")
+    nd = list(dims)
+    nd[mode] = J
+    if X is None:
+        X = torch.empty(tuple(reversed(nd)), dtype=torch.float64, device=Z.device)
+    _check_Z(X, nd)
+    d = (ctypes.c_int64 * len(dims))(*[int(x) for x in dims])
+    _check(lib().cp_mode_product(ctypes.c_int32(len(dims)), d, _ptr(Z), ctypes.c_int32(mode),
+                                 _ptr(U), ctypes.c_int64(J), _ptr(X), ctypes.c_void_p(),
+                                 ctypes.c_size_t(0), _stream(stream)), "cp_mode_product")
+    return X, nd
+
+
+def fit(Z, dims, A, normZ2, F=None, want_G=False, out=None, ws=None, stream=None):
+    """f (direct), g and ||G^(n)||^2 at one iterate (cp_fit).  Returns (out, G list or None)."""
+    _check_Z(Z, dims)
+    N = len(dims)
+    R = A[0].shape[1]
+    for k, a in enumerate(A):
+        _check_cm(a, dims[k], R, f"A[{k}]")
+    Fp = None
+    if F is not None:
+        for k, f in enumerate(F):
+            if f is not None:
+                _check_cm(f, dims[k], R, f"F[{k}]")
+        Fp = _ptr_array(list(F))
+    G = [empty_factor(dims[k], R, Z.device) for k in range(N)] if want_G else None
+    out = torch.empty(2 + N, dtype=torch.float64, device=Z.device) if out is None else out
+    ws = _ws(ws, dims, R, Z.device)
+    _check(lib().cp_fit(ctypes.byref(_shape(dims, R)), _ptr(Z), _ptr(normZ2), _ptr_array(A), Fp,
+                        _ptr(out), _ptr_array(G) if G else None, _ptr(ws.buf),
+                        ctypes.c_size_t(ws.nbytes), _stream(stream)), "cp_fit")
+    return out, G

@@ -1,0 +1,60 @@
+"""Loader of lib/libcp.so.  No fallback: a missing library or a failed load raises."""
+import ctypes
+import os
+
+CP_MAX_N = 8
+CP_MAX_R = 32
+CP_OK, CP_EINVAL, CP_EDIM, CP_ENOTSPD, CP_ECUDA, CP_EWORKSPACE = 0, -1, -2, -3, -4, -5
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "lib", "libcp.so")
+_lib = None
+
+# every symbol include/cp.h declares (checked by tests/test_capi_symbols.py)
+EXPORTS = ["cp_workspace_bytes", "cp_norm2", "cp_mttkrp", "cp_als_sweep",
+           "cp_mode_product_workspace_bytes", "cp_mode_product", "cp_fit",
+           "cp_last_launch_count", "cp_status_string", "cp_version"]
+
+
+class CPError(RuntimeError):
+    def __init__(self, code, what=""):
+        self.code = code
+        msg = _status(code)
+        super().__init__(f"{what}: {msg} ({code})" if what else f"{msg} ({code})")
+
+
+def _status(code):
+    try:
+        return lib().cp_status_string(int(code)).decode()
+    except Exception:
+        return "status"
+
+
+def lib_path():
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            raise ImportError(f"libcp.so not built ({_LIB}); run `python -m paper_1111_6091_b200.build` "
+                              "or __graft_entry__.build() -- there is no CPU fallback")
+        L = ctypes.CDLL(_LIB)
+        vp, sz, i32, i64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32, ctypes.c_int64
+        L.cp_workspace_bytes.argtypes = [vp]
+        L.cp_workspace_bytes.restype = sz
+        L.cp_norm2.argtypes = [vp, vp, vp, vp, sz, vp]
+        L.cp_mttkrp.argtypes = [vp, vp, vp, i32, vp, vp, sz, vp]
+        L.cp_als_sweep.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.cp_mode_product_workspace_bytes.argtypes = [i32, vp, i32, i64]
+        L.cp_mode_product_workspace_bytes.restype = sz
+        L.cp_mode_product.argtypes = [i32, vp, vp, i32, vp, i64, vp, vp, sz, vp]
+        L.cp_fit.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        for f in ["cp_norm2", "cp_mttkrp", "cp_als_sweep", "cp_mode_product", "cp_fit",
+                  "cp_last_launch_count", "cp_version"]:
+            getattr(L, f).restype = ctypes.c_int
+        L.cp_status_string.argtypes = [ctypes.c_int]
+        L.cp_status_string.restype = ctypes.c_char_p
+        _lib = L
+    return _lib

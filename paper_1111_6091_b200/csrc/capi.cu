@@ -1,0 +1,498 @@
+// capi.cu -- the C ABI of libcp.so (include/cp.h): argument validation, workspace layout,
+// launch plans and the launch sequences of cp_mttkrp / cp_als_sweep / cp_fit / cp_norm2 /
+// cp_mode_product.  Every numeric step runs in the CUDA kernels of this directory.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "small_kernels.cuh"
+#include "stream_kernel.cuh"
+
+namespace cpk {
+cudaError_t launch_mode_product(int N, const int64_t *dims, const double *Z, int mode,
+                                const double *U, int64_t J, double *X, cudaStream_t st);
+int mode_product_launch_count(int N, const int64_t *dims, int mode);
+
+static thread_local int g_launches = 0;
+
+// ---------------------------------------------------------------- kernel table
+static StreamEntry g_table[kStreamTableSize];
+static int g_occ[kStreamTableSize];  // resident CTAs / SM at the configured smem (0 = unknown)
+static std::once_flag g_table_once;
+
+const StreamEntry &stream_entry(int R, int V, int op) {
+  std::call_once(g_table_once, [] {
+    register_stream_part0(g_table);
+    register_stream_part1(g_table);
+    register_stream_part2(g_table);
+    register_stream_part3(g_table);
+  });
+  return g_table[stream_index(R, V, op)];
+}
+
+static int device_sms() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+    return 148;
+  return sms;
+}
+
+static int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+static int stream_occupancy(int R, int V, int op, int smem) {
+  const StreamEntry &e = stream_entry(R, V, op);
+  int n = 0;
+  if (cudaFuncSetAttribute(e.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, e.kernel, kStreamThreads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  return n > 0 ? n : 1;
+}
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms) {
+  memset(&p, 0, sizeof(p));
+  p.N = s.N;
+  p.R = s.R;
+  p.op = op;
+  p.mode = (op == OP_RESID) ? 0 : mode;
+  int64_t P = 1;
+  for (int k = 0; k < s.N; ++k) {
+    p.dims[k] = s.dims[k];
+    P *= s.dims[k];
+  }
+  p.I1 = s.dims[0];
+  p.Q = P / p.I1;
+  p.V = (p.I1 % 2 == 0) ? 2 : 1;
+  const int maxW = (p.V == 2) ? kMaxRows : kMaxRows / 2;
+  // row-block width: mode 0 MTTKRP uses narrower blocks (fewer column groups -> smaller I1 x R
+  // partials); every other pass keeps whole columns in one CTA.
+  int64_t Wt = p.I1;
+  if (op == OP_MTTKRP && p.mode == 0) {
+    const int w0 = env_int("CP_MTTKRP_W0", 128);
+    if (p.I1 >= 2 * w0) Wt = w0;
+  }
+  if (Wt > maxW) Wt = maxW;
+  p.RB = (int)ceil_div(p.I1, Wt);
+  int64_t W = ceil_div(p.I1, p.RB);
+  if (p.V == 2 && (W & 1)) ++W;
+  p.Wmax = (int)W;
+  if (p.mode == 0) {
+    p.In = 1;
+    p.Qn = p.Q;
+    p.L = p.Q;
+  } else {
+    p.In = s.dims[mode];
+    p.Qn = p.Q / p.In;
+    int64_t L = 1;
+    for (int k = 1; k < mode; ++k) L *= s.dims[k];
+    p.L = L;
+  }
+  const int U = p.Wmax / p.V;
+  const int cpt = (kConsumers / U) > 0 ? (kConsumers / U) : 1;
+  const int stage_target = env_int("CP_STAGE_BYTES", 16384);
+  int cps = stage_target / (p.Wmax * 8);
+  if (cps < 1) cps = 1;
+  if (cps >= cpt) cps = (cps / cpt) * cpt;
+  else cps = cpt;
+  if (cps > 64) cps = 64;
+  if (cps > p.Q) cps = (int)p.Q;
+  p.cps = cps;
+  const int WSTR = (s.R % 2 == 0) ? s.R + 2 : s.R + 1;
+  const int stage_doubles = cps * p.Wmax + cps * WSTR;
+  int nst = env_int("CP_RING_BYTES", 96 * 1024) / (stage_doubles * 8);
+  if (nst < 2) nst = 2;
+  if (nst > 8) nst = 8;
+  // mode-0 slot reduction reuses the Z ring: it must hold Wmax x R doubles
+  while ((int64_t)nst * cps * p.Wmax < (int64_t)p.Wmax * s.R) ++nst;
+  p.nstages = nst;
+  p.smem_bytes = (nst * stage_doubles + kConsumerWarps * s.R + 8) * 8 + nst * 16 + nst * 16 + 64;
+  if (p.smem_bytes > 200 * 1024) return false;
+  const int occ = stream_occupancy(s.R, p.V, op, p.smem_bytes);
+  const int ctas = env_int("CP_CTAS_PER_SM", 0);
+  const int64_t Gtot = (int64_t)num_sms * (ctas > 0 ? (ctas < occ ? ctas : occ) : occ);
+  int64_t Gc = Gtot / p.RB;
+  if (Gc < 1) Gc = 1;
+  const int64_t maxGc = ceil_div(p.Q, cps);
+  if (Gc > maxGc) Gc = maxGc;
+  if (Gc > p.Q) Gc = p.Q;
+  p.Gc = (int)Gc;
+  if (p.mode == 0) {
+    p.slots = 1;
+  } else {
+    const int64_t maxrange = ceil_div(p.Q, Gc);
+    p.slots = (int)(maxrange / p.Qn + 2);
+  }
+  return true;
+}
+
+size_t stream_part_doubles(const StreamPlan &p) {
+  if (p.op == OP_RESID) return (size_t)p.Gc * p.RB;
+  if (p.mode == 0) return (size_t)p.Gc * p.I1 * p.R;
+  return (size_t)p.Gc * p.RB * p.slots * p.R;
+}
+
+cudaError_t launch_stream(const StreamPlan &p, cudaStream_t st) {
+  const StreamEntry &e = stream_entry(p.R, p.V, p.op);
+  ++g_launches;
+  return e.launch(p, st);
+}
+
+// ---------------------------------------------------------------- workspace layout
+struct Layout {
+  size_t status, Ups, gpart0, gpart1, dotM, dotF, gradp, normp, residp, part, At[CP_MAX_N], total;
+  int rpc, gp_max, grad_max, norm_blocks;
+  int nsolve[CP_MAX_N], ngrad[CP_MAX_N];
+  StreamPlan plans[CP_MAX_N];
+  StreamPlan resid;
+};
+
+static size_t align_up(size_t x) { return (x + 31) & ~(size_t)31; }  // 256 B in doubles
+
+static bool make_layout(Layout &L, const cp_shape &s) {
+  memset(&L, 0, sizeof(L));
+  const int sms = device_sms();
+  const int R = s.R;
+  L.rpc = 256 / R > 0 ? 256 / R : 1;
+  size_t part = 0;
+  for (int n = 0; n < s.N; ++n) {
+    if (!make_stream_plan(L.plans[n], s, n, OP_MTTKRP, sms)) return false;
+    const size_t d = stream_part_doubles(L.plans[n]);
+    if (d > part) part = d;
+    L.nsolve[n] = (int)ceil_div(s.dims[n], L.rpc);
+    if (L.nsolve[n] > L.gp_max) L.gp_max = L.nsolve[n];
+    L.ngrad[n] = (int)ceil_div(s.dims[n] * R, 256);
+    if (L.ngrad[n] > L.grad_max) L.grad_max = L.ngrad[n];
+  }
+  if (!make_stream_plan(L.resid, s, 0, OP_RESID, sms)) return false;
+  L.norm_blocks = 2 * sms;
+  size_t off = 0;
+  L.status = off; off = align_up(off + 8);
+  L.Ups = off; off = align_up(off + (size_t)s.N * R * R);
+  L.gpart0 = off; off = align_up(off + (size_t)L.gp_max * R * R);
+  L.gpart1 = off; off = align_up(off + (size_t)L.gp_max * R * R);
+  L.dotM = off; off = align_up(off + L.gp_max);
+  L.dotF = off; off = align_up(off + (size_t)s.N * L.gp_max);
+  L.gradp = off; off = align_up(off + (size_t)s.N * L.grad_max);
+  L.normp = off; off = align_up(off + L.norm_blocks);
+  L.residp = off; off = align_up(off + stream_part_doubles(L.resid));
+  for (int k = 0; k < s.N; ++k) {
+    L.At[k] = off;
+    off = align_up(off + (size_t)s.dims[k] * R);
+  }
+  L.part = off; off = align_up(off + part);
+  L.total = off * sizeof(double);
+  return true;
+}
+
+static int check_shape(const cp_shape *s, int minN) {
+  if (s == nullptr) return CP_EINVAL;
+  if (s->N < minN || s->N > CP_MAX_N || s->R < 1 || s->R > CP_MAX_R) return CP_EINVAL;
+  double P = 1.0;
+  for (int k = 0; k < s->N; ++k) {
+    if (s->dims[k] < 1) return CP_EDIM;
+    P *= (double)s->dims[k];
+  }
+  if (P >= 1125899906842624.0) return CP_EDIM;  // 2^50 elements
+  return CP_OK;
+}
+
+static bool aligned(const void *p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+static int check_ws(const Layout &L, void *ws, size_t ws_bytes) {
+  if (ws == nullptr || !aligned(ws, 256)) return CP_EINVAL;
+  if (ws_bytes < L.total) return CP_EWORKSPACE;
+  return CP_OK;
+}
+
+static int ret_cuda(cudaError_t e) { return e == cudaSuccess ? CP_OK : CP_ECUDA; }
+
+#define CK_LAUNCH()                                  \
+  do {                                               \
+    cudaError_t _e = cudaGetLastError();             \
+    if (_e != cudaSuccess) return CP_ECUDA;          \
+  } while (0)
+
+}  // namespace cpk
+
+using namespace cpk;
+
+extern "C" {
+
+size_t cp_workspace_bytes(const cp_shape *s) {
+  if (check_shape(s, 1) != CP_OK) return 0;
+  if (s->N < 2) {
+    // cp_norm2 only needs its block partials
+    return (size_t)(2 * device_sms() + 64) * sizeof(double);
+  }
+  Layout L;
+  if (!make_layout(L, *s)) return 0;
+  return L.total;
+}
+
+int cp_norm2(const cp_shape *s, const double *Z, double *out, void *ws, size_t ws_bytes,
+             cp_stream_t stream) {
+  g_launches = 0;
+  int st = check_shape(s, 1);
+  if (st) return st;
+  if (!Z || !out || !aligned(Z, 16)) return CP_EINVAL;
+  const size_t need = cp_workspace_bytes(s);
+  if (ws == nullptr || !aligned(ws, 256)) return CP_EINVAL;
+  if (ws_bytes < need) return CP_EWORKSPACE;
+  int64_t P = 1;
+  for (int k = 0; k < s->N; ++k) P *= s->dims[k];
+  const int nb = 2 * device_sms();
+  double *part = static_cast<double *>(ws);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  norm2_kernel<<<nb, 512, 0, cs>>>(Z, P, part);
+  CK_LAUNCH();
+  norm2_final_kernel<<<1, 32, 0, cs>>>(part, nb, out);
+  CK_LAUNCH();
+  g_launches = 2;
+  return CP_OK;
+}
+
+int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_t mode, double *M,
+              void *ws, size_t ws_bytes, cp_stream_t stream) {
+  g_launches = 0;
+  int st = check_shape(s, 2);
+  if (st) return st;
+  if (!Z || !A || !M || mode < 0 || mode >= s->N || !aligned(Z, 16)) return CP_EINVAL;
+  for (int k = 0; k < s->N; ++k)
+    if (k != mode && A[k] == nullptr) return CP_EINVAL;
+  Layout L;
+  if (!make_layout(L, *s)) return CP_EINVAL;
+  if ((st = check_ws(L, ws, ws_bytes))) return st;
+  double *w = static_cast<double *>(ws);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  PrepArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  pa.N = s->N;
+  pa.R = s->R;
+  for (int k = 0; k < s->N; ++k) {
+    pa.dims[k] = s->dims[k];
+    pa.A[k] = (k == mode) ? nullptr : A[k];
+    pa.At[k] = w + L.At[k];
+  }
+  prep_kernel<<<s->N, 256, 0, cs>>>(pa);
+  CK_LAUNCH();
+  StreamPlan p = L.plans[mode];
+  p.Z = Z;
+  for (int k = 0; k < s->N; ++k) p.At[k] = w + L.At[k];
+  p.part = w + L.part;
+  if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
+  const ReduceGeom g = reduce_geom(p);
+  const int64_t n = s->dims[mode] * s->R;
+  reduce_mttkrp_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, cs>>>(g, M);
+  CK_LAUNCH();
+  g_launches = 3;
+  return CP_OK;
+}
+
+int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
+                 const double *const *F, double *out, void *ws, size_t ws_bytes,
+                 cp_stream_t stream) {
+  g_launches = 0;
+  int st = check_shape(s, 2);
+  if (st) return st;
+  if (!Z || !normZ2 || !A || !out || !aligned(Z, 16)) return CP_EINVAL;
+  for (int k = 0; k < s->N; ++k)
+    if (A[k] == nullptr) return CP_EINVAL;
+  Layout L;
+  if (!make_layout(L, *s)) return CP_EINVAL;
+  if ((st = check_ws(L, ws, ws_bytes))) return st;
+  double *w = static_cast<double *>(ws);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  const int N = s->N, R = s->R;
+
+  PrepArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  pa.N = N;
+  pa.R = R;
+  for (int k = 0; k < N; ++k) {
+    pa.dims[k] = s->dims[k];
+    pa.A[k] = A[k];
+    pa.At[k] = w + L.At[k];
+  }
+  pa.Ups = w + L.Ups;
+  pa.status = w + L.status;
+  prep_kernel<<<N, 256, 0, cs>>>(pa);
+  CK_LAUNCH();
+  int launches = 1;
+  double *gp[2] = {w + L.gpart0, w + L.gpart1};
+  for (int n = 0; n < N; ++n) {
+    StreamPlan p = L.plans[n];
+    p.Z = Z;
+    for (int k = 0; k < N; ++k) p.At[k] = w + L.At[k];
+    p.part = w + L.part;
+    if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
+    SolveArgs sa;
+    memset(&sa, 0, sizeof(sa));
+    sa.N = N;
+    sa.R = R;
+    sa.mode = n;
+    sa.prev_mode = n - 1;
+    sa.nprev = (n > 0) ? L.nsolve[n - 1] : 0;
+    sa.rpc = L.rpc;
+    sa.In = s->dims[n];
+    sa.rg = reduce_geom(p);
+    sa.F = (F != nullptr) ? F[n] : nullptr;
+    sa.A = A[n];
+    sa.At = w + L.At[n];
+    sa.Ups = w + L.Ups;
+    sa.gprev = (n > 0) ? gp[(n - 1) & 1] : nullptr;
+    sa.gcur = gp[n & 1];
+    sa.dotM = w + L.dotM;
+    sa.dotF = w + L.dotF + (size_t)n * L.gp_max;
+    sa.status = w + L.status;
+    solve_kernel<<<L.nsolve[n], 256, 0, cs>>>(sa);
+    CK_LAUNCH();
+    launches += 2;
+  }
+  FinalizeArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.N = N;
+  fa.R = R;
+  fa.nlast = L.nsolve[N - 1];
+  fa.dot_stride = L.gp_max;
+  for (int n = 0; n < N; ++n) fa.nsolve[n] = L.nsolve[n];
+  fa.glast = gp[(N - 1) & 1];
+  fa.dotM_last = w + L.dotM;
+  fa.dotF = w + L.dotF;
+  fa.Ups = w + L.Ups;
+  fa.normZ2 = normZ2;
+  fa.status = w + L.status;
+  fa.out = out;
+  finalize_sweep_kernel<<<1, 256, 0, cs>>>(fa);
+  CK_LAUNCH();
+  g_launches = launches + 1;
+  return CP_OK;
+}
+
+size_t cp_mode_product_workspace_bytes(int32_t N, const int64_t *dims, int32_t mode, int64_t J) {
+  (void)N; (void)dims; (void)mode; (void)J;
+  return 0;
+}
+
+int cp_mode_product(int32_t N, const int64_t *dims, const double *Z, int32_t mode, const double *U,
+                    int64_t J, double *X, void *ws, size_t ws_bytes, cp_stream_t stream) {
+  g_launches = 0;
+  (void)ws; (void)ws_bytes;
+  if (N < 1 || N > CP_MAX_N || dims == nullptr || mode < 0 || mode >= N || J < 1) return CP_EINVAL;
+  if (!Z || !U || !X) return CP_EINVAL;
+  double P = 1.0, PX = 1.0;
+  for (int k = 0; k < N; ++k) {
+    if (dims[k] < 1) return CP_EDIM;
+    P *= (double)dims[k];
+    PX *= (double)(k == mode ? J : dims[k]);
+  }
+  if (P >= 1125899906842624.0 || PX >= 1125899906842624.0) return CP_EDIM;
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  const cudaError_t e = launch_mode_product(N, dims, Z, mode, U, J, X, cs);
+  if (e != cudaSuccess) return e == cudaErrorInvalidConfiguration ? CP_EDIM : CP_ECUDA;
+  g_launches = mode_product_launch_count(N, dims, mode);
+  return CP_OK;
+}
+
+int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const double *const *A,
+           const double *const *F, double *out, double *const *G, void *ws, size_t ws_bytes,
+           cp_stream_t stream) {
+  g_launches = 0;
+  int st = check_shape(s, 2);
+  if (st) return st;
+  if (!Z || !normZ2 || !A || !out || !aligned(Z, 16)) return CP_EINVAL;
+  for (int k = 0; k < s->N; ++k)
+    if (A[k] == nullptr) return CP_EINVAL;
+  Layout L;
+  if (!make_layout(L, *s)) return CP_EINVAL;
+  if ((st = check_ws(L, ws, ws_bytes))) return st;
+  double *w = static_cast<double *>(ws);
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+  const int N = s->N, R = s->R;
+  PrepArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  pa.N = N;
+  pa.R = R;
+  for (int k = 0; k < N; ++k) {
+    pa.dims[k] = s->dims[k];
+    pa.A[k] = A[k];
+    pa.At[k] = w + L.At[k];
+  }
+  pa.Ups = w + L.Ups;
+  pa.status = nullptr;
+  prep_kernel<<<N, 256, 0, cs>>>(pa);
+  CK_LAUNCH();
+  int launches = 1;
+  // residual pass 1/2 ||Z - [[A]]||^2 (eq:CPfunctional): one partial per CTA
+  StreamPlan rp = L.resid;
+  rp.Z = Z;
+  for (int k = 0; k < N; ++k) rp.At[k] = w + L.At[k];
+  rp.part = w + L.residp;
+  if (launch_stream(rp, cs) != cudaSuccess) return CP_ECUDA;
+  ++launches;
+  for (int n = 0; n < N; ++n) {
+    StreamPlan p = L.plans[n];
+    p.Z = Z;
+    for (int k = 0; k < N; ++k) p.At[k] = w + L.At[k];
+    p.part = w + L.part;
+    if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
+    GradArgs ga;
+    memset(&ga, 0, sizeof(ga));
+    ga.N = N;
+    ga.R = R;
+    ga.mode = n;
+    ga.In = s->dims[n];
+    ga.rg = reduce_geom(p);
+    ga.A = A[n];
+    ga.F = (F != nullptr) ? F[n] : nullptr;
+    ga.Ups = w + L.Ups;
+    ga.G = (G != nullptr) ? G[n] : nullptr;
+    ga.gpart = w + L.gradp + (size_t)n * L.grad_max;
+    gradient_kernel<<<L.ngrad[n], 256, 0, cs>>>(ga);
+    CK_LAUNCH();
+    launches += 2;
+  }
+  FitFinalArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.N = N;
+  fa.nresid = rp.Gc * rp.RB;
+  fa.gstride = L.grad_max;
+  for (int n = 0; n < N; ++n) fa.ngrad[n] = L.ngrad[n];
+  fa.resid = rp.part;
+  fa.gpart = w + L.gradp;
+  fa.normZ2 = normZ2;
+  fa.out = out;
+  finalize_fit_kernel<<<1, 32, 0, cs>>>(fa);
+  CK_LAUNCH();
+  g_launches = launches + 1;
+  return CP_OK;
+}
+
+int cp_last_launch_count(void) { return g_launches; }
+
+const char *cp_status_string(int code) {
+  switch (code) {
+    case CP_OK: return "ok";
+    case CP_EINVAL: return "invalid argument";
+    case CP_EDIM: return "invalid dimension";
+    case CP_ENOTSPD: return "Gamma not positive definite (Cholesky pivot <= 0)";
+    case CP_ECUDA: return "CUDA launch failure";
+    case CP_EWORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+int cp_version(void) { return CP_VERSION; }
+
+}  // extern "C"

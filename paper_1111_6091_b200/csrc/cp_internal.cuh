@@ -1,0 +1,111 @@
+// cp_internal.cuh -- shared device helpers and launch plans of libcp.so (sm_100a).
+// Product code: nothing here is shared with, or derived from, oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/cp.h"
+
+namespace cpk {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;   // 256 consumer threads
+constexpr int kStreamThreads = kConsumers + 32;   // + 1 producer warp
+constexpr int kMaxRows = 512;                     // widest row block (V = 2: 2 rows / thread)
+
+enum StreamOp { OP_MTTKRP = 0, OP_RESID = 1 };
+
+// Plan of one streaming pass over Z (MTTKRP of one mode, or the residual pass of cp_fit).
+// Z is viewed as an I1 x Q column-major matrix (Q = P / I1 "columns" = mode-1 fibers).
+// Column groups: CTA (c, rb) streams virtual columns [v0(c), v1(c)) restricted to row block
+// rb.  For mode m >= 1 the virtual order puts i_m outermost, so that a contiguous v-range
+// touches few output rows ("segments" of Qn columns each).
+struct StreamPlan {
+  int N, R, mode, op;
+  int V;            // 2: rows in pairs (I1 even, 16-B bulk copies);  1: scalar fallback
+  int Wmax;         // row-block width (even when V = 2)
+  int RB;           // number of row blocks
+  int Gc;           // number of column groups
+  int cps;          // columns per pipeline stage
+  int nstages;      // pipeline depth
+  int slots;        // mode >= 1: output segments a column group can touch
+  int smem_bytes;
+  int64_t dims[CP_MAX_N];
+  int64_t I1, Q;    // rows and columns of the mode-1 view
+  int64_t Qn;       // columns per segment (mode >= 1); Q for mode 0 / residual
+  int64_t L;        // contiguous run length in q for one segment (prod_{0<k<m} I_k); Q for mode 0
+  int64_t In;       // I_mode (segments); 1 for mode 0 / residual
+  const double *Z;
+  const double *At[CP_MAX_N];   // row-major (I_k x R) copies of the factors
+  double *part;     // partial outputs (workspace)
+};
+
+// Kernel table: one entry per (R, V, op) instantiation of stream_kernel.
+struct StreamEntry {
+  cudaError_t (*launch)(const StreamPlan &, cudaStream_t);
+  const void *kernel;
+};
+constexpr int stream_index(int R, int V, int op) { return (R * 2 + (V - 1)) * 2 + op; }
+constexpr int kStreamTableSize = stream_index(CP_MAX_R, 2, 1) + 1;
+void register_stream_part0(StreamEntry *t);
+void register_stream_part1(StreamEntry *t);
+void register_stream_part2(StreamEntry *t);
+void register_stream_part3(StreamEntry *t);
+const StreamEntry &stream_entry(int R, int V, int op);
+
+// Host: build the plan (geometry only; pointers filled by the caller).
+bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms);
+size_t stream_part_doubles(const StreamPlan &p);
+cudaError_t launch_stream(const StreamPlan &p, cudaStream_t st);
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Bounded wait: a pipeline bug must fail loudly (trap -> cudaErrorLaunchFailure) instead of
+// hanging the GPU.  ~30 s at 2 GHz is far beyond any legitimate wait.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > 60000000000LL) __trap();
+  }
+}
+// TMA bulk copy global -> shared (async proxy), completion via mbarrier transaction bytes.
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+}  // namespace cpk

@@ -1,0 +1,159 @@
+// mode_product.cu -- n-mode product X = Z x_n U, the restriction Z x_n Phat^T that
+// builds coarse-level tensors (eq:ctensor_transformed P:176-180, Alg. 1 step 7 P:273) and the
+// interpolation Phat A_c (eq:CGC P:191).  As matrices, X_(n) = U Z_(n); with Z stored mode-1
+// fastest this is a strided batched GEMM over the trailing modes:
+//   mode 0:      X (J x Q)            = U (J x I1)  * Z (I1 x Q)                  batch 1
+//   mode n > 0:  X_b (left x J)       = Z_b (left x I_n) * U^T (I_n x J)          batch b < right
+// fp64 DFMA register-tiled GEMM (64 x 64 x 16 tiles, 4 x 4 outputs per thread, register
+// prefetch of the next k-tile).  FP64 tensor cores (DMMA) are a later, measured variant.
+#include "cp_internal.cuh"
+
+namespace cpk {
+
+struct GemmArgs {
+  int64_t M, N, K, batch;
+  const double *A;
+  int64_t sam, sak, sab;
+  const double *B;
+  int64_t sbk, sbn, sbb;
+  double *C;
+  int64_t scm, scn, scb;
+  int swap;  // 1: blockIdx.x indexes n-tiles, blockIdx.y m-tiles (the larger count goes on x)
+};
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+template <bool CM_FAST>  // CM_FAST: C is contiguous along m (threads' fast index -> m)
+__global__ void __launch_bounds__(256) gemm_f64_kernel(const GemmArgs g) {
+  __shared__ double As[2][BK][BM + 1];
+  __shared__ double Bs[2][BK][BN + 1];
+  const int t = threadIdx.x;
+  const int tx = t & 15, ty = t >> 4;
+  const int64_t bm = (int64_t)(g.swap ? blockIdx.y : blockIdx.x) * BM;
+  const int64_t bn = (int64_t)(g.swap ? blockIdx.x : blockIdx.y) * BN;
+  const int64_t b = blockIdx.z;
+  const double *A = g.A + b * g.sab;
+  const double *B = g.B + b * g.sbb;
+  double *C = g.C + b * g.scb;
+  const bool a_mfast = (g.sam == 1);
+  const bool b_nfast = (g.sbn == 1);
+
+  double ra[4], rbv[4];
+  auto load_tiles = [&](int64_t k0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int mm, kk;
+      if (a_mfast) { mm = t & 63; kk = (t >> 6) + 4 * j; }
+      else { kk = t & 15; mm = (t >> 4) + 16 * j; }
+      const int64_t m = bm + mm, k = k0 + kk;
+      ra[j] = (m < g.M && k < g.K) ? __ldg(A + m * g.sam + k * g.sak) : 0.0;
+      int nn, kb;
+      if (b_nfast) { nn = t & 63; kb = (t >> 6) + 4 * j; }
+      else { kb = t & 15; nn = (t >> 4) + 16 * j; }
+      const int64_t n = bn + nn, kq = k0 + kb;
+      rbv[j] = (n < g.N && kq < g.K) ? __ldg(B + kq * g.sbk + n * g.sbn) : 0.0;
+    }
+  };
+  auto store_tiles = [&](int buf) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int mm, kk;
+      if (a_mfast) { mm = t & 63; kk = (t >> 6) + 4 * j; }
+      else { kk = t & 15; mm = (t >> 4) + 16 * j; }
+      As[buf][kk][mm] = ra[j];
+      int nn, kb;
+      if (b_nfast) { nn = t & 63; kb = (t >> 6) + 4 * j; }
+      else { kb = t & 15; nn = (t >> 4) + 16 * j; }
+      Bs[buf][kb][nn] = rbv[j];
+    }
+  };
+
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  const int mi = CM_FAST ? tx : ty;  // thread's m lane
+  const int nj = CM_FAST ? ty : tx;  // thread's n lane
+
+  load_tiles(0);
+  store_tiles(0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = 0; k0 < g.K; k0 += BK) {
+    const bool more = (k0 + BK < g.K);
+    if (more) load_tiles(k0 + BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[buf][kk][mi + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][kk][nj + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    if (more) {
+      store_tiles(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t m = bm + mi + 16 * i, n = bn + nj + 16 * j;
+      if (m < g.M && n < g.N) C[m * g.scm + n * g.scn] = acc[i][j];
+    }
+}
+
+cudaError_t launch_mode_product(int N, const int64_t *dims, const double *Z, int mode,
+                                const double *U, int64_t J, double *X, cudaStream_t st) {
+  int64_t left = 1, right = 1;
+  for (int k = 0; k < mode; ++k) left *= dims[k];
+  for (int k = mode + 1; k < N; ++k) right *= dims[k];
+  const int64_t In = dims[mode];
+  GemmArgs g;
+  if (mode == 0) {
+    // X(j, q) = sum_i U(j,i) Z(i,q)
+    g.M = J; g.N = right; g.K = In; g.batch = 1;
+    g.A = U; g.sam = 1; g.sak = J; g.sab = 0;
+    g.B = Z; g.sbk = 1; g.sbn = In; g.sbb = 0;
+    g.C = X; g.scm = 1; g.scn = J; g.scb = 0;
+  } else {
+    // X_b(a, j) = sum_i Z_b(a, i) U(j, i)
+    g.M = left; g.N = J; g.K = In; g.batch = right;
+    g.A = Z; g.sam = 1; g.sak = left; g.sab = left * In;
+    g.B = U; g.sbk = J; g.sbn = 1; g.sbb = 0;
+    g.C = X; g.scm = 1; g.scn = left; g.scb = left * J;
+  }
+  // grid.z is limited to 65535: fold large batches into chunks
+  const int64_t gx = (g.M + BM - 1) / BM, gy = (g.N + BN - 1) / BN;
+  g.swap = (gy > gx) ? 1 : 0;
+  const int64_t gbig = g.swap ? gy : gx, gsmall = g.swap ? gx : gy;
+  if (gsmall > 65535 || gbig > 0x7fffffff) return cudaErrorInvalidConfiguration;
+  for (int64_t b0 = 0; b0 < g.batch; b0 += 65535) {
+    GemmArgs gb = g;
+    gb.batch = (g.batch - b0) < 65535 ? (g.batch - b0) : 65535;
+    gb.A = g.A + b0 * g.sab;
+    gb.B = g.B + b0 * g.sbb;
+    gb.C = g.C + b0 * g.scb;
+    dim3 grid((unsigned)gbig, (unsigned)gsmall, (unsigned)gb.batch);
+    gemm_f64_kernel<true><<<grid, 256, 0, st>>>(gb);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+int mode_product_launch_count(int N, const int64_t *dims, int mode) {
+  int64_t right = 1;
+  for (int k = mode + 1; k < N; ++k) right *= dims[k];
+  if (mode == 0) right = 1;
+  return (int)((right + 65534) / 65535);
+}
+
+}  // namespace cpk

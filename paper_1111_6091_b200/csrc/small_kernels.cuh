@@ -1,0 +1,87 @@
+// small_kernels.cuh -- argument structs of the R x R / reduction kernels (small_kernels.cu).
+#pragma once
+#include "cp_internal.cuh"
+
+namespace cpk {
+
+// Where the stream kernel left its partials, and how to sum them (fixed order).
+struct ReduceGeom {
+  int R, Gc, RB, slots, mode0;  // mode0: partials are I1 x R per column group
+  int64_t I1, Q, Qn, In;  // In == 1 for mode 0
+  int64_t In_rows;        // rows of the output (I_mode)
+  const double *part;
+};
+
+inline ReduceGeom reduce_geom(const StreamPlan &p) {
+  ReduceGeom g;
+  g.R = p.R;
+  g.Gc = p.Gc;
+  g.RB = p.RB;
+  g.slots = p.slots;
+  g.mode0 = (p.mode == 0) ? 1 : 0;
+  g.I1 = p.I1;
+  g.Q = p.Q;
+  g.Qn = p.Qn;
+  g.In = p.In;
+  g.In_rows = (p.mode == 0) ? p.I1 : p.dims[p.mode];
+  g.part = p.part;
+  return g;
+}
+
+struct PrepArgs {
+  int N, R;
+  int64_t dims[CP_MAX_N];
+  const double *A[CP_MAX_N];
+  double *At[CP_MAX_N];
+  double *Ups;     // may be null (no Grams)
+  double *status;  // may be null
+};
+
+struct SolveArgs {
+  int N, R, mode, prev_mode, nprev, rpc;
+  int64_t In;
+  ReduceGeom rg;
+  const double *F;   // F^(mode) or null
+  double *A;         // A^(mode), column-major (output)
+  double *At;        // row-major copy (output)
+  double *Ups;       // N x R x R Gram totals
+  const double *gprev;  // previous mode's per-CTA partial Grams (null for mode 0)
+  double *gcur;      // this kernel's per-CTA partial Grams
+  double *dotM, *dotF;  // per-CTA <M,A>, <F,A>
+  double *status;    // [0] status, [1] failed mode
+};
+
+struct FinalizeArgs {
+  int N, R, nlast, dot_stride;
+  int nsolve[CP_MAX_N];
+  const double *glast, *dotM_last, *dotF;
+  double *Ups;
+  const double *normZ2;
+  double *status, *out;
+};
+
+struct GradArgs {
+  int N, R, mode;
+  int64_t In;
+  ReduceGeom rg;
+  const double *A, *F, *Ups;
+  double *G, *gpart;
+};
+
+struct FitFinalArgs {
+  int N, nresid, gstride;
+  int ngrad[CP_MAX_N];
+  const double *resid, *gpart, *normZ2;
+  double *out;
+};
+
+__global__ void reduce_mttkrp_kernel(const ReduceGeom g, double *M);
+__global__ void prep_kernel(const PrepArgs a);
+__global__ void solve_kernel(const SolveArgs a);
+__global__ void finalize_sweep_kernel(const FinalizeArgs a);
+__global__ void gradient_kernel(const GradArgs a);
+__global__ void finalize_fit_kernel(const FitFinalArgs a);
+__global__ void norm2_kernel(const double *__restrict__ Z, int64_t P, double *part);
+__global__ void norm2_final_kernel(const double *part, int n, double *out);
+
+}  // namespace cpk

@@ -1,0 +1,291 @@
+"""GPU parity: libcp.so (through the Python binding over the C ABI) against the CPU oracle on
+identical seeded inputs.  Tolerances (BASELINE.json north star):
+  MTTKRP and mode products: relative Frobenius error <= 1e-12 per output array;
+  factors and f after each sweep: <= 1e-10 relative (f: 1e-10*f + 1e-14*||Z||^2/2);
+  g: 1e-10*g + 1e-13.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import cpsynth
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1111_6091_b200 as cp  # noqa: E402
+from gpu_util import dev_factor, dev_tensor, host_factor, host_tensor, relerr  # noqa: E402
+
+RAGGED = [
+    ((3, 4, 2), 2),
+    ((5, 7, 3), 3),          # odd I1: scalar fallback path
+    ((2, 3, 2, 3), 3),
+    ((20, 20, 20), 3),
+    ((6, 1, 5), 1),
+    ((1, 4, 3), 2),
+    ((33, 2), 5),            # N = 2
+    ((64, 9, 7, 5, 3), 4),   # N = 5
+    ((1030, 3, 2), 7),       # I1 > 512: row blocks
+    ((1031, 2, 3), 2),       # odd and > 256: scalar row blocks
+    ((700, 5, 4), 16),       # mode-0 narrow row blocks
+    ((8, 8, 8), 32),         # R = CP_MAX_R
+    ((512, 3, 4), 16),
+    ((96, 5, 6, 7), 10),
+    ((2, 2, 2, 2, 2, 2, 2, 2), 3),  # N = CP_MAX_N
+]
+
+_cfg_cache = {}
+
+
+def config(name):
+    if name not in _cfg_cache:
+        _cfg_cache.clear()  # keep at most one config (c4a is 1 GiB) in host memory
+        _cfg_cache[name] = cpsynth.make_config(name)
+    return _cfg_cache[name]
+
+
+def dev_problem(Z, A):
+    return dev_tensor(Z), [dev_factor(a) for a in A]
+
+
+# ------------------------------------------------------------------------------- ||Z||^2
+@pytest.mark.parametrize("dims", [(3,), (7, 5), (20, 20, 20), (5, 7, 3), (1,)])
+def test_norm2(dims):
+    Z, _ = cpsynth.random_problem(dims, 1, seed=len(dims))
+    out = cp.norm2(dev_tensor(Z), dims)
+    assert relerr(host_tensor(out)[0], oracle.norm2(Z)) <= 1e-13
+
+
+# ------------------------------------------------------------------------------- MTTKRP
+@pytest.mark.parametrize("dims,R", RAGGED)
+def test_mttkrp_ragged(dims, R):
+    Z, A = cpsynth.random_problem(dims, R, seed=7 * len(dims) + R)
+    Zd, Ad = dev_problem(Z, A)
+    for n in range(len(dims)):
+        M = host_factor(cp.mttkrp(Zd, dims, Ad, n))
+        Mo = oracle.mttkrp(Z, dims, A, n)
+        assert relerr(M, Mo) <= 1e-12, (dims, R, n)
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c3"])
+def test_mttkrp_configs_full(name):
+    d = config(name)
+    dims, Z, A = d["dims"], d["Z"], d["A0"]
+    Zd, Ad = dev_problem(Z, A)
+    for n in range(len(dims)):
+        M = host_factor(cp.mttkrp(Zd, dims, Ad, n))
+        assert relerr(M, oracle.mttkrp(Z, dims, A, n)) <= 1e-12, (name, n)
+
+
+@pytest.mark.parametrize("name", ["c4a", "c4b"])
+def test_mttkrp_configs_sampled_rows(name):
+    """Full-size configs at the bench launch configuration: sampled output rows against the
+    oracle computed row by row, plus the Kruskal closed form of the noiseless part."""
+    d = config(name)
+    dims, Z, A = d["dims"], d["Z"], d["A0"]
+    Zd, Ad = dev_problem(Z, A)
+    rng = np.random.default_rng(3)
+    for n in range(len(dims)):
+        M = host_factor(cp.mttkrp(Zd, dims, Ad, n))
+        rows = sorted(set([0, dims[n] - 1] + list(rng.integers(0, dims[n], 4))))
+        for i in rows:
+            Mo = oracle.mttkrp(Z, dims, A, n, rows=(i, i + 1))
+            assert relerr(M[i], Mo[i]) <= 1e-12, (name, n, i)
+    del Zd
+
+
+def test_mttkrp_kruskal_closed_form_c4a():
+    """MTTKRP of the noiseless c4a target T = [[A*]] at full size equals
+    A*^(n) (*_{k != n} A*^(k)^T A^(k)) (eq:propKKR) -- a property at any size."""
+    _, dims, R, C, *_ = cpsynth.CONFIGS["c4a"]
+    rng = np.random.default_rng(11)
+    At = cpsynth.congruence_factors(rng, dims, R, C)
+    A = [np.asfortranarray(rng.standard_normal((I, R))) for I in dims]
+    T = cpsynth.kruskal(At)
+    Td = dev_tensor(T)
+    del T
+    Ad = [dev_factor(a) for a in A]
+    for n in range(3):
+        H = np.ones((R, R))
+        for k in range(3):
+            if k != n:
+                H *= At[k].T @ A[k]
+        M = host_factor(cp.mttkrp(Td, dims, Ad, n))
+        assert relerr(M, At[n] @ H) <= 1e-12
+
+
+# ------------------------------------------------------------------------------- sweep
+def _sweep_pair(Z, dims, A, F=None, nsweeps=1, nz2=None):
+    """Run nsweeps on both sides from the same A; yield (k, gpu A, gpu out, oracle A, oracle out)."""
+    nz2 = float(np.vdot(Z, Z)) if nz2 is None else nz2
+    Zd, Ad = dev_problem(Z, A)
+    nzd = cp.norm2(Zd, dims)
+    Fd = None if F is None else [dev_factor(f) if f is not None else None for f in F]
+    Ao = [a.copy(order="F") for a in A]
+    ws = cp.Workspace(dims, A[0].shape[1])
+    for k in range(nsweeps):
+        out = host_tensor(cp.als_sweep(Zd, dims, Ad, nzd, F=Fd, ws=ws))
+        Ao, oo = oracle.als_sweep(Z, dims, Ao, F=F, normZ2=nz2)
+        yield k, [host_factor(a) for a in Ad], out, Ao, oo
+
+
+def _check_sweep(Ag, og, Ao, oo, nz2, tol=1e-10):
+    if oo[2] != 0:  # singular Gamma (e.g. R > rank possible): both sides must report it
+        assert og[2] == oo[2] and og[3] == oo[3]
+        return
+    assert og[2] == 0
+    for a, b in zip(Ag, Ao):
+        assert relerr(a, b) <= tol
+    assert abs(og[0] - oo[0]) <= tol * abs(oo[0]) + 1e-14 * 0.5 * nz2
+    assert abs(og[1] - oo[1]) <= tol * abs(oo[1]) + 1e-14 * 0.5 * nz2
+
+
+def _well_posed(dims, R):
+    """Gamma^(n) can be nonsingular only if Phi^(n) has full column rank: R <= prod_{k!=n} I_k."""
+    P = int(np.prod(dims))
+    return all(R <= P // d for d in dims)
+
+
+@pytest.mark.parametrize("dims,R", [r for r in RAGGED if r[1] <= 16 and len(r[0]) <= 5 and _well_posed(*r)])
+def test_sweep_single_step_ragged(dims, R):
+    Z, A = cpsynth.random_problem(dims, R, seed=100 + R)
+    nz2 = float(np.vdot(Z, Z))
+    for _, Ag, og, Ao, oo in _sweep_pair(Z, dims, A, nsweeps=2, nz2=nz2):
+        _check_sweep(Ag, og, Ao, oo, nz2)
+
+
+@pytest.mark.parametrize("name,nsweeps", [("c0", 20), ("c1", 20), ("c2", 20), ("c3", 4)])
+def test_sweep_trajectory_configs(name, nsweeps):
+    d = config(name)
+    dims, Z = d["dims"], d["Z"]
+    nz2 = float(np.vdot(Z, Z))
+    for k, Ag, og, Ao, oo in _sweep_pair(Z, dims, d["A0"], nsweeps=nsweeps, nz2=nz2):
+        _check_sweep(Ag, og, Ao, oo, nz2)
+
+
+@pytest.mark.parametrize("name", ["c4a", "c4b"])
+def test_sweep_full_size_one_step(name):
+    d = config(name)
+    dims, Z = d["dims"], d["Z"]
+    nz2 = float(np.vdot(Z, Z))
+    for k, Ag, og, Ao, oo in _sweep_pair(Z, dims, d["A0"], nsweeps=1, nz2=nz2):
+        _check_sweep(Ag, og, Ao, oo, nz2)
+
+
+def test_sweep_with_rhs():
+    """BNGS with a FAS right-hand side (eq:relaxinnersolve), including NULL entries."""
+    dims, R = (12, 10, 9), 3
+    Z, A = cpsynth.random_problem(dims, R, seed=5)
+    F = [0.05 * cpsynth.random_matrix(dims[0], R, 1), None, 0.05 * cpsynth.random_matrix(dims[2], R, 2)]
+    nz2 = float(np.vdot(Z, Z))
+    for _, Ag, og, Ao, oo in _sweep_pair(Z, dims, A, F=F, nsweeps=3, nz2=nz2):
+        _check_sweep(Ag, og, Ao, oo, nz2)
+
+
+def test_sweep_singular_gamma_reports_enotspd():
+    dims, R = (6, 5, 4), 2
+    Z, A = cpsynth.random_problem(dims, R, seed=9)
+    A[1][:, 0] = 0.0
+    Zd, Ad = dev_problem(Z, A)
+    out = host_tensor(cp.als_sweep(Zd, dims, Ad, cp.norm2(Zd, dims)))
+    _, oo = oracle.als_sweep(Z, dims, A)
+    assert out[2] == cp.CP_ENOTSPD == oo[2]
+    assert out[3] == oo[3] == 0
+    assert math.isnan(out[0])
+
+
+def test_sweep_rank1_exact():
+    dims = (16, 12, 10)
+    Z, _, A0 = cpsynth.lowrank_problem(dims, 1, seed=1)
+    Zd, Ad = dev_problem(Z, A0)
+    out = host_tensor(cp.als_sweep(Zd, dims, Ad, cp.norm2(Zd, dims)))
+    X = cpsynth.kruskal([host_factor(a) for a in Ad])
+    assert relerr(X, Z) <= 1e-13
+    assert abs(out[0]) <= 1e-14 * 0.5 * float(np.vdot(Z, Z))
+
+
+def test_sweep_deterministic():
+    d = config("c2")
+    dims = d["dims"]
+    res = []
+    for _ in range(2):
+        Zd, Ad = dev_problem(d["Z"], d["A0"])
+        nzd = cp.norm2(Zd, dims)
+        for _ in range(3):
+            out = cp.als_sweep(Zd, dims, Ad, nzd)
+        res.append(([host_factor(a) for a in Ad], host_tensor(out)))
+    for a, b in zip(res[0][0], res[1][0]):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(res[0][1], res[1][1])
+
+
+# ------------------------------------------------------------------------------- mode products
+@pytest.mark.parametrize("dims,J", [((5, 4, 3), 2), ((7, 6, 5), 9), ((20, 20, 20), 10), ((3, 3, 3, 3), 4),
+                                    ((130, 70), 65), ((9,), 4), ((65, 3, 67), 33)])
+def test_mode_product_ragged(dims, J):
+    Z, _ = cpsynth.random_problem(dims, 1, seed=sum(dims))
+    Zd = dev_tensor(Z)
+    for n in range(len(dims)):
+        U = cpsynth.random_matrix(J, dims[n], seed=n + 3)
+        X, nd = cp.mode_product(Zd, dims, n, dev_factor(U))
+        Xo, ndo = oracle.mode_product(Z, dims, n, U)
+        assert nd == ndo
+        assert relerr(host_tensor(X), Xo) <= 1e-12, (dims, J, n)
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_restriction_configs(name):
+    """Restriction Z x_n Phat^T with a dense orthonormal Phat (c3: 256 x 128), every mode."""
+    d = config(name)
+    dims, Z = d["dims"], d["Z"]
+    Zd = dev_tensor(Z)
+    for n in range(len(dims)):
+        U = np.asfortranarray(d["Phat"][n].T)
+        X, nd = cp.mode_product(Zd, dims, n, dev_factor(U))
+        Xo, _ = oracle.mode_product(Z, dims, n, U)
+        assert relerr(host_tensor(X), Xo) <= 1e-12, (name, n)
+
+
+def test_interpolation_factor_matrix():
+    """Interpolation A = Phat A_c (eq:CGC) = cp_mode_product on the 2-way factor matrix."""
+    I, Ic, R = 50, 25, 3
+    Ph = cpsynth.random_matrix(I, Ic, 1)
+    Ac = cpsynth.random_matrix(Ic, R, 2)
+    X, nd = cp.mode_product(dev_tensor(np.ascontiguousarray(Ac.T)), (Ic, R), 0, dev_factor(Ph))
+    assert nd == [I, R]
+    assert relerr(host_tensor(X).T, Ph @ Ac) <= 1e-13
+
+
+# ------------------------------------------------------------------------------- fit
+@pytest.mark.parametrize("dims,R", [((5, 7, 3), 3), ((20, 20, 20), 3), ((2, 3, 2, 3), 2), ((700, 5, 4), 16),
+                                    ((33, 2), 5)])
+def test_fit_ragged(dims, R):
+    Z, A = cpsynth.random_problem(dims, R, seed=R + 50)
+    F = [0.1 * cpsynth.random_matrix(I, R, k) for k, I in enumerate(dims)]
+    for Fuse in (None, F):
+        Zd, Ad = dev_problem(Z, A)
+        Fd = None if Fuse is None else [dev_factor(f) for f in Fuse]
+        out, G = cp.fit(Zd, dims, Ad, cp.norm2(Zd, dims), F=Fd, want_G=True)
+        out = host_tensor(out)
+        oo, Go = oracle.gradient(Z, dims, A, F=Fuse)
+        assert abs(out[0] - oo[0]) <= 1e-12 * abs(oo[0]) + 1e-14 * float(np.vdot(Z, Z))
+        assert abs(out[1] - oo[1]) <= 1e-10 * abs(oo[1]) + 1e-13
+        for n in range(len(dims)):
+            assert relerr(host_factor(G[n]), Go[n]) <= 1e-11
+            assert abs(out[2 + n] - oo[2 + n]) <= 1e-10 * oo[2 + n] + 1e-24
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2"])
+def test_fit_configs(name):
+    d = config(name)
+    dims, Z, A = d["dims"], d["Z"], d["A0"]
+    Zd, Ad = dev_problem(Z, A)
+    out = host_tensor(cp.fit(Zd, dims, Ad, cp.norm2(Zd, dims))[0])
+    oo, _ = oracle.gradient(Z, dims, A, want_G=False)
+    assert abs(out[0] - oo[0]) <= 1e-12 * abs(oo[0])
+    assert abs(out[1] - oo[1]) <= 1e-10 * abs(oo[1]) + 1e-13
