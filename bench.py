@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""bench.py -- the hot path of arXiv 1111.6091 on B200: ALS sweeps/s on BASELINE.json's
+largest single-GPU config (c4a: 3-way 512^3 fp64, R = 16, 1 GiB tensor).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c4a]
+
+One step = one cp_als_sweep (per-mode MTTKRP, Gram/Hadamard,
+Cholesky solve, functional f) on the device-resident tensor.  Rows a0 (||Z||^2, once per
+tensor), a7 (restriction Z x_1 Phat^T, once per setup cycle) and a8 (cp_fit, the stopping
+test the paper excludes from its timings) are timed in the same run and reported under
+"rows".  Rank 0 prints ONE JSON line.  Multi-GPU: independent replicas (weak scaling; the
+path has no exchange step at one tensor per GPU -- DESIGN.md "Multi-GPU").
+
+--impl reference times the CPU oracle (oracle/, plain C fp64) on the same config and metric:
+each step is a bounded sample (MTTKRP of a contiguous 1/16 of the output rows of every mode,
+scaled to sweeps/s).
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import cpsynth  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4a", choices=list(cpsynth.CONFIGS))
+    ap.add_argument("--no-rows", action="store_true", help="skip the per-row extra timings")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def metric_name(workload):
+    _, dims, R, *_ = cpsynth.CONFIGS[workload]
+    shape = "x".join(str(d) for d in dims)
+    return f"ALS sweeps/s (fp64 {shape}, R={R}; MTTKRP HBM GB/s in roofline)"
+
+
+def config_block(workload, world):
+    idx, dims, R, C, l1, l2, note = cpsynth.CONFIGS[workload]
+    P = int(np.prod(dims))
+    return {"workload": workload, "desc": note, "dims": list(dims), "R": R, "congruence": C,
+            "noise_l1": l1, "noise_l2": l2, "tensor_bytes": 8 * P,
+            "step": "one cp_als_sweep (all N modes: MTTKRP + Gram/Hadamard + Cholesky solve + f)",
+            "l2_policy": ("inputs larger than L2 (no flush)" if 8 * P > 2 * 126 * 2**20
+                          else "L2 flushed (256 MiB write) between timed steps"),
+            "parallelism": f"replicas x{world}"}
+
+
+# ---------------------------------------------------------------------------- clocks (NVML)
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def report(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------- oracle timing
+def oracle_sampled_sweeps_per_s(d, min_seconds, max_steps=None, frac_den=16):
+    """Time the CPU oracle on a bounded sample: per step, MTTKRP of a contiguous 1/frac_den of
+    the output rows of every mode (each row of mode n costs the same P/I_n * R work), i.e.
+    1/frac_den of a sweep's MTTKRP work (the R x R solves, < 0.1% of it, are not timed)."""
+    import oracle
+    dims, Z, A = d["dims"], d["Z"], d["A0"]
+    t_total, sweeps, steps = 0.0, 0.0, 0
+    while True:
+        t0 = time.perf_counter()
+        frac = 0.0
+        for n in range(len(dims)):
+            nr = max(1, dims[n] // frac_den)
+            lo = (steps * nr) % max(1, dims[n] - nr + 1)
+            oracle.mttkrp(Z, dims, A, n, rows=(lo, lo + nr))
+            frac += nr / dims[n] / len(dims)
+        t_total += time.perf_counter() - t0
+        sweeps += frac
+        steps += 1
+        if (max_steps is not None and steps >= max_steps) or (max_steps is None and t_total >= min_seconds):
+            break
+    return sweeps / t_total, steps, t_total
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import oracle
+    d = cpsynth.make_config(args.workload, with_transfer=False)
+    cores = oracle.num_threads()
+    for _ in range(args.warmup):
+        oracle_sampled_sweeps_per_s(d, 0, max_steps=1)
+    val, steps, t = oracle_sampled_sweeps_per_s(d, 0, max_steps=args.steps)
+    sample = (f"oracle (plain C fp64, OpenMP over output rows) MTTKRP of a contiguous 1/16 of the "
+              f"output rows of every mode per step, {steps} steps in {t:.2f} s, scaled to sweeps/s")
+    line = {"impl": "reference", "metric": metric_name(args.workload), "value": val,
+            "unit": "sweeps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * t / steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json config recipe)",
+            "config": config_block(args.workload, 1),
+            "cpu_baseline": {"value": val, "unit": "sweeps/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1111_6091_b200 as cp
+    from paper_1111_6091_b200 import colmajor
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    d = cpsynth.make_config(args.workload)
+    dims, R = d["dims"], d["R"]
+    P = int(np.prod(dims))
+    Zh = torch.from_numpy(d["Z"]).pin_memory()
+    Zd = Zh.to(dev, non_blocking=False)
+    A0 = [torch.from_numpy(np.ascontiguousarray(a.T)).to(dev).t() for a in d["A0"]]
+    A = [colmajor(a.clone()) for a in A0]
+    for a, a0 in zip(A, A0):
+        a.copy_(a0)
+    ws = cp.Workspace(dims, R, dev)
+    nz = cp.norm2(Zd, dims, ws=ws)
+    out = torch.empty(4, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (untimed)
+    for _ in range(max(3, args.warmup)):
+        cp.als_sweep(Zd, dims, A, nz, out=out, ws=ws)
+    torch.cuda.synchronize()
+    for a, a0 in zip(A, A0):
+        a.copy_(a0)
+
+    # ---- timed region: K sweeps, device-timed with CUDA events on the launch stream
+    launches = 0
+    sampler = ClockSampler(local)
+    cp.profile_enable(True)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record(stream)
+        for _ in range(args.steps):
+            cp.als_sweep(Zd, dims, A, nz, out=out, ws=ws)
+            launches += cp.last_launch_count()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    nlaunch_prof, prof_ms, prof_bytes = cp.profile_read()
+    cp.profile_enable(False)
+    res = out.cpu().numpy()
+    if res[2] != 0 or not math.isfinite(res[0]):
+        raise SystemExit(f"sweep failed: status {res[2]} mode {res[3]} f {res[0]}")
+    t_max = ms
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = world * args.steps / (t_max / 1000.0)
+
+    # ---- roofline of the dominant kernel (the Z-streaming MTTKRP kernel)
+    peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs, STREAM copy)" if peak else "fallback (B200_PROFILING.md)"
+    peak = peak or FALLBACK_HBM
+    avg_ms = prof_ms / max(1, nlaunch_prof)
+    bytes_per_launch = prof_bytes / max(1, nlaunch_prof)
+    achieved = bytes_per_launch / (avg_ms / 1000.0) / 1e9 if nlaunch_prof else None
+    traffic = None
+    if os.path.exists(TRAFFIC_PATH):
+        tr = json.load(open(TRAFFIC_PATH)).get(args.workload)
+        if tr:
+            traffic = tr.get("dram_bytes_per_launch")
+    roofline = {"kernel": "stream_kernel (MTTKRP, all modes)", "bound": "hbm",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "peak_source": peak_src, "alg_bytes_per_launch": bytes_per_launch,
+                "avg_launch_ms": avg_ms, "launches_timed": nlaunch_prof,
+                "share_of_step": (prof_ms / ms) if ms > 0 else None,
+                "frac_of_8TBs_nominal": (achieved / 8000.0) if achieved else None}
+
+    # ---- extra rows (same run, outside the timed region)
+    rows = {}
+    if not args.no_rows:
+        rows = time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P)
+
+    # ---- e2e through the public API with host buffers
+    e2e = time_e2e(cp, torch, d, Zh, Zd, A0, A, nz, ws, dev, stream, dims, R, P, min(args.steps, 10))
+
+    line = {"metric": metric_name(args.workload), "value": value, "unit": "sweeps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json config recipe)",
+            "config": config_block(args.workload, world), "roofline": roofline,
+            "clocks": sampler.report(), "e2e": e2e, "gpu_launches": launches, "rows": rows,
+            "f_after_timed_sweeps": float(res[0])}
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        val, steps, t = oracle_sampled_sweeps_per_s(d, min_seconds=10.0)
+        line["cpu_baseline"] = {
+            "value": val, "unit": "sweeps/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": (f"oracle MTTKRP of a contiguous 1/16 of the output rows of every mode per "
+                       f"sample step, {steps} steps in {t:.1f} s on the host cores, scaled to sweeps/s "
+                       f"(R x R solves not timed)")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
+    rows = {}
+    reps = 20
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def timed(fn, n=reps):
+        fn()
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for _ in range(n):
+            fn()
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]) / n
+
+    # a1: MTTKRP per mode (cp_mttkrp: prep + stream + reduce)
+    M = [torch.empty((R, I), dtype=torch.float64, device=dev).t() for I in dims]
+    for n in range(len(dims)):
+        t = timed(lambda: cp.mttkrp(Zd, dims, A, n, M=M[n], ws=ws))
+        alg = 8.0 * (P + sum(dims[k] * R for k in range(len(dims)) if k != n) + dims[n] * R)
+        rows[f"mttkrp_mode{n}"] = {"ms": t, "alg_GBps": alg / t / 1e6}
+    # a0: ||Z||^2
+    t = timed(lambda: cp.norm2(Zd, dims, ws=ws))
+    rows["norm2"] = {"ms": t, "alg_GBps": 8.0 * P / t / 1e6}
+    # a8: cp_fit (residual pass + N MTTKRPs + gradients)
+    t = timed(lambda: cp.fit(Zd, dims, A, nz, ws=ws), n=5)
+    rows["fit"] = {"ms": t}
+    # a7: restriction Z x_1 Phat^T (dense orthonormal Phat, I_1 -> ceil(I_1/2))
+    Ph = d["Phat"][0]
+    U = torch.from_numpy(np.ascontiguousarray(Ph)).to(dev).t()  # (Ic x I1) column-major = Phat^T
+    from paper_1111_6091_b200 import colmajor
+    U = colmajor(U)
+    J = U.shape[0]
+    nd = list(dims)
+    nd[0] = J
+    X = torch.empty(tuple(reversed(nd)), dtype=torch.float64, device=dev)
+    t = timed(lambda: cp.mode_product(Zd, dims, 0, U, X=X), n=3)
+    flops = 2.0 * J * P
+    rows["restriction_mode0"] = {"ms": t, "TFLOPs": flops / t / 1e9, "J": J,
+                                 "alg_GBps": 8.0 * (P + P * J / dims[0]) / t / 1e6}
+    del X
+    return rows
+
+
+def time_e2e(cp, torch, d, Zh, Zd, A0, A, nz, ws, dev, stream, dims, R, P, K):
+    """Same metric through the public API with host buffers: every step copies the tensor and
+    the initial factors from pinned host memory, computes ||Z||^2, runs the sweep and reads f."""
+    Ah = [torch.from_numpy(np.ascontiguousarray(a.T)).pin_memory() for a in d["A0"]]
+    outh = torch.empty(4, dtype=torch.float64).pin_memory()
+    out = torch.empty(4, dtype=torch.float64, device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def step():
+        Zd.copy_(Zh, non_blocking=True)
+        for a, h in zip(A, Ah):
+            a.t().copy_(h, non_blocking=True)
+        cp.norm2(Zd, dims, out=nz, ws=ws)
+        cp.als_sweep(Zd, dims, A, nz, out=out, ws=ws)
+        outh.copy_(out, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for _ in range(K):
+        step()
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1])
+    return {"value": K / (ms / 1000.0), "unit": "sweeps/s", "steps": K,
+            "h2d_bytes_per_step": 8 * P + sum(8 * I * R for I in dims), "d2h_bytes_per_step": 32,
+            "note": "per step: H2D of Z and the factors from pinned memory, cp_norm2, cp_als_sweep, D2H of f"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

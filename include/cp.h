@@ -132,6 +132,16 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
  * benchmark's gpu_launches count). */
 int cp_last_launch_count(void);
 
+/* Live per-kernel timing for the roofline report.  While enabled, every launch of the
+ * Z-streaming kernel (the MTTKRP / residual pass that dominates the sweep) is bracketed by a
+ * pair of CUDA events recorded on the launch stream (at most 8192 pairs are kept).
+ * cp_profile_read synchronizes on the recorded events and returns, for the launches recorded
+ * since the last read: their count, the summed event durations in ms, and the summed
+ * ALGORITHMIC bytes (8P + 8R*sum_{k != n} I_k + 8 I_n R per MTTKRP launch);
+ * then it resets.  Host-side only; not thread-safe. */
+int cp_profile_enable(int enable);
+int cp_profile_read(int64_t *launches, double *total_ms, double *alg_bytes);
+
 const char *cp_status_string(int code);
 int cp_version(void);
 

@@ -123,6 +123,19 @@ def last_launch_count():
     return int(lib().cp_last_launch_count())
 
 
+def profile_enable(on=True):
+    _check(lib().cp_profile_enable(1 if on else 0), "cp_profile_enable")
+
+
+def profile_read():
+    """(launches, total_ms, algorithmic_bytes) of the streaming-kernel launches since the last read."""
+    n = ctypes.c_int64()
+    ms = ctypes.c_double()
+    b = ctypes.c_double()
+    _check(lib().cp_profile_read(ctypes.byref(n), ctypes.byref(ms), ctypes.byref(b)), "cp_profile_read")
+    return int(n.value), float(ms.value), float(b.value)
+
+
 def norm2(Z, dims, out=None, ws=None, stream=None):
     """||Z||^2 as a 1-element float64 CUDA tensor (cp_norm2)."""
     _check_Z(Z, dims)

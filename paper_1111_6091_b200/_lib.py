@@ -13,7 +13,8 @@ _lib = None
 # every symbol include/cp.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = ["cp_workspace_bytes", "cp_norm2", "cp_mttkrp", "cp_als_sweep",
            "cp_mode_product_workspace_bytes", "cp_mode_product", "cp_fit",
-           "cp_last_launch_count", "cp_status_string", "cp_version"]
+           "cp_last_launch_count", "cp_profile_enable", "cp_profile_read", "cp_status_string",
+           "cp_version"]
 
 
 class CPError(RuntimeError):
@@ -54,6 +55,10 @@ def lib():
         for f in ["cp_norm2", "cp_mttkrp", "cp_als_sweep", "cp_mode_product", "cp_fit",
                   "cp_last_launch_count", "cp_version"]:
             getattr(L, f).restype = ctypes.c_int
+        L.cp_profile_enable.argtypes = [ctypes.c_int]
+        L.cp_profile_enable.restype = ctypes.c_int
+        L.cp_profile_read.argtypes = [vp, vp, vp]
+        L.cp_profile_read.restype = ctypes.c_int
         L.cp_status_string.argtypes = [ctypes.c_int]
         L.cp_status_string.restype = ctypes.c_char_p
         _lib = L

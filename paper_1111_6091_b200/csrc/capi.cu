@@ -99,6 +99,22 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     for (int k = 1; k < mode; ++k) L *= s.dims[k];
     p.L = L;
   }
+  // v-order digits (see StreamPlan)
+  {
+    int64_t qstride[CP_MAX_N];
+    qstride[1] = 1;
+    for (int k = 2; k < s.N; ++k) qstride[k] = qstride[k - 1] * s.dims[k - 1];
+    int j = 0;
+    for (int k = 1; k < s.N; ++k)
+      if (k != p.mode) p.ord[j++] = k;
+    if (p.mode != 0) p.ord[j++] = p.mode;
+    p.nd = j;
+    for (int t = 0; t < p.nd; ++t) {
+      if (s.dims[p.ord[t]] > 0x7fffffff) return false;
+      p.rad[t] = (int)s.dims[p.ord[t]];
+      p.qsd[t] = qstride[p.ord[t]];
+    }
+  }
   const int U = p.Wmax / p.V;
   const int cpt = (kConsumers / U) > 0 ? (kConsumers / U) : 1;
   const int stage_target = env_int("CP_STAGE_BYTES", 16384);
@@ -143,10 +159,36 @@ size_t stream_part_doubles(const StreamPlan &p) {
   return (size_t)p.Gc * p.RB * p.slots * p.R;
 }
 
+// ---------------------------------------------------------------- live kernel timing
+constexpr int kProfMax = 8192;
+static bool g_prof_on = false;
+static int g_prof_n = 0;
+static cudaEvent_t g_prof_ev[2 * kProfMax];
+static double g_prof_bytes[kProfMax];
+static bool g_prof_init = false;
+
+static double stream_alg_bytes(const StreamPlan &p) {
+  double P = 1.0, fac = 0.0;
+  for (int k = 0; k < p.N; ++k) {
+    P *= (double)p.dims[k];
+    if (k != p.mode || p.op == OP_RESID) fac += (double)p.dims[k] * p.R;
+  }
+  const double out = (p.op == OP_RESID) ? 0.0 : (double)p.dims[p.mode] * p.R;
+  return 8.0 * (P + fac + out);
+}
+
 cudaError_t launch_stream(const StreamPlan &p, cudaStream_t st) {
   const StreamEntry &e = stream_entry(p.R, p.V, p.op);
   ++g_launches;
-  return e.launch(p, st);
+  const bool prof = g_prof_on && g_prof_n < kProfMax;
+  if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], st);
+  const cudaError_t err = e.launch(p, st);
+  if (prof) {
+    cudaEventRecord(g_prof_ev[2 * g_prof_n + 1], st);
+    g_prof_bytes[g_prof_n] = stream_alg_bytes(p);
+    ++g_prof_n;
+  }
+  return err;
 }
 
 // ---------------------------------------------------------------- workspace layout
@@ -480,6 +522,34 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
 }
 
 int cp_last_launch_count(void) { return g_launches; }
+
+int cp_profile_enable(int enable) {
+  if (enable && !g_prof_init) {
+    for (int i = 0; i < 2 * kProfMax; ++i)
+      if (cudaEventCreate(&g_prof_ev[i]) != cudaSuccess) return CP_ECUDA;
+    g_prof_init = true;
+  }
+  g_prof_on = enable != 0;
+  g_prof_n = 0;
+  return CP_OK;
+}
+
+int cp_profile_read(int64_t *launches, double *total_ms, double *alg_bytes) {
+  if (!launches || !total_ms || !alg_bytes) return CP_EINVAL;
+  double ms = 0.0, bytes = 0.0;
+  for (int i = 0; i < g_prof_n; ++i) {
+    float t = 0.f;
+    if (cudaEventSynchronize(g_prof_ev[2 * i + 1]) != cudaSuccess) return CP_ECUDA;
+    if (cudaEventElapsedTime(&t, g_prof_ev[2 * i], g_prof_ev[2 * i + 1]) != cudaSuccess) return CP_ECUDA;
+    ms += t;
+    bytes += g_prof_bytes[i];
+  }
+  *launches = g_prof_n;
+  *total_ms = ms;
+  *alg_bytes = bytes;
+  g_prof_n = 0;
+  return CP_OK;
+}
 
 const char *cp_status_string(int code) {
   switch (code) {

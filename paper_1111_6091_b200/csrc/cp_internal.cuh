@@ -12,6 +12,7 @@ constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;   // 256 consumer threads
 constexpr int kStreamThreads = kConsumers + 32;   // + 1 producer warp
 constexpr int kMaxRows = 512;                     // widest row block (V = 2: 2 rows / thread)
+constexpr int kMaxDigits = CP_MAX_N - 1;          // column multi-index digits (modes 1..N-1)
 
 enum StreamOp { OP_MTTKRP = 0, OP_RESID = 1 };
 
@@ -35,6 +36,13 @@ struct StreamPlan {
   int64_t Qn;       // columns per segment (mode >= 1); Q for mode 0 / residual
   int64_t L;        // contiguous run length in q for one segment (prod_{0<k<m} I_k); Q for mode 0
   int64_t In;       // I_mode (segments); 1 for mode 0 / residual
+  // v-order odometer: digit j (fastest first) is the index of mode ord[j], radix rad[j],
+  // column stride qsd[j] = prod_{1 <= k < ord[j]} I_k.  mode 0: modes 1..N-1;
+  // mode m >= 1: modes 1..m-1, m+1..N-1, then m (the segment digit).
+  int nd;
+  int ord[CP_MAX_N - 1];
+  int rad[CP_MAX_N - 1];
+  int64_t qsd[CP_MAX_N - 1];
   const double *Z;
   const double *At[CP_MAX_N];   // row-major (I_k x R) copies of the factors
   double *part;     // partial outputs (workspace)

@@ -19,21 +19,28 @@
 
 namespace cpk {
 
-__device__ __forceinline__ int64_t stream_column(const StreamPlan &p, int64_t v, int64_t *run) {
-  if (p.mode == 0) {  // mode 0 / residual: v is the column index
-    *run = p.Q - v;
-    return v;
+// v-order odometer: digit j has radix p.rad[j] and is the index of mode p.ord[j]
+// (fastest first).  add_carry adds a small non-negative c; digits_to_q maps to the column q.
+__device__ __forceinline__ void add_carry(int (&d)[kMaxDigits], int nd, const int *rad, int c) {
+#pragma unroll
+  for (int j = 0; j < kMaxDigits; ++j) {
+    if (j < nd && c != 0) {
+      const int t = d[j] + c;
+      c = t / rad[j];
+      d[j] = t - c * rad[j];
+    }
   }
-  const int64_t seg = v / p.Qn;
-  const int64_t o = v - seg * p.Qn;
-  const int64_t ihi = o / p.L;
-  const int64_t ilo = o - ihi * p.L;
-  *run = p.L - ilo;
-  return ilo + p.L * (seg + p.In * ihi);
+}
+__device__ __forceinline__ int64_t digits_to_q(const StreamPlan &p, const int (&d)[kMaxDigits]) {
+  int64_t q = 0;
+#pragma unroll
+  for (int j = 0; j < kMaxDigits; ++j)
+    if (j < p.nd) q += (int64_t)d[j] * p.qsd[j];
+  return q;
 }
 
 template <int R, int V, int OP>
-__global__ void __launch_bounds__(kStreamThreads) stream_kernel(const __grid_constant__ StreamPlan p) {
+__global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1)) stream_kernel(const __grid_constant__ StreamPlan p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int WSTR = (R % 2 == 0) ? R + 2 : R + 1;  // weight row stride (even: 16-B aligned)
   const int zst = p.cps * p.Wmax;                      // doubles per Z stage
@@ -65,71 +72,118 @@ __global__ void __launch_bounds__(kStreamThreads) stream_kernel(const __grid_con
 
   if (warp == kConsumerWarps) {
     // ============================ producer warp ============================
-    const int cpp = 32 / R;           // weight columns per pass (lanes over (col, r))
+    // Columns are visited in "v order"; the producer keeps the v-digits of the
+    // stage start in registers (an odometer over p.rad, 32-bit), so no 64-bit division runs
+    // per column.  Lane 0 issues the TMA bulk copies; all lanes form the Khatri-Rao rows.
+    const int cpp = 32 / R;  // weight columns per pass (lanes over (col, r))
     const int lc = lane / R, lr = lane - (lane / R) * R;
-    const int64_t seg_first = v0 / p.Qn;
+    const int nd = p.nd;
+    int B[kMaxDigits];
+    {
+      int64_t t = v0;
+#pragma unroll
+      for (int j = 0; j < kMaxDigits; ++j) {
+        B[j] = 0;
+        if (j < nd) {
+          B[j] = (int)(t % p.rad[j]);
+          t /= p.rad[j];
+        }
+      }
+    }
+    int64_t seg_left = p.Qn - (v0 % p.Qn);
+    int seg_slot = 0;
     int stage = 0;
     uint32_t eph = 1;
     int64_t v = v0;
     while (v < v1) {
-      const int64_t seg = v / p.Qn;
-      const int64_t vend = ((seg + 1) * p.Qn < v1) ? (seg + 1) * p.Qn : v1;
-      const int ncols = (int)((vend - v) < p.cps ? (vend - v) : p.cps);
-      const bool eos = (v + ncols == vend);
+      const int64_t lim = (seg_left < v1 - v) ? seg_left : (v1 - v);
+      const int ncols = (int)(lim < p.cps ? lim : p.cps);
       const bool last = (v + ncols == v1);
+      const bool eos = (ncols == seg_left) || last;  // a segment ends, or this CTA's range does
       mbar_wait(&empty[stage], eph);
       double *zs = zbuf + (size_t)stage * zst;
       if (V == 2) {
         if (lane == 0) {
           mbar_expect_tx(&full[stage], (uint32_t)(ncols * Wb * 8));
-          int col = 0;
-          while (col < ncols) {
-            int64_t run;
-            const int64_t q = stream_column(p, v + col, &run);
-            const int n = (int)((ncols - col) < run ? (ncols - col) : run);
-            if (p.RB == 1) {
-              bulk_g2s(zs + (size_t)col * Wb, p.Z + q * p.I1, (uint32_t)(n * Wb * 8), &full[stage]);
-            } else {
-              for (int j = 0; j < n; ++j)
-                bulk_g2s(zs + (size_t)(col + j) * Wb, p.Z + (q + j) * p.I1 + row0, (uint32_t)(Wb * 8),
-                         &full[stage]);
+          int D[kMaxDigits];
+#pragma unroll
+          for (int j = 0; j < kMaxDigits; ++j) D[j] = B[j];
+          int64_t q = digits_to_q(p, D);
+          int64_t run_q = q;
+          int run_col = 0, run_n = 1;
+          for (int col = 1; col <= ncols; ++col) {
+            int64_t q2 = -1;
+            if (col < ncols) {
+              add_carry(D, nd, p.rad, 1);
+              q2 = digits_to_q(p, D);
             }
-            col += n;
+            if (col < ncols && p.RB == 1 && q2 == q + 1) {
+              ++run_n;
+            } else {
+              bulk_g2s(zs + (size_t)run_col * Wb, p.Z + run_q * p.I1 + row0, (uint32_t)(run_n * Wb * 8),
+                       &full[stage]);
+              run_q = q2;
+              run_col = col;
+              run_n = 1;
+            }
+            q = q2;
           }
         }
       } else {
         // scalar fallback (odd I1: columns are not 16-B aligned): the warp copies elements
+        int D[kMaxDigits];
+#pragma unroll
+        for (int j = 0; j < kMaxDigits; ++j) D[j] = B[j];
         for (int col = 0; col < ncols; ++col) {
-          int64_t run;
-          const int64_t q = stream_column(p, v + col, &run);
-          const double *src = p.Z + q * p.I1 + row0;
+          if (col > 0) add_carry(D, nd, p.rad, 1);
+          const double *src = p.Z + digits_to_q(p, D) * p.I1 + row0;
           for (int i = lane; i < Wb; i += 32) zs[(size_t)col * Wb + i] = __ldg(src + i);
         }
       }
-      // Khatri-Rao rows w_q[r] = prod_{k>=1, k != mode} A^(k)(i_k, r) of this stage's columns
+      // Khatri-Rao rows w_q[r] = prod_{k>=1, k != mode} A^(k)(i_k, r) of this stage's columns,
+      // four columns per lane at a time so their factor loads are in flight together
       double *ws = wbuf + (size_t)stage * wst;
       if (lc < cpp) {
-        for (int col = lc; col < ncols; col += cpp) {
-          int64_t run;
-          int64_t t = stream_column(p, v + col, &run);
-          double w = 1.0;
-          for (int k = 1; k < p.N; ++k) {
-            const int64_t ik = t % p.dims[k];
-            t /= p.dims[k];
-            if (k != p.mode) w *= __ldg(p.At[k] + ik * R + lr);
+        for (int c0 = lc; c0 < ncols; c0 += 4 * cpp) {
+          int D[4][kMaxDigits];
+          double w[4];
+#pragma unroll
+          for (int u4 = 0; u4 < 4; ++u4) {
+#pragma unroll
+            for (int j = 0; j < kMaxDigits; ++j) D[u4][j] = B[j];
+            add_carry(D[u4], nd, p.rad, c0 + u4 * cpp);
+            w[u4] = 1.0;
           }
-          ws[col * WSTR + lr] = w;
+#pragma unroll
+          for (int j = 0; j < kMaxDigits; ++j) {
+            if (j < nd && p.ord[j] != p.mode) {
+              const double *a = p.At[p.ord[j]] + lr;
+#pragma unroll
+              for (int u4 = 0; u4 < 4; ++u4) w[u4] *= __ldg(a + D[u4][j] * R);
+            }
+          }
+#pragma unroll
+          for (int u4 = 0; u4 < 4; ++u4) {
+            const int col = c0 + u4 * cpp;
+            if (col < ncols) ws[col * WSTR + lr] = w[u4];
+          }
         }
       }
       if (lane == 0) {
         int *h = hdr + stage * 4;
         h[0] = ncols;
         h[1] = (eos ? 1 : 0) | (last ? 2 : 0);
-        h[2] = (int)(seg - seg_first);
+        h[2] = seg_slot;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[stage]);
       v += ncols;
+      add_carry(B, nd, p.rad, ncols);
+      seg_left -= ncols;
+      if (seg_left == 0) {
+        seg_left = p.Qn;
+        ++seg_slot;
+      }
       if (++stage == p.nstages) {
         stage = 0;
         eph ^= 1u;
