@@ -80,7 +80,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   // partials); every other pass keeps whole columns in one CTA.
   int64_t Wt = p.I1;
   if (op == OP_MTTKRP && p.mode == 0) {
-    const int w0 = env_int("CP_MTTKRP_W0", 128);
+    const int w0 = env_int("CP_MTTKRP_W0", 512);
     if (p.I1 >= 2 * w0) Wt = w0;
   }
   if (Wt > maxW) Wt = maxW;
@@ -126,14 +126,16 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   if (cps > p.Q) cps = (int)p.Q;
   p.cps = cps;
   const int WSTR = (s.R % 2 == 0) ? s.R + 2 : s.R + 1;
-  const int stage_doubles = cps * p.Wmax + cps * WSTR;
+  p.RS = s.R + (s.R & 1);
+  const int stage_doubles = cps * p.Wmax + cps * p.RS + cps * WSTR;
   int nst = env_int("CP_RING_BYTES", 96 * 1024) / (stage_doubles * 8);
   if (nst < 2) nst = 2;
   if (nst > 8) nst = 8;
   // mode-0 slot reduction reuses the Z ring: it must hold Wmax x R doubles
   while ((int64_t)nst * cps * p.Wmax < (int64_t)p.Wmax * s.R) ++nst;
   p.nstages = nst;
-  p.smem_bytes = (nst * stage_doubles + kConsumerWarps * s.R + 8) * 8 + nst * 16 + nst * 16 + 64;
+  // ring | red[8R+8] | sS[32] | 3 x nst mbarriers | nst x 16-int headers
+  p.smem_bytes = (nst * stage_doubles + kConsumerWarps * s.R + 8 + 32) * 8 + nst * 24 + nst * 64 + 64;
   if (p.smem_bytes > 200 * 1024) return false;
   const int occ = stream_occupancy(s.R, p.V, op, p.smem_bytes);
   const int ctas = env_int("CP_CTAS_PER_SM", 0);
@@ -231,7 +233,7 @@ static bool make_layout(Layout &L, const cp_shape &s) {
   L.residp = off; off = align_up(off + stream_part_doubles(L.resid));
   for (int k = 0; k < s.N; ++k) {
     L.At[k] = off;
-    off = align_up(off + (size_t)s.dims[k] * R);
+    off = align_up(off + (size_t)s.dims[k] * (R + (R & 1)));
   }
   L.part = off; off = align_up(off + part);
   L.total = off * sizeof(double);

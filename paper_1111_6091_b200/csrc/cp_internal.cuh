@@ -10,7 +10,7 @@ namespace cpk {
 
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;   // 256 consumer threads
-constexpr int kStreamThreads = kConsumers + 32;   // + 1 producer warp
+constexpr int kStreamThreads = kConsumers + 64;   // + TMA producer warp + weight warp
 constexpr int kMaxRows = 512;                     // widest row block (V = 2: 2 rows / thread)
 constexpr int kMaxDigits = CP_MAX_N - 1;          // column multi-index digits (modes 1..N-1)
 
@@ -31,6 +31,7 @@ struct StreamPlan {
   int nstages;      // pipeline depth
   int slots;        // mode >= 1: output segments a column group can touch
   int smem_bytes;
+  int RS;           // row stride of the row-major factor copies At (R rounded up to even)
   int64_t dims[CP_MAX_N];
   int64_t I1, Q;    // rows and columns of the mode-1 view
   int64_t Qn;       // columns per segment (mode >= 1); Q for mode 0 / residual

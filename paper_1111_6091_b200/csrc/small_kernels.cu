@@ -52,10 +52,11 @@ __global__ void prep_kernel(const PrepArgs a) {
   const double *A = a.A[k];
   if (A == nullptr) return;
   double *At = a.At[k];
-  for (int64_t e = threadIdx.x; e < I * R; e += blockDim.x) {
-    const int64_t i = e / R;
-    const int r = (int)(e - i * R);
-    At[e] = A[i + I * r];
+  const int RS = R + (R & 1);  // padded row stride (16-B aligned rows for the TMA copies)
+  for (int64_t e = threadIdx.x; e < I * RS; e += blockDim.x) {
+    const int64_t i = e / RS;
+    const int r = (int)(e - i * RS);
+    At[e] = (r < R) ? A[i + I * r] : 0.0;
   }
   if (a.Ups != nullptr) {
     for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(256) solve_kernel(const SolveArgs a) {
     double dm = 0.0, df = 0.0;
     if (lane < R) {
       a.A[i + In * lane] = b;
-      a.At[i * R + lane] = b;
+      a.At[i * (R + (R & 1)) + lane] = b;
       sX[ii * R + lane] = b;
       dm = sM[ii * R + lane] * b;
       df = (a.F != nullptr) ? a.F[i + In * lane] * b : 0.0;

@@ -3,14 +3,17 @@
 //
 // Design:
 //  * Z is viewed as an I1 x Q column-major matrix (mode-1 fibers are columns).  Every mode's
-//    MTTKRP streams Z in that order: a thread owns fixed rows i1 (2 per thread) for the whole
-//    pass and keeps R accumulators per row in registers, so the Khatri-Rao row w_q of a column
-//    is formed ONCE per column (by the producer warp, into shared memory) and broadcast to all
-//    rows of the column -- the "reuse along the fast mode" of the north star.
-//  * One producer warp feeds a ring of shared-memory stages with TMA bulk copies
-//    (cp.async.bulk + mbarrier complete_tx); 8 consumer warps do R DFMAs per element.
-//  * mode 0 (paper mode 1): the output rows are the owned rows; each column group writes
-//    an I1 x R partial, reduced in fixed order by the next kernel (no atomics).
+//    MTTKRP streams Z in that order: a consumer thread owns fixed rows i1 (2 per thread) for
+//    the whole pass and keeps R accumulators per row in registers, so the Khatri-Rao row w_q
+//    of a column is formed ONCE per column (into shared memory) and broadcast to all rows of
+//    the column -- the "reuse along the fast mode" of the north star.
+//  * Warp roles (320 threads): warp 8 = TMA producer (one elected lane issues cp.async.bulk
+//    copies of the stage's Z columns AND of the factor rows the stage's Khatri-Rao rows need);
+//    warp 9 = weight warp (forms w_q[r] = A^(k0)(i_k0, r) * S[r] from the staged rows, S the
+//    product of the slowly varying factors); warps 0-7 = consumers (R DFMAs per element).
+//    Three mbarrier rings: full (TMA bytes landed), wready (weights formed), empty (consumed).
+//  * mode 0 (paper mode 1): the output rows are the owned rows; each column group writes an
+//    I1 x R partial, reduced in a fixed order by the next kernel (no atomics).
 //  * mode m >= 1: columns are visited with i_m outermost; at the end of each i_m segment the
 //    consumers contract their accumulators with A^(1) rows and reduce across the CTA
 //    (warp shuffles + shared memory), writing one R-vector partial per (CTA, segment).
@@ -19,38 +22,183 @@
 
 namespace cpk {
 
-// v-order odometer: digit j has radix p.rad[j] and is the index of mode p.ord[j]
-// (fastest first).  add_carry adds a small non-negative c; digits_to_q maps to the column q.
-__device__ __forceinline__ void add_carry(int (&d)[kMaxDigits], int nd, const int *rad, int c) {
+constexpr int kHdrInts = 16;  // per-stage header: ncols, flags, slot, -, digits[kMaxDigits]
+
+// Shared-memory carve-up of one CTA (all offsets in doubles except the tail).
+struct StreamSmem {
+  double *zbuf, *abuf, *wbuf, *red, *sS;
+  uint64_t *full, *wready, *empty;
+  int *hdr;
+};
+
+template <int R>
+__device__ __forceinline__ StreamSmem carve(unsigned char *raw, const StreamPlan &p) {
+  constexpr int WSTR = (R % 2 == 0) ? R + 2 : R + 1;
+  StreamSmem s;
+  s.zbuf = reinterpret_cast<double *>(raw);
+  s.abuf = s.zbuf + (size_t)p.nstages * p.cps * p.Wmax;
+  s.wbuf = s.abuf + (size_t)p.nstages * p.cps * p.RS;
+  s.red = s.wbuf + (size_t)p.nstages * p.cps * WSTR;
+  s.sS = s.red + kConsumerWarps * R + 8;
+  s.full = reinterpret_cast<uint64_t *>(s.sS + 32);
+  s.wready = s.full + p.nstages;
+  s.empty = s.wready + p.nstages;
+  s.hdr = reinterpret_cast<int *>(s.empty + p.nstages);
+  return s;
+}
+
+// ------------------------------------------------------------------------ producer (warp 8)
+// Stage boundaries: a stage never crosses an i_m segment, the CTA's range end, or a wrap of
+// the fastest column digit -- so the fastest factor's rows of a stage are contiguous in At
+// (one bulk copy) and every slower digit is constant over the stage.
+template <int R, int V>
+__device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, int64_t row0, int Wb,
+                        const StreamSmem &sm) {
+  const int nd = p.nd;
+  const bool has_f0 = (p.ord[0] != p.mode);
+  const double *A0 = p.At[p.ord[0]];
+  int B[kMaxDigits];
+  {
+    int64_t t = v0;
 #pragma unroll
-  for (int j = 0; j < kMaxDigits; ++j) {
-    if (j < nd && c != 0) {
-      const int t = d[j] + c;
-      c = t / rad[j];
-      d[j] = t - c * rad[j];
+    for (int j = 0; j < kMaxDigits; ++j) {
+      B[j] = 0;
+      if (j < nd) {
+        B[j] = (int)(t % p.rad[j]);
+        t /= p.rad[j];
+      }
+    }
+  }
+  int64_t seg_left = p.Qn - (v0 % p.Qn);
+  int seg_slot = 0;
+  int stage = 0;
+  uint32_t eph = 1;
+  int64_t v = v0;
+  while (v < v1) {
+    int64_t lim = (seg_left < v1 - v) ? seg_left : (v1 - v);
+    if (lim > p.rad[0] - B[0]) lim = p.rad[0] - B[0];
+    const int ncols = (int)(lim < p.cps ? lim : p.cps);
+    const bool last = (v + ncols == v1);
+    const bool eos = (ncols == seg_left) || last;  // a segment ends, or this CTA's range does
+    int64_t q0 = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxDigits; ++j)
+      if (j < nd) q0 += (int64_t)B[j] * p.qsd[j];
+    mbar_wait(&sm.empty[stage], eph);
+    double *zs = sm.zbuf + (size_t)stage * p.cps * p.Wmax;
+    double *as = sm.abuf + (size_t)stage * p.cps * p.RS;
+    if (V == 2) {
+      if (lane == 0) {
+        mbar_expect_tx(&sm.full[stage],
+                       (uint32_t)(ncols * Wb * 8 + (has_f0 ? ncols * p.RS * 8 : 0)));
+        // Z columns: q advances by qsd[0] per column within a stage (digit 0 only)
+        if (p.RB == 1 && p.qsd[0] == 1) {
+          bulk_g2s(zs, p.Z + q0 * p.I1, (uint32_t)(ncols * Wb * 8), &sm.full[stage]);
+        } else {
+          for (int col = 0; col < ncols; ++col)
+            bulk_g2s(zs + (size_t)col * Wb, p.Z + (q0 + col * p.qsd[0]) * p.I1 + row0,
+                     (uint32_t)(Wb * 8), &sm.full[stage]);
+        }
+        if (has_f0)
+          bulk_g2s(as, A0 + (int64_t)B[0] * p.RS, (uint32_t)(ncols * p.RS * 8), &sm.full[stage]);
+      }
+    } else {
+      // scalar fallback (odd I1: columns are not 16-B aligned): the warp copies elements
+      for (int col = 0; col < ncols; ++col) {
+        const double *src = p.Z + (q0 + col * p.qsd[0]) * p.I1 + row0;
+        for (int i = lane; i < Wb; i += 32) zs[(size_t)col * Wb + i] = __ldg(src + i);
+      }
+      if (has_f0)
+        for (int e = lane; e < ncols * p.RS; e += 32) as[e] = __ldg(A0 + (int64_t)B[0] * p.RS + e);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      int *h = sm.hdr + stage * kHdrInts;
+      h[0] = ncols;
+      h[1] = (eos ? 1 : 0) | (last ? 2 : 0);
+      h[2] = seg_slot;
+#pragma unroll
+      for (int j = 0; j < kMaxDigits; ++j) h[4 + j] = B[j];
+      mbar_arrive(&sm.full[stage]);
+    }
+    // advance: digit 0 by ncols (at most to its wrap), then carry
+    v += ncols;
+    B[0] += ncols;
+#pragma unroll
+    for (int j = 0; j + 1 < kMaxDigits; ++j) {
+      if (j + 1 < nd && B[j] >= p.rad[j]) {
+        B[j] -= p.rad[j];
+        B[j + 1] += 1;
+      }
+    }
+    seg_left -= ncols;
+    if (seg_left == 0) {
+      seg_left = p.Qn;
+      ++seg_slot;
+    }
+    if (++stage == p.nstages) {
+      stage = 0;
+      eph ^= 1u;
     }
   }
 }
-__device__ __forceinline__ int64_t digits_to_q(const StreamPlan &p, const int (&d)[kMaxDigits]) {
-  int64_t q = 0;
+
+// ------------------------------------------------------------------------ weight warp (warp 9)
+// w_q[r] = A^(k0)(i_k0, r) * S[r],  S[r] = prod_{j >= 1, ord[j] != mode} A^(ord[j])(B_j, r).
+template <int R>
+__device__ void form_weights(const StreamPlan &p, int lane, const StreamSmem &sm) {
+  constexpr int WSTR = (R % 2 == 0) ? R + 2 : R + 1;
+  const int nd = p.nd;
+  const bool has_f0 = (p.ord[0] != p.mode);
+  int Bc[kMaxDigits];
 #pragma unroll
-  for (int j = 0; j < kMaxDigits; ++j)
-    if (j < p.nd) q += (int64_t)d[j] * p.qsd[j];
-  return q;
+  for (int j = 0; j < kMaxDigits; ++j) Bc[j] = -1;
+  int stage = 0;
+  uint32_t fph = 0;
+  for (;;) {
+    mbar_wait(&sm.full[stage], fph);
+    const int *h = sm.hdr + stage * kHdrInts;
+    const int ncols = h[0];
+    const int flags = h[1];
+    bool changed = false;
+#pragma unroll
+    for (int j = 1; j < kMaxDigits; ++j)
+      if (j < nd && h[4 + j] != Bc[j]) changed = true;
+    if (changed || Bc[0] == -1) {
+      double s = 1.0;
+#pragma unroll
+      for (int j = 1; j < kMaxDigits; ++j) {
+        if (j < nd) {
+          Bc[j] = h[4 + j];
+          if (p.ord[j] != p.mode && lane < R) s *= __ldg(p.At[p.ord[j]] + (int64_t)Bc[j] * p.RS + lane);
+        }
+      }
+      Bc[0] = 0;
+      if (lane < R) sm.sS[lane] = s;
+      __syncwarp();
+    }
+    const double *as = sm.abuf + (size_t)stage * p.cps * p.RS;
+    double *ws = sm.wbuf + (size_t)stage * p.cps * WSTR;
+    for (int e = lane; e < ncols * R; e += 32) {
+      const int col = e / R, r = e - (e / R) * R;
+      ws[col * WSTR + r] = (has_f0 ? as[col * p.RS + r] : 1.0) * sm.sS[r];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.wready[stage]);
+    if (flags & 2) break;
+    if (++stage == p.nstages) {
+      stage = 0;
+      fph ^= 1u;
+    }
+  }
 }
 
 template <int R, int V, int OP>
-__global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1)) stream_kernel(const __grid_constant__ StreamPlan p) {
+__global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1))
+    stream_kernel(const __grid_constant__ StreamPlan p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int WSTR = (R % 2 == 0) ? R + 2 : R + 1;  // weight row stride (even: 16-B aligned)
-  const int zst = p.cps * p.Wmax;                      // doubles per Z stage
-  const int wst = p.cps * WSTR;                        // doubles per weight stage
-  double *zbuf = reinterpret_cast<double *>(smem_raw);
-  double *wbuf = zbuf + (size_t)p.nstages * zst;
-  double *red = wbuf + (size_t)p.nstages * wst;        // [8][R] (+8 spare)
-  uint64_t *full = reinterpret_cast<uint64_t *>(red + kConsumerWarps * R + 8);
-  uint64_t *empty = full + p.nstages;
-  int *hdr = reinterpret_cast<int *>(empty + p.nstages);  // [nstages][4]
+  const StreamSmem sm = carve<R>(smem_raw, p);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -63,137 +211,25 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1)) stream_kern
 
   if (tid == 0) {
     for (int s = 0; s < p.nstages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.wready[s], 1);
+      mbar_init(&sm.empty[s], kConsumerWarps);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    // ============================ producer warp ============================
-    // Columns are visited in "v order"; the producer keeps the v-digits of the
-    // stage start in registers (an odometer over p.rad, 32-bit), so no 64-bit division runs
-    // per column.  Lane 0 issues the TMA bulk copies; all lanes form the Khatri-Rao rows.
-    const int cpp = 32 / R;  // weight columns per pass (lanes over (col, r))
-    const int lc = lane / R, lr = lane - (lane / R) * R;
-    const int nd = p.nd;
-    int B[kMaxDigits];
-    {
-      int64_t t = v0;
-#pragma unroll
-      for (int j = 0; j < kMaxDigits; ++j) {
-        B[j] = 0;
-        if (j < nd) {
-          B[j] = (int)(t % p.rad[j]);
-          t /= p.rad[j];
-        }
-      }
-    }
-    int64_t seg_left = p.Qn - (v0 % p.Qn);
-    int seg_slot = 0;
-    int stage = 0;
-    uint32_t eph = 1;
-    int64_t v = v0;
-    while (v < v1) {
-      const int64_t lim = (seg_left < v1 - v) ? seg_left : (v1 - v);
-      const int ncols = (int)(lim < p.cps ? lim : p.cps);
-      const bool last = (v + ncols == v1);
-      const bool eos = (ncols == seg_left) || last;  // a segment ends, or this CTA's range does
-      mbar_wait(&empty[stage], eph);
-      double *zs = zbuf + (size_t)stage * zst;
-      if (V == 2) {
-        if (lane == 0) {
-          mbar_expect_tx(&full[stage], (uint32_t)(ncols * Wb * 8));
-          int D[kMaxDigits];
-#pragma unroll
-          for (int j = 0; j < kMaxDigits; ++j) D[j] = B[j];
-          int64_t q = digits_to_q(p, D);
-          int64_t run_q = q;
-          int run_col = 0, run_n = 1;
-          for (int col = 1; col <= ncols; ++col) {
-            int64_t q2 = -1;
-            if (col < ncols) {
-              add_carry(D, nd, p.rad, 1);
-              q2 = digits_to_q(p, D);
-            }
-            if (col < ncols && p.RB == 1 && q2 == q + 1) {
-              ++run_n;
-            } else {
-              bulk_g2s(zs + (size_t)run_col * Wb, p.Z + run_q * p.I1 + row0, (uint32_t)(run_n * Wb * 8),
-                       &full[stage]);
-              run_q = q2;
-              run_col = col;
-              run_n = 1;
-            }
-            q = q2;
-          }
-        }
-      } else {
-        // scalar fallback (odd I1: columns are not 16-B aligned): the warp copies elements
-        int D[kMaxDigits];
-#pragma unroll
-        for (int j = 0; j < kMaxDigits; ++j) D[j] = B[j];
-        for (int col = 0; col < ncols; ++col) {
-          if (col > 0) add_carry(D, nd, p.rad, 1);
-          const double *src = p.Z + digits_to_q(p, D) * p.I1 + row0;
-          for (int i = lane; i < Wb; i += 32) zs[(size_t)col * Wb + i] = __ldg(src + i);
-        }
-      }
-      // Khatri-Rao rows w_q[r] = prod_{k>=1, k != mode} A^(k)(i_k, r) of this stage's columns,
-      // four columns per lane at a time so their factor loads are in flight together
-      double *ws = wbuf + (size_t)stage * wst;
-      if (lc < cpp) {
-        for (int c0 = lc; c0 < ncols; c0 += 4 * cpp) {
-          int D[4][kMaxDigits];
-          double w[4];
-#pragma unroll
-          for (int u4 = 0; u4 < 4; ++u4) {
-#pragma unroll
-            for (int j = 0; j < kMaxDigits; ++j) D[u4][j] = B[j];
-            add_carry(D[u4], nd, p.rad, c0 + u4 * cpp);
-            w[u4] = 1.0;
-          }
-#pragma unroll
-          for (int j = 0; j < kMaxDigits; ++j) {
-            if (j < nd && p.ord[j] != p.mode) {
-              const double *a = p.At[p.ord[j]] + lr;
-#pragma unroll
-              for (int u4 = 0; u4 < 4; ++u4) w[u4] *= __ldg(a + D[u4][j] * R);
-            }
-          }
-#pragma unroll
-          for (int u4 = 0; u4 < 4; ++u4) {
-            const int col = c0 + u4 * cpp;
-            if (col < ncols) ws[col * WSTR + lr] = w[u4];
-          }
-        }
-      }
-      if (lane == 0) {
-        int *h = hdr + stage * 4;
-        h[0] = ncols;
-        h[1] = (eos ? 1 : 0) | (last ? 2 : 0);
-        h[2] = seg_slot;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&full[stage]);
-      v += ncols;
-      add_carry(B, nd, p.rad, ncols);
-      seg_left -= ncols;
-      if (seg_left == 0) {
-        seg_left = p.Qn;
-        ++seg_slot;
-      }
-      if (++stage == p.nstages) {
-        stage = 0;
-        eph ^= 1u;
-      }
-    }
+    if (V == 1 || lane == 0) produce<R, V>(p, lane, v0, v1, row0, Wb, sm);
+    return;
+  }
+  if (warp == kConsumerWarps + 1) {
+    form_weights<R>(p, lane, sm);
     return;
   }
 
   // ============================ consumer warps ============================
-  const int U = Wb / V;                       // row units per column in this block
+  const int U = Wb / V;                                          // row units per column
   const int cpt = (kConsumers / U) > 0 ? (kConsumers / U) : 1;  // columns per sub-tile
   const int u = tid % U;
   const int sl = tid / U;
@@ -211,19 +247,20 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1)) stream_kern
     for (int v = 0; v < V; ++v)
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        arow[v][r] = active ? __ldg(p.At[0] + (row0 + u * V + v) * R + r) : 0.0;
+        arow[v][r] = active ? __ldg(p.At[0] + (row0 + u * V + v) * p.RS + r) : 0.0;
   }
 
   int stage = 0;
   uint32_t fph = 0;
   for (;;) {
-    mbar_wait(&full[stage], fph);
-    const int *h = hdr + stage * 4;
+    mbar_wait(&sm.wready[stage], fph);
+    mbar_wait(&sm.full[stage], fph);
+    const int *h = sm.hdr + stage * kHdrInts;
     const int ncols = h[0];
     const int flags = h[1];
     const int slot = h[2];
-    const double *zs = zbuf + (size_t)stage * zst;
-    const double *wsb = wbuf + (size_t)stage * wst;
+    const double *zs = sm.zbuf + (size_t)stage * p.cps * p.Wmax;
+    const double *wsb = sm.wbuf + (size_t)stage * p.cps * WSTR;
     if (active) {
       for (int col = sl; col < ncols; col += cpt) {
         double z[V];
@@ -277,7 +314,7 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1)) stream_kern
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (lane == 0) mbar_arrive(&sm.empty[stage]);
     if (++stage == p.nstages) {
       stage = 0;
       fph ^= 1u;
@@ -291,7 +328,7 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1)) stream_kern
       if (active) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          const double *a1 = p.At[0] + (row0 + u * V + v) * R;
+          const double *a1 = p.At[0] + (row0 + u * V + v) * p.RS;
 #pragma unroll
           for (int r = 0; r < R; ++r) pr[r] = fma(__ldg(a1 + r), acc[v][r], pr[r]);
         }
@@ -307,13 +344,13 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1)) stream_kern
       }
       if (lane == 0) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) red[warp * R + r] = pr[r];
+        for (int r = 0; r < R; ++r) sm.red[warp * R + r] = pr[r];
       }
       named_bar_sync(1, kConsumers);
       if (tid < R) {
         double sum = 0.0;
 #pragma unroll
-        for (int w8 = 0; w8 < kConsumerWarps; ++w8) sum += red[w8 * R + tid];
+        for (int w8 = 0; w8 < kConsumerWarps; ++w8) sum += sm.red[w8 * R + tid];
         p.part[((int64_t)blockIdx.x * p.slots + slot) * R + tid] = sum;
       }
       named_bar_sync(1, kConsumers);
@@ -326,7 +363,7 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1)) stream_kern
     double *out = p.part + (int64_t)c * p.I1 * R;
     if (cpt > 1) {
       named_bar_sync(1, kConsumers);  // every consumer is past the ring: reuse it
-      double *sred = zbuf;            // Wb x R
+      double *sred = sm.zbuf;         // Wb x R
       for (int s = 1; s < cpt; ++s) {
         if (active && sl == s) {
 #pragma unroll
@@ -356,11 +393,11 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1)) stream_kern
     for (int v = 0; v < V; ++v) sacc += acc[v][0];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, off);
-    if (lane == 0) red[warp] = sacc;
+    if (lane == 0) sm.red[warp] = sacc;
     named_bar_sync(1, kConsumers);
     if (tid == 0) {
       double sum = 0.0;
-      for (int w8 = 0; w8 < kConsumerWarps; ++w8) sum += red[w8];
+      for (int w8 = 0; w8 < kConsumerWarps; ++w8) sum += sm.red[w8];
       p.part[blockIdx.x] = sum;
     }
   }
@@ -378,7 +415,5 @@ cudaError_t launch_stream_t(const StreamPlan &p, cudaStream_t st) {
   kern<<<p.Gc * p.RB, kStreamThreads, p.smem_bytes, st>>>(p);
   return cudaGetLastError();
 }
-
-using StreamLauncher = cudaError_t (*)(const StreamPlan &, cudaStream_t);
 
 }  // namespace cpk
