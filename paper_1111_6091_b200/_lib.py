@@ -7,7 +7,7 @@ CP_MAX_R = 32
 CP_OK, CP_EINVAL, CP_EDIM, CP_ENOTSPD, CP_ECUDA, CP_EWORKSPACE = 0, -1, -2, -3, -4, -5
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = os.path.join(_HERE, "lib", "libcp.so")
+_LIB = os.environ.get("CP_LIB_PATH") or os.path.join(_HERE, "lib", "libcp.so")
 _lib = None
 
 # every symbol include/cp.h declares (checked by tests/test_capi_symbols.py)

@@ -74,8 +74,22 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   }
   p.I1 = s.dims[0];
   p.Q = P / p.I1;
-  p.V = (p.I1 % 2 == 0) ? 2 : 1;
-  const int maxW = (p.V == 2) ? kMaxRows : kMaxRows / 2;
+  // rows per consumer thread: the largest V dividing I1 with V * RT <= 32 accumulators, which
+  // keeps the kernel at <= 96 registers and 2 CTAs/SM (measured: 2 CTAs/SM beat 1 CTA/SM with
+  // a larger register tile, profiles/README.md); residual pass: V <= 4 and V * R <= 64
+  const int RT = stream_rt(s.R, op), RG = stream_rg(s.R, op);
+  const int vmax_env = env_int("CP_MAX_V", 8);
+  const int vr_max = env_int("CP_MAX_VR", 32);
+  p.V = 1;
+  for (int v : {8, 4, 2}) {
+    if (v > vmax_env || p.I1 % v != 0) continue;
+    if (op == OP_MTTKRP && v * RT > vr_max && v > 2) continue;
+    if (op == OP_RESID && (v > 4 || v * s.R > 64)) continue;
+    p.V = v;
+    break;
+  }
+  int maxW = (kConsumers / RG) * p.V;  // one column per sub-tile at most
+  if (maxW > kMaxRows) maxW = kMaxRows;
   // row-block width: mode 0 MTTKRP uses narrower blocks (fewer column groups -> smaller I1 x R
   // partials); every other pass keeps whole columns in one CTA.
   int64_t Wt = p.I1;
@@ -86,7 +100,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   if (Wt > maxW) Wt = maxW;
   p.RB = (int)ceil_div(p.I1, Wt);
   int64_t W = ceil_div(p.I1, p.RB);
-  if (p.V == 2 && (W & 1)) ++W;
+  while (W % p.V) ++W;
   p.Wmax = (int)W;
   if (p.mode == 0) {
     p.In = 1;
@@ -116,8 +130,8 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     }
   }
   const int U = p.Wmax / p.V;
-  const int cpt = (kConsumers / U) > 0 ? (kConsumers / U) : 1;
-  const int stage_target = env_int("CP_STAGE_BYTES", 16384);
+  const int cpt = (kConsumers / (U * RG)) > 0 ? (kConsumers / (U * RG)) : 1;
+  const int stage_target = env_int("CP_STAGE_BYTES", 40960);  // tools/sweep4.sh
   int cps = stage_target / (p.Wmax * 8);
   if (cps < 1) cps = 1;
   if (cps >= cpt) cps = (cps / cpt) * cpt;
@@ -134,8 +148,8 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   // mode-0 slot reduction reuses the Z ring: it must hold Wmax x R doubles
   while ((int64_t)nst * cps * p.Wmax < (int64_t)p.Wmax * s.R) ++nst;
   p.nstages = nst;
-  // ring | red[8R+8] | sS[32] | 3 x nst mbarriers | nst x 16-int headers
-  p.smem_bytes = (nst * stage_doubles + kConsumerWarps * s.R + 8 + 32) * 8 + nst * 24 + nst * 64 + 64;
+  // ring | red | sS[32] | 3 x nst mbarriers | nst x 16-int headers
+  p.smem_bytes = (nst * stage_doubles + stream_red_doubles(s.R, op) + 32) * 8 + nst * 24 + nst * 64 + 64;
   if (p.smem_bytes > 200 * 1024) return false;
   const int occ = stream_occupancy(s.R, p.V, op, p.smem_bytes);
   const int ctas = env_int("CP_CTAS_PER_SM", 0);
@@ -196,7 +210,9 @@ cudaError_t launch_stream(const StreamPlan &p, cudaStream_t st) {
 // ---------------------------------------------------------------- workspace layout
 struct Layout {
   size_t status, Ups, gpart0, gpart1, dotM, dotF, gradp, normp, residp, part, At[CP_MAX_N], total;
-  int rpc, gp_max, grad_max, norm_blocks;
+  int gp_max, grad_max, norm_blocks, prep_blocks;
+  size_t gpre;
+  int rpc[CP_MAX_N], sp[CP_MAX_N];  // row blocking of the solve / gradient / reduce kernels
   int nsolve[CP_MAX_N], ngrad[CP_MAX_N];
   StreamPlan plans[CP_MAX_N];
   StreamPlan resid;
@@ -208,22 +224,28 @@ static bool make_layout(Layout &L, const cp_shape &s) {
   memset(&L, 0, sizeof(L));
   const int sms = device_sms();
   const int R = s.R;
-  L.rpc = 256 / R > 0 ? 256 / R : 1;
   size_t part = 0;
+  int64_t maxI = 1;
   for (int n = 0; n < s.N; ++n) {
     if (!make_stream_plan(L.plans[n], s, n, OP_MTTKRP, sms)) return false;
     const size_t d = stream_part_doubles(L.plans[n]);
     if (d > part) part = d;
-    L.nsolve[n] = (int)ceil_div(s.dims[n], L.rpc);
+    row_blocking(L.plans[n], &L.rpc[n], &L.sp[n]);
+    L.nsolve[n] = (int)ceil_div(s.dims[n], L.rpc[n]);
     if (L.nsolve[n] > L.gp_max) L.gp_max = L.nsolve[n];
-    L.ngrad[n] = (int)ceil_div(s.dims[n] * R, 256);
+    L.ngrad[n] = L.nsolve[n];
     if (L.ngrad[n] > L.grad_max) L.grad_max = L.ngrad[n];
+    if (s.dims[n] > maxI) maxI = s.dims[n];
   }
+  L.prep_blocks = 0;
+  for (int k = 0; k < s.N; ++k) L.prep_blocks += (int)ceil_div(s.dims[k], kPrepRows);
+  (void)maxI;
   if (!make_stream_plan(L.resid, s, 0, OP_RESID, sms)) return false;
   L.norm_blocks = 2 * sms;
   size_t off = 0;
   L.status = off; off = align_up(off + 8);
   L.Ups = off; off = align_up(off + (size_t)s.N * R * R);
+  L.gpre = off; off = align_up(off + (size_t)L.prep_blocks * R * R);
   L.gpart0 = off; off = align_up(off + (size_t)L.gp_max * R * R);
   L.gpart1 = off; off = align_up(off + (size_t)L.gp_max * R * R);
   L.dotM = off; off = align_up(off + L.gp_max);
@@ -238,6 +260,25 @@ static bool make_layout(Layout &L, const cp_shape &s) {
   L.part = off; off = align_up(off + part);
   L.total = off * sizeof(double);
   return true;
+}
+
+// Arguments of the prep kernel (At copies of every factor except skip_mode; per-block partial
+// Grams when grams) and where its Gram partials land.
+static void fill_prep(const cp_shape &s, const Layout &L, double *w, const double *const *A,
+                      int skip_mode, bool grams, double *status, PrepArgs &pa, PrepGrams &pg) {
+  memset(&pa, 0, sizeof(pa));
+  memset(&pg, 0, sizeof(pg));
+  pa.N = s.N;
+  pa.R = s.R;
+  for (int k = 0; k < s.N; ++k) {
+    pa.dims[k] = s.dims[k];
+    pa.A[k] = (k == skip_mode) ? nullptr : A[k];
+    pa.At[k] = w + L.At[k];
+  }
+  pa.gpre = grams ? w + L.gpre : nullptr;
+  pa.status = status;
+  prep_blocks(s, pa, pg);
+  pg.gpre = w + L.gpre;
 }
 
 static int check_shape(const cp_shape *s, int minN) {
@@ -301,7 +342,7 @@ int cp_norm2(const cp_shape *s, const double *Z, double *out, void *ws, size_t w
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   norm2_kernel<<<nb, 512, 0, cs>>>(Z, P, part);
   CK_LAUNCH();
-  norm2_final_kernel<<<1, 32, 0, cs>>>(part, nb, out);
+  norm2_final_kernel<<<1, 256, 0, cs>>>(part, nb, out);
   CK_LAUNCH();
   g_launches = 2;
   return CP_OK;
@@ -321,24 +362,16 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
   double *w = static_cast<double *>(ws);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   PrepArgs pa;
-  memset(&pa, 0, sizeof(pa));
-  pa.N = s->N;
-  pa.R = s->R;
-  for (int k = 0; k < s->N; ++k) {
-    pa.dims[k] = s->dims[k];
-    pa.A[k] = (k == mode) ? nullptr : A[k];
-    pa.At[k] = w + L.At[k];
-  }
-  prep_kernel<<<s->N, 256, 0, cs>>>(pa);
-  CK_LAUNCH();
+  PrepGrams pg;
+  fill_prep(*s, L, w, A, mode, false, nullptr, pa, pg);
+  if (launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
   StreamPlan p = L.plans[mode];
   p.Z = Z;
   for (int k = 0; k < s->N; ++k) p.At[k] = w + L.At[k];
   p.part = w + L.part;
   if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
   const ReduceGeom g = reduce_geom(p);
-  const int64_t n = s->dims[mode] * s->R;
-  reduce_mttkrp_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, cs>>>(g, M);
+  reduce_mttkrp_kernel<<<L.nsolve[mode], 256, 0, cs>>>(g, L.rpc[mode], L.sp[mode], M);
   CK_LAUNCH();
   g_launches = 3;
   return CP_OK;
@@ -361,18 +394,9 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
   const int N = s->N, R = s->R;
 
   PrepArgs pa;
-  memset(&pa, 0, sizeof(pa));
-  pa.N = N;
-  pa.R = R;
-  for (int k = 0; k < N; ++k) {
-    pa.dims[k] = s->dims[k];
-    pa.A[k] = A[k];
-    pa.At[k] = w + L.At[k];
-  }
-  pa.Ups = w + L.Ups;
-  pa.status = w + L.status;
-  prep_kernel<<<N, 256, 0, cs>>>(pa);
-  CK_LAUNCH();
+  PrepGrams pg;
+  fill_prep(*s, L, w, (const double *const *)A, -1, true, w + L.status, pa, pg);
+  if (launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
   int launches = 1;
   double *gp[2] = {w + L.gpart0, w + L.gpart1};
   for (int n = 0; n < N; ++n) {
@@ -388,9 +412,11 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     sa.mode = n;
     sa.prev_mode = n - 1;
     sa.nprev = (n > 0) ? L.nsolve[n - 1] : 0;
-    sa.rpc = L.rpc;
+    sa.rpc = L.rpc[n];
+    sa.sp = L.sp[n];
     sa.In = s->dims[n];
     sa.rg = reduce_geom(p);
+    sa.pg = pg;
     sa.F = (F != nullptr) ? F[n] : nullptr;
     sa.A = A[n];
     sa.At = w + L.At[n];
@@ -400,8 +426,7 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     sa.dotM = w + L.dotM;
     sa.dotF = w + L.dotF + (size_t)n * L.gp_max;
     sa.status = w + L.status;
-    solve_kernel<<<L.nsolve[n], 256, 0, cs>>>(sa);
-    CK_LAUNCH();
+    if (launch_solve(sa, L.nsolve[n], cs) != cudaSuccess) return CP_ECUDA;
     launches += 2;
   }
   FinalizeArgs fa;
@@ -465,18 +490,9 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   const int N = s->N, R = s->R;
   PrepArgs pa;
-  memset(&pa, 0, sizeof(pa));
-  pa.N = N;
-  pa.R = R;
-  for (int k = 0; k < N; ++k) {
-    pa.dims[k] = s->dims[k];
-    pa.A[k] = A[k];
-    pa.At[k] = w + L.At[k];
-  }
-  pa.Ups = w + L.Ups;
-  pa.status = nullptr;
-  prep_kernel<<<N, 256, 0, cs>>>(pa);
-  CK_LAUNCH();
+  PrepGrams pg;
+  fill_prep(*s, L, w, A, -1, true, nullptr, pa, pg);
+  if (launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
   int launches = 1;
   // residual pass 1/2 ||Z - [[A]]||^2 (eq:CPfunctional): one partial per CTA
   StreamPlan rp = L.resid;
@@ -496,8 +512,11 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
     ga.N = N;
     ga.R = R;
     ga.mode = n;
+    ga.rpc = L.rpc[n];
+    ga.sp = L.sp[n];
     ga.In = s->dims[n];
     ga.rg = reduce_geom(p);
+    ga.pg = pg;
     ga.A = A[n];
     ga.F = (F != nullptr) ? F[n] : nullptr;
     ga.Ups = w + L.Ups;
@@ -517,7 +536,7 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
   fa.gpart = w + L.gradp;
   fa.normZ2 = normZ2;
   fa.out = out;
-  finalize_fit_kernel<<<1, 32, 0, cs>>>(fa);
+  finalize_fit_kernel<<<1, 256, 0, cs>>>(fa);
   CK_LAUNCH();
   g_launches = launches + 1;
   return CP_OK;

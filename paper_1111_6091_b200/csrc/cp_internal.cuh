@@ -23,7 +23,7 @@ enum StreamOp { OP_MTTKRP = 0, OP_RESID = 1 };
 // touches few output rows ("segments" of Qn columns each).
 struct StreamPlan {
   int N, R, mode, op;
-  int V;            // 2: rows in pairs (I1 even, 16-B bulk copies);  1: scalar fallback
+  int V;            // rows per consumer thread: 8/4/2 (I1 divisible), 1 (odd I1: scalar fallback)
   int Wmax;         // row-block width (even when V = 2)
   int RB;           // number of row blocks
   int Gc;           // number of column groups
@@ -54,8 +54,19 @@ struct StreamEntry {
   cudaError_t (*launch)(const StreamPlan &, cudaStream_t);
   const void *kernel;
 };
-constexpr int stream_index(int R, int V, int op) { return (R * 2 + (V - 1)) * 2 + op; }
-constexpr int kStreamTableSize = stream_index(CP_MAX_R, 2, 1) + 1;
+constexpr int stream_index(int R, int V, int op) {
+  return (R * 4 + (V == 8 ? 3 : (V == 4 ? 2 : V - 1))) * 2 + op;
+}
+// Consumer rank tile (see StreamTile in stream_kernel.cuh): ranks per thread and rank groups.
+__host__ __device__ constexpr int stream_rg(int R, int op) { return (op == 0 && R > 12) ? (R + 7) / 8 : 1; }
+__host__ __device__ constexpr int stream_rt(int R, int op) {
+  return (stream_rg(R, op) > 1 && (((R + stream_rg(R, op) - 1) / stream_rg(R, op)) & 1))
+             ? (R + stream_rg(R, op) - 1) / stream_rg(R, op) + 1
+             : (R + stream_rg(R, op) - 1) / stream_rg(R, op);
+}
+// shared-memory reduction area of the consumers (doubles)
+__host__ __device__ constexpr int stream_red_doubles(int R, int op) { return 256 * stream_rt(R, op) + 8 > 8 * R + 8 ? 256 * stream_rt(R, op) + 8 : 8 * R + 8; }
+constexpr int kStreamTableSize = stream_index(CP_MAX_R, 8, 1) + 1;
 void register_stream_part0(StreamEntry *t);
 void register_stream_part1(StreamEntry *t);
 void register_stream_part2(StreamEntry *t);

@@ -1,151 +1,235 @@
 // small_kernels.cu -- the R x R side of the hot path (eq:Gamma P:113-116, Cholesky solve of
 // P:121 / eq:relaxinnersolve P:356-358, the functional eq:CPfunctional P:38-42, the gradient
 // eq:gradEqn and g eq:gradConv P:454-456) plus ||Z||^2.  All reductions run in a fixed order
-// (no atomics), so results are bitwise reproducible.
+// (no atomics), so results are bitwise reproducible.  These kernels are latency-bound: every
+// global read is issued in independent batches, and the R x R algebra runs in registers of
+// one warp (R is a template parameter).
 #include "small_kernels.cuh"
 
 namespace cpk {
 
+// ---------------------------------------------------------------- block reduction (fixed tree)
+// blockDim.x == 256; returns the sum to every thread.
+__device__ double block_sum_256(double v, double *sred) {
+  const int tid = threadIdx.x;
+  __syncthreads();
+  sred[tid] = v;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (tid < off) sred[tid] += sred[tid + off];
+    __syncthreads();
+  }
+  const double r = sred[0];
+  __syncthreads();
+  return r;
+}
+
+// sum of n strided values, 8 independent loads in flight, combined in a fixed order
+__device__ __forceinline__ double sum_strided(const double *p, int64_t stride, int n) {
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int c = 0;
+  for (; c + 8 <= n; c += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] += p[(int64_t)(c + j) * stride];
+  }
+  for (int j = 0; c + j < n; ++j) s[j] += p[(int64_t)(c + j) * stride];
+  return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+}
+
 // ---------------------------------------------------------------- reduction of stream partials
-__device__ __forceinline__ double reduce_entry(const ReduceGeom &g, int64_t i, int r) {
+// Part j of sp of the fixed-order sum that forms M(i, r) from the stream kernel's partials.
+__device__ __forceinline__ double reduce_entry_part(const ReduceGeom &g, int64_t i, int r, int j, int sp) {
+  if (g.mode0) {  // mode 0: one I1 x R partial per column group; chunk j of the groups
+    const int c0 = (int)(((int64_t)g.Gc * j) / sp), c1 = (int)(((int64_t)g.Gc * (j + 1)) / sp);
+    return sum_strided(g.part + (int64_t)c0 * g.I1 * g.R + i + g.I1 * r, g.I1 * g.R, c1 - c0);
+  }
+  if (j != 0) return 0.0;
+  // mode m >= 1: R-vector partials per (column group, row block, segment)
   double s = 0.0;
-  if (g.mode0) {  // mode 0: one I1 x R partial per column group
-    const double *p = g.part + i + g.I1 * r;
-    const int64_t stride = g.I1 * g.R;
-    int c = 0;
-    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    for (; c + 3 < g.Gc; c += 4) {  // four independent chains, combined in fixed order
-      s += p[(int64_t)c * stride];
-      s1 += p[(int64_t)(c + 1) * stride];
-      s2 += p[(int64_t)(c + 2) * stride];
-      s3 += p[(int64_t)(c + 3) * stride];
-    }
-    for (; c < g.Gc; ++c) s += p[(int64_t)c * stride];
-    s = (s + s1) + (s2 + s3);
-  } else {  // mode m >= 1: R-vector partials per (column group, row block, segment)
-    const int64_t lo = i * g.Qn, hi = (i + 1) * g.Qn - 1;
-    const int64_t clo = ((lo + 1) * g.Gc - 1) / g.Q;
-    const int64_t chi = ((hi + 1) * g.Gc - 1) / g.Q;
-    for (int64_t c = clo; c <= chi; ++c) {
-      const int64_t seg_first = ((c * g.Q) / g.Gc) / g.Qn;
-      for (int rb = 0; rb < g.RB; ++rb)
-        s += g.part[(((c * g.RB + rb) * g.slots) + (i - seg_first)) * g.R + r];
-    }
+  const int64_t lo = i * g.Qn, hi = (i + 1) * g.Qn - 1;
+  const int64_t clo = ((lo + 1) * g.Gc - 1) / g.Q;
+  const int64_t chi = ((hi + 1) * g.Gc - 1) / g.Q;
+  for (int64_t c = clo; c <= chi; ++c) {
+    const int64_t seg_first = ((c * g.Q) / g.Gc) / g.Qn;
+    for (int rb = 0; rb < g.RB; ++rb) s += g.part[(((c * g.RB + rb) * g.slots) + (i - seg_first)) * g.R + r];
   }
   return s;
 }
 
-__global__ void reduce_mttkrp_kernel(const ReduceGeom g, double *M) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= g.In_rows * g.R) return;
-  const int64_t i = idx % g.In_rows;
-  const int r = (int)(idx / g.In_rows);
-  M[i + g.In_rows * r] = reduce_entry(g, i, r);
+// Phase A of the solve / gradient kernels: M rows [i0, i0 + nrows) into sM (row-major, R per
+// row), using sp threads per entry.  Needs a 256-double scratch.
+__device__ void gather_rows(const ReduceGeom &g, int64_t i0, int nrows, int R, int sp, double *sM,
+                            double *scratch) {
+  const int tid = threadIdx.x;
+  const int ent = tid / sp, j = tid - (tid / sp) * sp;
+  double v = 0.0;
+  if (ent < nrows * R) {
+    const int ii = ent / R, r = ent - (ent / R) * R;
+    v = reduce_entry_part(g, i0 + ii, r, j, sp);
+  }
+  if (sp == 1) {
+    if (ent < nrows * R) sM[ent] = v;
+    return;
+  }
+  scratch[tid] = v;
+  __syncthreads();
+  if (j == 0 && ent < nrows * R) {
+    double s = 0.0;
+    for (int k = 0; k < sp; ++k) s += scratch[tid + k];
+    sM[ent] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) reduce_mttkrp_kernel(const ReduceGeom g, int rpc, int sp, double *M) {
+  __shared__ double sM[256], scratch[256];
+  const int64_t i0 = (int64_t)blockIdx.x * rpc;
+  const int nrows = (int)((g.In_rows - i0) < rpc ? (g.In_rows - i0) : rpc);
+  gather_rows(g, i0, nrows, g.R, sp, sM, scratch);
+  __syncthreads();
+  for (int e = threadIdx.x; e < nrows * g.R; e += blockDim.x) {
+    const int ii = e / g.R, r = e - (e / g.R) * g.R;
+    M[(i0 + ii) + g.In_rows * r] = sM[e];
+  }
 }
 
 // ---------------------------------------------------------------- prep: At copies + Grams
-// block k: At^(k) (row-major copy), Upsilon^(k) = A^(k)^T A^(k), fixed-order sums.
-__global__ void prep_kernel(const PrepArgs a) {
-  const int k = blockIdx.x;
-  const int R = a.R;
+// One block per (mode k, chunk of kPrepRows rows): At^(k) rows (row-major copy, padded stride
+// RS) and the chunk's partial Gram A_chunk^T A_chunk, summed later in chunk order.
+__global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
+  __shared__ double sA[kPrepRows * 33];  // chunk x R, column-major (r * kPrepRows + ii)
+  int k = 0;
+  while (k + 1 < a.N && (int)blockIdx.x >= a.blk_off[k + 1]) ++k;
+  const int b = blockIdx.x - a.blk_off[k];
+  const int R = a.R, RS = R + (R & 1), RR = R * R;
   const int64_t I = a.dims[k];
   const double *A = a.A[k];
-  if (A == nullptr) return;
-  double *At = a.At[k];
-  const int RS = R + (R & 1);  // padded row stride (16-B aligned rows for the TMA copies)
-  for (int64_t e = threadIdx.x; e < I * RS; e += blockDim.x) {
-    const int64_t i = e / RS;
-    const int r = (int)(e - i * RS);
-    At[e] = (r < R) ? A[i + I * r] : 0.0;
-  }
-  if (a.Ups != nullptr) {
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-      const int r = e % R, s = e / R;
-      const double *ar = A + I * r;
-      const double *as = A + I * s;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int64_t i = 0;
-      for (; i + 3 < I; i += 4) {
-        s0 = fma(ar[i], as[i], s0);
-        s1 = fma(ar[i + 1], as[i + 1], s1);
-        s2 = fma(ar[i + 2], as[i + 2], s2);
-        s3 = fma(ar[i + 3], as[i + 3], s3);
-      }
-      for (; i < I; ++i) s0 = fma(ar[i], as[i], s0);
-      a.Ups[(int64_t)k * R * R + e] = (s0 + s1) + (s2 + s3);
-    }
-  }
-  if (k == 0 && threadIdx.x == 0 && a.status != nullptr) {
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0 && tid == 0 && a.status != nullptr) {
     a.status[0] = 0.0;
     a.status[1] = -1.0;
   }
+  if (A == nullptr) return;
+  double *At = a.At[k];
+  const int64_t i0 = (int64_t)b * kPrepRows;
+  const int n = (int)((I - i0) < kPrepRows ? (I - i0) : kPrepRows);
+  for (int e = tid; e < n * R; e += blockDim.x) {
+    const int r = e / n, ii = e - (e / n) * n;
+    sA[r * kPrepRows + ii] = A[(i0 + ii) + I * r];
+  }
+  __syncthreads();
+  for (int e = tid; e < n * RS; e += blockDim.x) {
+    const int ii = e / RS, r = e - (e / RS) * RS;
+    At[(i0 + ii) * RS + r] = (r < R) ? sA[r * kPrepRows + ii] : 0.0;
+  }
+  if (a.gpre != nullptr) {
+    for (int e = tid; e < RR; e += blockDim.x) {
+      const int r = e % R, s = e / R;
+      const double *ar = sA + r * kPrepRows, *as = sA + s * kPrepRows;
+      double g = 0.0;
+      for (int ii = 0; ii < n; ++ii) g = fma(ar[ii], as[ii], g);
+      a.gpre[(int64_t)blockIdx.x * RR + e] = g;
+    }
+  }
 }
 
-// Cholesky Gamma = L L^T (lower, no pivoting) of an R x R matrix in shared memory (stride 33),
-// by one warp: lane i owns row i.  Returns false on a pivot <= 0 (or NaN).
-__device__ bool warp_cholesky(double *G, int R, int lane) {
-  bool ok = true;
-  for (int j = 0; j < R; ++j) {
-    double d = 0.0;
-    if (lane == j) {
-      d = G[j * 33 + j];
-      for (int k = 0; k < j; ++k) d -= G[j * 33 + k] * G[j * 33 + k];
-    }
-    d = __shfl_sync(0xffffffffu, d, j);
-    if (!(d > 0.0)) {
-      ok = false;
-      break;
-    }
-    const double ljj = sqrt(d);
-    if (lane == j) G[j * 33 + j] = ljj;
-    __syncwarp();
-    if (lane > j && lane < R) {
-      double s = G[lane * 33 + j];
-      for (int k = 0; k < j; ++k) s -= G[lane * 33 + k] * G[j * 33 + k];
-      G[lane * 33 + j] = s / ljj;
-    }
-    __syncwarp();
-  }
-  return ok;
+// Upsilon^(k) entry e from the prep partials of mode k (fixed chunk order)
+__device__ __forceinline__ double prep_gram(const PrepGrams &pg, int k, int e, int RR) {
+  return sum_strided(pg.gpre + (int64_t)pg.blk_off[k] * RR + e, RR, pg.nblk[k]);
 }
 
 // ---------------------------------------------------------------- per-mode solve (sweep)
-__global__ void __launch_bounds__(256) solve_kernel(const SolveArgs a) {
-  __shared__ double sL[32 * 33];
-  __shared__ double sUp[32 * 32];
-  __shared__ double sX[256];   // rows x R of the new factor block (row-major)
-  __shared__ double sB[256];   // rhs M + F (row-major)
-  __shared__ double sM[256];   // M (row-major), for <M, A>
-  __shared__ double sdot[2][32];
+// One warp factors Gamma = L L^T in registers (lane i holds row i) and forms L^{-1}; every
+// row of A^(n) is then x = L^{-T} (L^{-1} (m + f)) as two small triangular mat-vecs.
+template <int R>
+__global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
+  constexpr int RR = R * R;
+  constexpr int LS = R + 1;  // smem row stride of the R x R matrices
+  __shared__ double sL[R * LS];    // Gamma, then L (lower)
+  __shared__ double sLi[R * LS];   // L^{-1} (lower)
+  __shared__ double sUp[RR];
+  __shared__ double sM[256], sB[256], sX[256], scratch[256];
   __shared__ int sfail;
-  const int R = a.R, RR = R * R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (a.status[0] != 0.0) return;  // an earlier mode already failed
 
   // total Gram of the previous mode from its per-CTA partials (fixed order)
   if (a.gprev != nullptr) {
     for (int e = tid; e < RR; e += blockDim.x) {
-      double s = 0.0;
-      for (int c = 0; c < a.nprev; ++c) s += a.gprev[(int64_t)c * RR + e];
+      const double s = sum_strided(a.gprev + e, RR, a.nprev);
       sUp[e] = s;
       if (blockIdx.x == 0) a.Ups[(int64_t)a.prev_mode * RR + e] = s;
     }
-    __syncthreads();
   }
-  // Gamma^(n) = *_{k != n} Upsilon^(k)   (eq:Gamma)
+  const int64_t In = a.In;
+  const int64_t i0 = (int64_t)blockIdx.x * a.rpc;
+  const int nrows = (int)((In - i0) < a.rpc ? (In - i0) : a.rpc);
+  // phase A (independent of Gamma): M rows from the stream partials
+  gather_rows(a.rg, i0, nrows, R, a.sp, sM, scratch);
+  __syncthreads();
+  // Gamma^(n) = *_{k != n} Upsilon^(k)   (eq:Gamma).  Upsilon^(k): k > n from the prep
+  // partials (factor not yet updated in this sweep), k = n-1 from the previous solve's
+  // partials, k < n-1 from the totals the earlier solves wrote.
   for (int e = tid; e < RR; e += blockDim.x) {
     double gm = 1.0;
     for (int k = 0; k < a.N; ++k) {
       if (k == a.mode) continue;
-      gm *= (a.gprev != nullptr && k == a.prev_mode) ? sUp[e] : a.Ups[(int64_t)k * RR + e];
+      double u;
+      if (k > a.mode) u = prep_gram(a.pg, k, e, RR);
+      else if (k == a.prev_mode) u = sUp[e];
+      else u = a.Ups[(int64_t)k * RR + e];
+      gm *= u;
     }
-    sL[(e % R) * 33 + (e / R)] = gm;
+    sL[(e % R) * LS + (e / R)] = gm;
+  }
+  for (int e = tid; e < nrows * R; e += blockDim.x) {
+    const int ii = e / R, r = e - (e / R) * R;
+    sB[e] = sM[e] + (a.F != nullptr ? a.F[(i0 + ii) + In * r] : 0.0);
   }
   if (tid == 0) sfail = 0;
   __syncthreads();
   if (warp == 0) {
-    const bool ok = warp_cholesky(sL, R, lane);
-    if (!ok && lane == 0) sfail = 1;
+    // Cholesky, right-looking, lane i = row i (no pivoting; fail on a pivot <= 0 or NaN)
+    double g[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) g[k] = (lane < R) ? sL[lane * LS + k] : 0.0;
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const double piv = __shfl_sync(0xffffffffu, g[j], j);
+      if (!(piv > 0.0)) {
+        ok = false;
+        break;
+      }
+      const double ljj = sqrt(piv);
+      const double inv = 1.0 / ljj;
+      if (lane == j) g[j] = ljj;
+      else if (lane > j) g[j] *= inv;
+#pragma unroll
+      for (int k = j + 1; k < R; ++k) {
+        const double lkj = __shfl_sync(0xffffffffu, g[j], k);
+        if (lane >= k) g[k] = fma(-g[j], lkj, g[k]);
+      }
+    }
+    if (!ok) {
+      if (lane == 0) sfail = 1;
+    } else {
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (lane < R) sL[lane * LS + k] = (k <= lane) ? g[k] : 0.0;
+      __syncwarp();
+      // L^{-1}: lane c forms column c by forward substitution
+      double x[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < i; ++k) s = fma(-sL[i * LS + k], x[k], s);
+        x[i] = (i >= lane) ? s / sL[i * LS + i] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (lane < R) sLi[i * LS + lane] = x[i];
+    }
   }
   __syncthreads();
   if (sfail) {
@@ -155,73 +239,43 @@ __global__ void __launch_bounds__(256) solve_kernel(const SolveArgs a) {
     }
     return;
   }
-
-  const int64_t In = a.In;
-  const int64_t i0 = (int64_t)blockIdx.x * a.rpc;
-  const int nrows = (int)((In - i0) < a.rpc ? (In - i0) : a.rpc);
-  // phase A: M rows from the stream partials (+F): thread per (row, r)
+  // y = L^{-1} b, then x = L^{-T} y, thread per (row, r)
   for (int e = tid; e < nrows * R; e += blockDim.x) {
     const int ii = e / R, r = e - (e / R) * R;
-    const int64_t i = i0 + ii;
-    const double m = reduce_entry(a.rg, i, r);
-    sM[e] = m;
-    sB[e] = m + (a.F != nullptr ? a.F[i + In * r] : 0.0);
+    double y = 0.0;
+    for (int k = 0; k <= r; ++k) y = fma(sLi[r * LS + k], sB[ii * R + k], y);
+    scratch[e] = y;
   }
   __syncthreads();
-  // phase B: warp per row, lane r: forward L y = b, back L^T x = y
-  for (int ii = warp; ii < nrows; ii += blockDim.x / 32) {
-    double b = (lane < R) ? sB[ii * R + lane] : 0.0;
-    for (int k = 0; k < R; ++k) {
-      const double yk = __shfl_sync(0xffffffffu, b / sL[k * 33 + k], k);
-      if (lane == k) b = yk;
-      if (lane > k && lane < R) b -= sL[lane * 33 + k] * yk;
-    }
-    for (int k = R - 1; k >= 0; --k) {
-      const double xk = __shfl_sync(0xffffffffu, b / sL[k * 33 + k], k);
-      if (lane == k) b = xk;
-      if (lane < k) b -= sL[k * 33 + lane] * xk;
-    }
+  double dm = 0.0, df = 0.0;
+  for (int e = tid; e < nrows * R; e += blockDim.x) {
+    const int ii = e / R, r = e - (e / R) * R;
+    double x = 0.0;
+    for (int k = r; k < R; ++k) x = fma(sLi[k * LS + r], scratch[ii * R + k], x);
     const int64_t i = i0 + ii;
-    double dm = 0.0, df = 0.0;
-    if (lane < R) {
-      a.A[i + In * lane] = b;
-      a.At[i * (R + (R & 1)) + lane] = b;
-      sX[ii * R + lane] = b;
-      dm = sM[ii * R + lane] * b;
-      df = (a.F != nullptr) ? a.F[i + In * lane] * b : 0.0;
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      dm += __shfl_xor_sync(0xffffffffu, dm, off);
-      df += __shfl_xor_sync(0xffffffffu, df, off);
-    }
-    if (lane == 0) {
-      sB[ii * R] = dm;  // reuse: row dots (rhs no longer needed for this row)
-      sM[ii * R] = df;
-    }
+    a.A[i + In * r] = x;
+    a.At[i * (R + (R & 1)) + r] = x;
+    sX[e] = x;
+    dm = fma(sM[e], x, dm);
+    if (a.F != nullptr) df = fma(a.F[i + In * r], x, df);
   }
-  __syncthreads();
   // partial Gram of the new rows, and the CTA's <M,A>, <F,A> (fixed order)
+  const double dms = block_sum_256(dm, scratch);
+  const double dfs = block_sum_256(df, scratch);
   for (int e = tid; e < RR; e += blockDim.x) {
     const int r = e % R, s = e / R;
-    double g = 0.0;
-    for (int ii = 0; ii < nrows; ++ii) g = fma(sX[ii * R + r], sX[ii * R + s], g);
-    a.gcur[(int64_t)blockIdx.x * RR + e] = g;
+    double gg = 0.0;
+    for (int ii = 0; ii < nrows; ++ii) gg = fma(sX[ii * R + r], sX[ii * R + s], gg);
+    a.gcur[(int64_t)blockIdx.x * RR + e] = gg;
   }
   if (tid == 0) {
-    double dm = 0.0, df = 0.0;
-    for (int ii = 0; ii < nrows; ++ii) {
-      dm += sB[ii * R];
-      df += sM[ii * R];
-    }
-    a.dotM[blockIdx.x] = dm;
-    a.dotF[blockIdx.x] = df;
+    a.dotM[blockIdx.x] = dms;
+    a.dotF[blockIdx.x] = dfs;
   }
 }
 
 // ---------------------------------------------------------------- sweep finalize: f, f_tilde
-__global__ void finalize_sweep_kernel(const FinalizeArgs a) {
-  __shared__ double sUp[32 * 32];
+__global__ void __launch_bounds__(256) finalize_sweep_kernel(const FinalizeArgs a) {
   __shared__ double sred[256];
   const int R = a.R, RR = R * R, tid = threadIdx.x;
   if (a.status[0] != 0.0) {
@@ -233,30 +287,24 @@ __global__ void finalize_sweep_kernel(const FinalizeArgs a) {
     }
     return;
   }
-  for (int e = tid; e < RR; e += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < a.nlast; ++c) s += a.glast[(int64_t)c * RR + e];
-    sUp[e] = s;
-    a.Ups[(int64_t)(a.N - 1) * RR + e] = s;
-  }
-  __syncthreads();
-  // ||[[A]]||^2 = 1^T (*_k Upsilon^(k)) 1
+  // Upsilon^(N) from the last solve's partials; ||[[A]]||^2 = 1^T (*_k Upsilon^(k)) 1
   double m2 = 0.0;
   for (int e = tid; e < RR; e += blockDim.x) {
-    double p = sUp[e];
+    const double u = sum_strided(a.glast + e, RR, a.nlast);
+    a.Ups[(int64_t)(a.N - 1) * RR + e] = u;
+    double p = u;
     for (int k = 0; k < a.N - 1; ++k) p *= a.Ups[(int64_t)k * RR + e];
     m2 += p;
   }
-  sred[tid] = m2;
-  __syncthreads();
+  const double model2 = block_sum_256(m2, sred);
+  double in = 0.0;
+  for (int c = tid; c < a.nlast; c += blockDim.x) in += a.dotM_last[c];
+  const double inner = block_sum_256(in, sred);
+  double fl = 0.0;
+  for (int n = 0; n < a.N; ++n)
+    for (int c = tid; c < a.nsolve[n]; c += blockDim.x) fl += a.dotF[(int64_t)n * a.dot_stride + c];
+  const double fa = block_sum_256(fl, sred);
   if (tid == 0) {
-    double model2 = 0.0;
-    for (int t = 0; t < blockDim.x; ++t) model2 += sred[t];
-    double inner = 0.0;
-    for (int c = 0; c < a.nlast; ++c) inner += a.dotM_last[c];
-    double fa = 0.0;
-    for (int n = 0; n < a.N; ++n)
-      for (int c = 0; c < a.nsolve[n]; ++c) fa += a.dotF[(int64_t)n * a.dot_stride + c];
     const double f = 0.5 * a.normZ2[0] - inner + 0.5 * model2;
     a.out[0] = f;
     a.out[1] = f - fa;
@@ -269,49 +317,51 @@ __global__ void finalize_sweep_kernel(const FinalizeArgs a) {
 // G^(n)(i,r) = -M(i,r) + sum_s A(i,s) Gamma(s,r) - F(i,r)   (eq:gradEqn; FAS residual with F)
 __global__ void __launch_bounds__(256) gradient_kernel(const GradArgs a) {
   __shared__ double sG[32 * 32];
-  __shared__ double sred[256];
+  __shared__ double sM[256], scratch[256];
   const int R = a.R, RR = R * R, tid = threadIdx.x;
   for (int e = tid; e < RR; e += blockDim.x) {
     double gm = 1.0;
     for (int k = 0; k < a.N; ++k)
-      if (k != a.mode) gm *= a.Ups[(int64_t)k * RR + e];
+      if (k != a.mode) gm *= prep_gram(a.pg, k, e, RR);
     sG[e] = gm;
   }
-  __syncthreads();
   const int64_t In = a.In;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + tid;
-  double g2 = 0.0;
-  if (idx < In * R) {
-    const int64_t i = idx % In;
-    const int r = (int)(idx / In);
-    double gv = -reduce_entry(a.rg, i, r);
-    for (int s = 0; s < R; ++s) gv = fma(a.A[i + In * s], sG[s + R * r], gv);
-    if (a.F != nullptr) gv -= a.F[idx];
-    if (a.G != nullptr) a.G[idx] = gv;
-    g2 = gv * gv;
-  }
-  sred[tid] = g2;
+  const int64_t i0 = (int64_t)blockIdx.x * a.rpc;
+  const int nrows = (int)((In - i0) < a.rpc ? (In - i0) : a.rpc);
+  gather_rows(a.rg, i0, nrows, R, a.sp, sM, scratch);
   __syncthreads();
-  for (int off = 128; off > 0; off >>= 1) {
-    if (tid < off) sred[tid] += sred[tid + off];
-    __syncthreads();
+  double g2 = 0.0;
+  for (int e = tid; e < nrows * R; e += blockDim.x) {
+    const int ii = e / R, r = e - (e / R) * R;
+    const int64_t i = i0 + ii;
+    double gv = -sM[e];
+    for (int s = 0; s < R; ++s) gv = fma(a.A[i + In * s], sG[s + R * r], gv);
+    if (a.F != nullptr) gv -= a.F[i + In * r];
+    if (a.G != nullptr) a.G[i + In * r] = gv;
+    g2 = fma(gv, gv, g2);
   }
-  if (tid == 0) a.gpart[blockIdx.x] = sred[0];
+  const double t = block_sum_256(g2, scratch);
+  if (tid == 0) a.gpart[blockIdx.x] = t;
 }
 
-__global__ void finalize_fit_kernel(const FitFinalArgs a) {
-  if (threadIdx.x != 0) return;
-  double res = 0.0;
-  for (int c = 0; c < a.nresid; ++c) res += a.resid[c];
+__global__ void __launch_bounds__(256) finalize_fit_kernel(const FitFinalArgs a) {
+  __shared__ double sred[256];
+  const int tid = threadIdx.x;
+  double rs = 0.0;
+  for (int c = tid; c < a.nresid; c += blockDim.x) rs += a.resid[c];
+  const double res = block_sum_256(rs, sred);
   double tot = 0.0;
   for (int n = 0; n < a.N; ++n) {
     double s = 0.0;
-    for (int c = 0; c < a.ngrad[n]; ++c) s += a.gpart[(int64_t)n * a.gstride + c];
-    a.out[2 + n] = s;
-    tot += s;
+    for (int c = tid; c < a.ngrad[n]; c += blockDim.x) s += a.gpart[(int64_t)n * a.gstride + c];
+    const double sn = block_sum_256(s, sred);
+    if (tid == 0) a.out[2 + n] = sn;
+    tot += sn;
   }
-  a.out[0] = 0.5 * res;
-  a.out[1] = sqrt(tot) / sqrt(a.normZ2[0]);
+  if (tid == 0) {
+    a.out[0] = 0.5 * res;
+    a.out[1] = sqrt(tot) / sqrt(a.normZ2[0]);
+  }
 }
 
 // ---------------------------------------------------------------- ||Z||^2
@@ -338,12 +388,40 @@ __global__ void __launch_bounds__(512) norm2_kernel(const double *__restrict__ Z
   if (tid == 0) part[blockIdx.x] = sred[0];
 }
 
-__global__ void norm2_final_kernel(const double *part, int n, double *out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int c = 0; c < n; ++c) s += part[c];
-    out[0] = s;
+__global__ void __launch_bounds__(256) norm2_final_kernel(const double *part, int n, double *out) {
+  __shared__ double sred[256];
+  double s = 0.0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) s += part[c];
+  const double t = block_sum_256(s, sred);
+  if (threadIdx.x == 0) out[0] = t;
+}
+
+// ---------------------------------------------------------------- host-side launchers
+template <int R>
+static cudaError_t launch_solve_t(const SolveArgs &a, int grid, cudaStream_t st) {
+  solve_kernel_t<R><<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solve(const SolveArgs &a, int grid, cudaStream_t st) {
+  switch (a.R) {
+#define CPK_SOLVE_CASE(r) \
+  case r: return launch_solve_t<r>(a, grid, st);
+    CPK_SOLVE_CASE(1) CPK_SOLVE_CASE(2) CPK_SOLVE_CASE(3) CPK_SOLVE_CASE(4) CPK_SOLVE_CASE(5)
+    CPK_SOLVE_CASE(6) CPK_SOLVE_CASE(7) CPK_SOLVE_CASE(8) CPK_SOLVE_CASE(9) CPK_SOLVE_CASE(10)
+    CPK_SOLVE_CASE(11) CPK_SOLVE_CASE(12) CPK_SOLVE_CASE(13) CPK_SOLVE_CASE(14) CPK_SOLVE_CASE(15)
+    CPK_SOLVE_CASE(16) CPK_SOLVE_CASE(17) CPK_SOLVE_CASE(18) CPK_SOLVE_CASE(19) CPK_SOLVE_CASE(20)
+    CPK_SOLVE_CASE(21) CPK_SOLVE_CASE(22) CPK_SOLVE_CASE(23) CPK_SOLVE_CASE(24) CPK_SOLVE_CASE(25)
+    CPK_SOLVE_CASE(26) CPK_SOLVE_CASE(27) CPK_SOLVE_CASE(28) CPK_SOLVE_CASE(29) CPK_SOLVE_CASE(30)
+    CPK_SOLVE_CASE(31) CPK_SOLVE_CASE(32)
+#undef CPK_SOLVE_CASE
+    default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_prep(const PrepArgs &a, cudaStream_t st) {
+  prep_kernel<<<a.blk_off[a.N], 256, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace cpk

@@ -7,8 +7,8 @@ namespace cpk {
 // Where the stream kernel left its partials, and how to sum them (fixed order).
 struct ReduceGeom {
   int R, Gc, RB, slots, mode0;  // mode0: partials are I1 x R per column group
-  int64_t I1, Q, Qn, In;  // In == 1 for mode 0
-  int64_t In_rows;        // rows of the output (I_mode)
+  int64_t I1, Q, Qn, In;
+  int64_t In_rows;  // rows of the output (I_mode)
   const double *part;
 };
 
@@ -28,27 +28,54 @@ inline ReduceGeom reduce_geom(const StreamPlan &p) {
   return g;
 }
 
+// Row blocking of the kernels that consume stream partials: sp threads per M entry (mode 0
+// has Gc partials per entry), rpc rows per 256-thread CTA.
+inline void row_blocking(const StreamPlan &p, int *rpc, int *sp) {
+  int s = 1;
+  if (p.mode == 0) {
+    s = p.Gc / 16;
+    if (s < 1) s = 1;
+    if (s > 8) s = 8;
+    while (s > 1 && p.R * s > 256) --s;
+  }
+  int r = 256 / (p.R * s);
+  if (r < 1) r = 1;
+  *sp = s;
+  *rpc = r;
+}
+
+constexpr int kPrepRows = 64;  // rows per prep block
+
 struct PrepArgs {
   int N, R;
+  int blk_off[CP_MAX_N + 1];  // first block of mode k (blk_off[N] = grid size)
   int64_t dims[CP_MAX_N];
   const double *A[CP_MAX_N];
   double *At[CP_MAX_N];
-  double *Ups;     // may be null (no Grams)
+  double *gpre;    // per-block partial Grams (may be null: no Grams)
   double *status;  // may be null
 };
 
+// Where the prep kernel left the partial Grams of the input factors.
+struct PrepGrams {
+  const double *gpre;
+  int blk_off[CP_MAX_N + 1];
+  int nblk[CP_MAX_N];
+};
+
 struct SolveArgs {
-  int N, R, mode, prev_mode, nprev, rpc;
+  int N, R, mode, prev_mode, nprev, rpc, sp;
   int64_t In;
   ReduceGeom rg;
-  const double *F;   // F^(mode) or null
-  double *A;         // A^(mode), column-major (output)
-  double *At;        // row-major copy (output)
-  double *Ups;       // N x R x R Gram totals
+  PrepGrams pg;
+  const double *F;      // F^(mode) or null
+  double *A;            // A^(mode), column-major (output)
+  double *At;           // row-major copy (output)
+  double *Ups;          // N x R x R Gram totals
   const double *gprev;  // previous mode's per-CTA partial Grams (null for mode 0)
-  double *gcur;      // this kernel's per-CTA partial Grams
+  double *gcur;         // this kernel's per-CTA partial Grams
   double *dotM, *dotF;  // per-CTA <M,A>, <F,A>
-  double *status;    // [0] status, [1] failed mode
+  double *status;       // [0] status, [1] failed mode
 };
 
 struct FinalizeArgs {
@@ -61,9 +88,10 @@ struct FinalizeArgs {
 };
 
 struct GradArgs {
-  int N, R, mode;
+  int N, R, mode, rpc, sp;
   int64_t In;
   ReduceGeom rg;
+  PrepGrams pg;
   const double *A, *F, *Ups;
   double *G, *gpart;
 };
@@ -75,13 +103,25 @@ struct FitFinalArgs {
   double *out;
 };
 
-__global__ void reduce_mttkrp_kernel(const ReduceGeom g, double *M);
-__global__ void prep_kernel(const PrepArgs a);
-__global__ void solve_kernel(const SolveArgs a);
+__global__ void reduce_mttkrp_kernel(const ReduceGeom g, int rpc, int sp, double *M);
 __global__ void finalize_sweep_kernel(const FinalizeArgs a);
 __global__ void gradient_kernel(const GradArgs a);
 __global__ void finalize_fit_kernel(const FitFinalArgs a);
 __global__ void norm2_kernel(const double *__restrict__ Z, int64_t P, double *part);
 __global__ void norm2_final_kernel(const double *part, int n, double *out);
+cudaError_t launch_solve(const SolveArgs &a, int grid, cudaStream_t st);
+cudaError_t launch_prep(const PrepArgs &a, cudaStream_t st);
+
+// Fill the prep block offsets for a shape (blocks of kPrepRows rows per mode).
+inline void prep_blocks(const cp_shape &s, PrepArgs &pa, PrepGrams &pg) {
+  int off = 0;
+  for (int k = 0; k < s.N; ++k) {
+    const int nb = (int)((s.dims[k] + kPrepRows - 1) / kPrepRows);
+    pa.blk_off[k] = pg.blk_off[k] = off;
+    pg.nblk[k] = nb;
+    off += nb;
+  }
+  pa.blk_off[s.N] = pg.blk_off[s.N] = off;
+}
 
 }  // namespace cpk

@@ -24,6 +24,12 @@ namespace cpk {
 
 constexpr int kHdrInts = 16;  // per-stage header: ncols, flags, slot, -, digits[kMaxDigits]
 
+// Register budget: up to this many accumulators per thread (V rows x R ranks) the kernel is
+// compiled for 2 CTAs/SM (<= 96 registers); above it for 1 CTA/SM.
+#ifndef CP_STREAM_2CTA_MAX_VR
+#define CP_STREAM_2CTA_MAX_VR 32
+#endif
+
 // Shared-memory carve-up of one CTA (all offsets in doubles except the tail).
 struct StreamSmem {
   double *zbuf, *abuf, *wbuf, *red, *sS;
@@ -31,7 +37,7 @@ struct StreamSmem {
   int *hdr;
 };
 
-template <int R>
+template <int R, int OP>
 __device__ __forceinline__ StreamSmem carve(unsigned char *raw, const StreamPlan &p) {
   constexpr int WSTR = (R % 2 == 0) ? R + 2 : R + 1;
   StreamSmem s;
@@ -39,12 +45,43 @@ __device__ __forceinline__ StreamSmem carve(unsigned char *raw, const StreamPlan
   s.abuf = s.zbuf + (size_t)p.nstages * p.cps * p.Wmax;
   s.wbuf = s.abuf + (size_t)p.nstages * p.cps * p.RS;
   s.red = s.wbuf + (size_t)p.nstages * p.cps * WSTR;
-  s.sS = s.red + kConsumerWarps * R + 8;
+  s.sS = s.red + stream_red_doubles(R, OP);
   s.full = reinterpret_cast<uint64_t *>(s.sS + 32);
   s.wready = s.full + p.nstages;
   s.empty = s.wready + p.nstages;
   s.hdr = reinterpret_cast<int *>(s.empty + p.nstages);
   return s;
+}
+
+// Consumer register tile: RT ranks per thread in RG rank groups.  MTTKRP with R > 12 splits
+// the ranks into groups of <= 8 (even RT: 16-B weight loads); R <= 12 and the residual pass
+// keep all R ranks in one thread.
+template <int R, int OP>
+struct StreamTile {
+  static constexpr int RG = stream_rg(R, OP);
+  static constexpr int RT = stream_rt(R, OP);
+};
+
+// Rows owned by consumer unit u of a column block of width Wb: V = 1: {u}; V >= 2: V/2 pairs
+// {2u, 2u+1} spaced 2*Wb/V apart (each 16-B load is contiguous across lanes).
+template <int V>
+__device__ __forceinline__ int row_of(int u, int v, int Wb) {
+  if (V == 1) return u;
+  return (v >> 1) * ((2 * Wb) / V) + 2 * u + (v & 1);
+}
+template <int V>
+__device__ __forceinline__ void load_rows(const double *zc, int u, int Wb, double (&z)[V]) {
+  if (V == 1) {
+    z[0] = zc[u];
+  } else {
+    const int sp = (2 * Wb) / V;
+#pragma unroll
+    for (int j = 0; j < V / 2; ++j) {
+      const double2 a = *reinterpret_cast<const double2 *>(zc + j * sp + 2 * u);
+      z[(2 * j) % V] = a.x;
+      z[(2 * j + 1) % V] = a.y;
+    }
+  }
 }
 
 // ------------------------------------------------------------------------ producer (warp 8)
@@ -87,7 +124,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
     mbar_wait(&sm.empty[stage], eph);
     double *zs = sm.zbuf + (size_t)stage * p.cps * p.Wmax;
     double *as = sm.abuf + (size_t)stage * p.cps * p.RS;
-    if (V == 2) {
+    if (V >= 2) {
       if (lane == 0) {
         mbar_expect_tx(&sm.full[stage],
                        (uint32_t)(ncols * Wb * 8 + (has_f0 ? ncols * p.RS * 8 : 0)));
@@ -194,11 +231,11 @@ __device__ void form_weights(const StreamPlan &p, int lane, const StreamSmem &sm
 }
 
 template <int R, int V, int OP>
-__global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1))
+__global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= CP_STREAM_2CTA_MAX_VR ? 2 : 1))
     stream_kernel(const __grid_constant__ StreamPlan p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int WSTR = (R % 2 == 0) ? R + 2 : R + 1;  // weight row stride (even: 16-B aligned)
-  const StreamSmem sm = carve<R>(smem_raw, p);
+  const StreamSmem sm = carve<R, OP>(smem_raw, p);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -229,17 +266,25 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1))
   }
 
   // ============================ consumer warps ============================
-  const int U = Wb / V;                                          // row units per column
-  const int cpt = (kConsumers / U) > 0 ? (kConsumers / U) : 1;  // columns per sub-tile
+  // Thread tile: V rows x RT ranks (register tiling: each shared-memory load feeds RT or V
+  // DFMAs).  Thread t -> (u, g, sl): row unit u (fastest, coalesced), rank group g, column
+  // slot sl.  Threads of one column: U * RG; columns per sub-tile: cpt.
+  constexpr int RG = StreamTile<R, OP>::RG;
+  constexpr int RT = StreamTile<R, OP>::RT;
+  const int U = Wb / V;
+  const int tpc = U * RG;
+  const int cpt = (kConsumers / tpc) > 0 ? (kConsumers / tpc) : 1;
   const int u = tid % U;
-  const int sl = tid / U;
+  const int g = (tid / U) % RG;
+  const int sl = tid / tpc;
   const bool active = sl < cpt;
+  const int r0 = g * RT;  // first rank of this thread
 
-  double acc[V][R];
+  double acc[V][RT];
 #pragma unroll
   for (int v = 0; v < V; ++v)
 #pragma unroll
-    for (int r = 0; r < R; ++r) acc[v][r] = 0.0;
+    for (int r = 0; r < RT; ++r) acc[v][r] = 0.0;
 
   double arow[OP == OP_RESID ? V : 1][OP == OP_RESID ? R : 1];
   if (OP == OP_RESID) {
@@ -247,14 +292,14 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1))
     for (int v = 0; v < V; ++v)
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        arow[v][r] = active ? __ldg(p.At[0] + (row0 + u * V + v) * p.RS + r) : 0.0;
+        arow[v][r] = active ? __ldg(p.At[0] + (row0 + row_of<V>(u, v, Wb)) * p.RS + r) : 0.0;
   }
 
   int stage = 0;
   uint32_t fph = 0;
   for (;;) {
     mbar_wait(&sm.wready[stage], fph);
-    mbar_wait(&sm.full[stage], fph);
+    // (the weight warp observed full[stage] before arriving on wready: the TMA bytes are visible)
     const int *h = sm.hdr + stage * kHdrInts;
     const int ncols = h[0];
     const int flags = h[1];
@@ -264,29 +309,21 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1))
     if (active) {
       for (int col = sl; col < ncols; col += cpt) {
         double z[V];
-        if (V == 2) {
-          const double2 zz = *reinterpret_cast<const double2 *>(zs + (size_t)col * Wb + 2 * u);
-          z[0] = zz.x;
-          z[V - 1] = zz.y;
-        } else {
-          z[0] = zs[(size_t)col * Wb + u];
-        }
-        const double *w = wsb + col * WSTR;
+        load_rows<V>(zs + (size_t)col * Wb, u, Wb, z);
+        const double *w = wsb + col * WSTR + r0;
         if (OP == OP_MTTKRP) {
+          double wr[RT];
 #pragma unroll
-          for (int r = 0; r + 1 < R; r += 2) {
+          for (int r = 0; r + 1 < RT; r += 2) {
             const double2 ww = *reinterpret_cast<const double2 *>(w + r);
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              acc[v][r] = fma(z[v], ww.x, acc[v][r]);
-              acc[v][r + 1] = fma(z[v], ww.y, acc[v][r + 1]);
-            }
+            wr[r] = ww.x;
+            wr[r + 1] = ww.y;
           }
-          if (R & 1) {
-            const double wl = w[R - 1];
+          if (RT & 1) wr[RT - 1] = w[RT - 1];
 #pragma unroll
-            for (int v = 0; v < V; ++v) acc[v][R - 1] = fma(z[v], wl, acc[v][R - 1]);
-          }
+          for (int v = 0; v < V; ++v)
+#pragma unroll
+            for (int r = 0; r < RT; ++r) acc[v][r] = fma(z[v], wr[r], acc[v][r]);
         } else {
           double x[V];
 #pragma unroll
@@ -322,36 +359,53 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1))
 
     if (OP == OP_MTTKRP && p.mode != 0 && (flags & 1)) {
       // ---- end of an i_m segment: contract with A^(1) rows and reduce over the CTA ----
-      double pr[R];
+      double pr[RT];
 #pragma unroll
-      for (int r = 0; r < R; ++r) pr[r] = 0.0;
+      for (int r = 0; r < RT; ++r) pr[r] = 0.0;
       if (active) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          const double *a1 = p.At[0] + (row0 + u * V + v) * p.RS;
+          const double *a1 = p.At[0] + (row0 + row_of<V>(u, v, Wb)) * p.RS + r0;
 #pragma unroll
-          for (int r = 0; r < R; ++r) pr[r] = fma(__ldg(a1 + r), acc[v][r], pr[r]);
+          for (int r = 0; r < RT; ++r)
+            if (r0 + r < R) pr[r] = fma(__ldg(a1 + r), acc[v][r], pr[r]);
         }
       }
 #pragma unroll
       for (int v = 0; v < V; ++v)
 #pragma unroll
-        for (int r = 0; r < R; ++r) acc[v][r] = 0.0;
+        for (int r = 0; r < RT; ++r) acc[v][r] = 0.0;
+      if (U % 32 == 0) {
+        // every lane of a warp shares (g, sl): warp shuffles, then one row per warp
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
+        for (int r = 0; r < RT; ++r) {
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) pr[r] += __shfl_xor_sync(0xffffffffu, pr[r], off);
-      }
-      if (lane == 0) {
+          for (int off = 16; off > 0; off >>= 1) pr[r] += __shfl_xor_sync(0xffffffffu, pr[r], off);
+        }
+        if (lane == 0) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) sm.red[warp * R + r] = pr[r];
-      }
-      named_bar_sync(1, kConsumers);
-      if (tid < R) {
-        double sum = 0.0;
+          for (int r = 0; r < RT; ++r) sm.red[warp * RT + r] = pr[r];
+        }
+        named_bar_sync(1, kConsumers);
+        if (tid < R) {
+          const int gr = tid / RT, rr = tid - (tid / RT) * RT;
+          double sum = 0.0;
+          for (int w8 = 0; w8 < kConsumerWarps; ++w8)
+            if (((w8 * 32) / U) % RG == gr) sum += sm.red[w8 * RT + rr];
+          p.part[((int64_t)blockIdx.x * p.slots + slot) * R + tid] = sum;
+        }
+      } else {
+        // generic: every thread's partial through shared memory, summed in thread order
 #pragma unroll
-        for (int w8 = 0; w8 < kConsumerWarps; ++w8) sum += sm.red[w8 * R + tid];
-        p.part[((int64_t)blockIdx.x * p.slots + slot) * R + tid] = sum;
+        for (int r = 0; r < RT; ++r) sm.red[tid * RT + r] = pr[r];
+        named_bar_sync(1, kConsumers);
+        if (tid < R) {
+          const int gr = tid / RT, rr = tid - (tid / RT) * RT;
+          double sum = 0.0;
+          for (int t = 0; t < kConsumers; ++t)
+            if ((t / U) % RG == gr) sum += sm.red[t * RT + rr];
+          p.part[((int64_t)blockIdx.x * p.slots + slot) * R + tid] = sum;
+        }
       }
       named_bar_sync(1, kConsumers);
     }
@@ -364,19 +418,21 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1))
     if (cpt > 1) {
       named_bar_sync(1, kConsumers);  // every consumer is past the ring: reuse it
       double *sred = sm.zbuf;         // Wb x R
-      for (int s = 1; s < cpt; ++s) {
-        if (active && sl == s) {
+      for (int s2 = 1; s2 < cpt; ++s2) {
+        if (active && sl == s2) {
 #pragma unroll
           for (int v = 0; v < V; ++v)
 #pragma unroll
-            for (int r = 0; r < R; ++r) sred[(u * V + v) + Wb * r] = acc[v][r];
+            for (int r = 0; r < RT; ++r)
+              if (r0 + r < R) sred[row_of<V>(u, v, Wb) + Wb * (r0 + r)] = acc[v][r];
         }
         named_bar_sync(1, kConsumers);
         if (sl == 0) {
 #pragma unroll
           for (int v = 0; v < V; ++v)
 #pragma unroll
-            for (int r = 0; r < R; ++r) acc[v][r] += sred[(u * V + v) + Wb * r];
+            for (int r = 0; r < RT; ++r)
+              if (r0 + r < R) acc[v][r] += sred[row_of<V>(u, v, Wb) + Wb * (r0 + r)];
         }
         named_bar_sync(1, kConsumers);
       }
@@ -385,7 +441,8 @@ __global__ void __launch_bounds__(kStreamThreads, (R <= 16 ? 2 : 1))
 #pragma unroll
       for (int v = 0; v < V; ++v)
 #pragma unroll
-        for (int r = 0; r < R; ++r) out[row0 + u * V + v + p.I1 * r] = acc[v][r];
+        for (int r = 0; r < RT; ++r)
+          if (r0 + r < R) out[row0 + row_of<V>(u, v, Wb) + p.I1 * (r0 + r)] = acc[v][r];
     }
   } else if (OP == OP_RESID) {
     double sacc = 0.0;
