@@ -125,20 +125,22 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
     double *zs = sm.zbuf + (size_t)stage * p.cps * p.Wmax;
     double *as = sm.abuf + (size_t)stage * p.cps * p.RS;
     if (V >= 2) {
-      if (lane == 0) {
+      if (lane == 0)
         mbar_expect_tx(&sm.full[stage],
                        (uint32_t)(ncols * Wb * 8 + (has_f0 ? ncols * p.RS * 8 : 0)));
-        // Z columns: q advances by qsd[0] per column within a stage (digit 0 only)
-        if (p.RB == 1 && p.qsd[0] == 1) {
-          bulk_g2s(zs, p.Z + q0 * p.I1, (uint32_t)(ncols * Wb * 8), &sm.full[stage]);
-        } else {
-          for (int col = 0; col < ncols; ++col)
-            bulk_g2s(zs + (size_t)col * Wb, p.Z + (q0 + col * p.qsd[0]) * p.I1 + row0,
-                     (uint32_t)(Wb * 8), &sm.full[stage]);
-        }
-        if (has_f0)
-          bulk_g2s(as, A0 + (int64_t)B[0] * p.RS, (uint32_t)(ncols * p.RS * 8), &sm.full[stage]);
+      __syncwarp();
+      // Z columns: q advances by qsd[0] per column within a stage (digit 0 only).  Strided
+      // columns are issued by all 32 lanes (one bulk copy per column).
+      if (p.RB == 1 && p.qsd[0] == 1) {
+        if (lane == 0) bulk_g2s(zs, p.Z + q0 * p.I1, (uint32_t)(ncols * Wb * 8), &sm.full[stage]);
+      } else {
+        for (int col = lane; col < ncols; col += 32)
+          bulk_g2s(zs + (size_t)col * Wb, p.Z + (q0 + col * p.qsd[0]) * p.I1 + row0,
+                   (uint32_t)(Wb * 8), &sm.full[stage]);
       }
+      if (has_f0 && lane == 31)
+        bulk_g2s(as, A0 + (int64_t)B[0] * p.RS, (uint32_t)(ncols * p.RS * 8), &sm.full[stage]);
+      __syncwarp();
     } else {
       // scalar fallback (odd I1: columns are not 16-B aligned): the warp copies elements
       for (int col = 0; col < ncols; ++col) {
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    if (V == 1 || lane == 0) produce<R, V>(p, lane, v0, v1, row0, Wb, sm);
+    produce<R, V>(p, lane, v0, v1, row0, Wb, sm);
     return;
   }
   if (warp == kConsumerWarps + 1) {
