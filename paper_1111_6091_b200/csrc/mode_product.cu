@@ -4,11 +4,17 @@
 // fastest this is a strided batched GEMM over the trailing modes:
 //   mode 0:      X (J x Q)            = U (J x I1)  * Z (I1 x Q)                  batch 1
 //   mode n > 0:  X_b (left x J)       = Z_b (left x I_n) * U^T (I_n x J)          batch b < right
-// fp64 DFMA register-tiled GEMM (64 x 64 x 16 tiles, 4 x 4 outputs per thread, register
-// prefetch of the next k-tile).  FP64 tensor cores (DMMA) are a later, measured variant.
+// Two kernels: the fp64 tensor-core (DMMA) GEMM below is the default -- measured 1.5x faster
+// than the DFMA register-tiled GEMM (c4a: 26.5 vs 17.1 TFLOP/s, c3: 23 vs 16; profiles/), which
+// stays available with CP_MODEPROD_DMMA=0.
+#include <cstdlib>
+
 #include "cp_internal.cuh"
 
 namespace cpk {
+
+cudaError_t launch_mode_product_dfma(int N, const int64_t *dims, const double *Z, int mode,
+                                     const double *U, int64_t J, double *X, cudaStream_t st);
 
 struct GemmArgs {
   int64_t M, N, K, batch;
@@ -110,8 +116,166 @@ __global__ void __launch_bounds__(256) gemm_f64_kernel(const GemmArgs g) {
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// FP64 tensor-core variant (legacy mma.sync.m8n8k4.f64 -> SASS DMMA; tcgen05 has no fp64 kind).
+// CTA tile 64 x 128 x 16, 8 warps in a 2 x 4 grid, warp tile 32 x 32 = 4 x 4 m8n8 fragments.
+// Operand tiles are kept in shared memory in their global orientation (A_MC: A contiguous
+// along m, else along k; B_NC: B contiguous along n, else along k) with padded strides that make
+// the fragment reads bank-conflict free (two 128-B wavefronts per 256-B fragment).
+constexpr int TBM = 64, TBN = 128, TBK = 16;
+constexpr int AMS = TBM + 8, AKS = TBK + 4, BNS = TBN + 8, BKS = TBK + 4;
+
+__device__ __forceinline__ void dmma_m8n8k4(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <bool A_MC, bool B_NC>
+__global__ void __launch_bounds__(256) gemm_dmma_kernel(const GemmArgs g) {
+  __shared__ double As[1][A_MC ? TBK * AMS : TBM * AKS];  // single buffer + register prefetch
+  __shared__ double Bs[1][B_NC ? TBK * BNS : TBN * BKS];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps
+  const int gq = lane >> 2, tq = lane & 3;  // fragment coordinates
+  const int64_t bm = (int64_t)(g.swap ? blockIdx.y : blockIdx.x) * TBM;
+  const int64_t bn = (int64_t)(g.swap ? blockIdx.x : blockIdx.y) * TBN;
+  const int64_t b = blockIdx.z;
+  const double *A = g.A + b * g.sab;
+  const double *B = g.B + b * g.sbb;
+  double *C = g.C + b * g.scb;
+
+  double ra[4], rb[8];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int mm, kk;
+      if (A_MC) { mm = t & 63; kk = (t >> 6) + 4 * j; }
+      else { kk = t & 15; mm = (t >> 4) + 16 * j; }
+      const int64_t m = bm + mm, k = k0 + kk;
+      ra[j] = (m < g.M && k < g.K) ? __ldg(A + m * g.sam + k * g.sak) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int nn, kk;
+      if (B_NC) { nn = t & 127; kk = (t >> 7) + 2 * j; }
+      else { kk = t & 15; nn = (t >> 4) + 16 * j; }
+      const int64_t n = bn + nn, k = k0 + kk;
+      rb[j] = (n < g.N && k < g.K) ? __ldg(B + k * g.sbk + n * g.sbn) : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (A_MC) As[buf][((t >> 6) + 4 * j) * AMS + (t & 63)] = ra[j];
+      else As[buf][((t >> 4) + 16 * j) * AKS + (t & 15)] = ra[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (B_NC) Bs[buf][((t >> 7) + 2 * j) * BNS + (t & 127)] = rb[j];
+      else Bs[buf][((t >> 4) + 16 * j) * BKS + (t & 15)] = rb[j];
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  load(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = 0; k0 < g.K; k0 += TBK) {
+    const bool more = (k0 + TBK < g.K);
+    if (more) load(k0 + TBK);
+#pragma unroll
+    for (int ks = 0; ks < TBK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int m = wm * 32 + i * 8 + gq, k = ks + tq;
+        af[i] = A_MC ? As[buf][k * AMS + m] : As[buf][m * AKS + k];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n = wn * 32 + j * 8 + gq, k = ks + tq;
+        bf[j] = B_NC ? Bs[buf][k * BNS + n] : Bs[buf][n * BKS + k];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    if (more) {
+      __syncthreads();  // every warp is done reading the tile
+      store(buf);
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t m = bm + wm * 32 + i * 8 + gq;
+        const int64_t n = bn + wn * 32 + j * 8 + 2 * tq + h;
+        if (m < g.M && n < g.N) C[m * g.scm + n * g.scn] = acc[i][j][h];
+      }
+}
+
+static int env_flag(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
 cudaError_t launch_mode_product(int N, const int64_t *dims, const double *Z, int mode,
                                 const double *U, int64_t J, double *X, cudaStream_t st) {
+  if (env_flag("CP_MODEPROD_DMMA", 1)) {
+    int64_t left = 1, right = 1;
+    for (int k = 0; k < mode; ++k) left *= dims[k];
+    for (int k = mode + 1; k < N; ++k) right *= dims[k];
+    const int64_t In = dims[mode];
+    GemmArgs g;
+    bool a_mc, b_nc;
+    if (mode == 0) {
+      g.M = J; g.N = right; g.K = In; g.batch = 1;
+      g.A = U; g.sam = 1; g.sak = J; g.sab = 0;
+      g.B = Z; g.sbk = 1; g.sbn = In; g.sbb = 0;
+      g.C = X; g.scm = 1; g.scn = J; g.scb = 0;
+      a_mc = true; b_nc = false;
+    } else {
+      g.M = left; g.N = J; g.K = In; g.batch = right;
+      g.A = Z; g.sam = 1; g.sak = left; g.sab = left * In;
+      g.B = U; g.sbk = J; g.sbn = 1; g.sbb = 0;
+      g.C = X; g.scm = 1; g.scn = left; g.scb = left * J;
+      a_mc = true; b_nc = true;
+    }
+    const int64_t gx = (g.M + TBM - 1) / TBM, gy = (g.N + TBN - 1) / TBN;
+    g.swap = (gy > gx) ? 1 : 0;
+    const int64_t gbig = g.swap ? gy : gx, gsmall = g.swap ? gx : gy;
+    if (gsmall > 65535 || gbig > 0x7fffffff) return cudaErrorInvalidConfiguration;
+    for (int64_t b0 = 0; b0 < g.batch; b0 += 65535) {
+      GemmArgs gb = g;
+      gb.batch = (g.batch - b0) < 65535 ? (g.batch - b0) : 65535;
+      gb.A = g.A + b0 * g.sab;
+      gb.B = g.B + b0 * g.sbb;
+      gb.C = g.C + b0 * g.scb;
+      dim3 grid((unsigned)gbig, (unsigned)gsmall, (unsigned)gb.batch);
+      if (a_mc && b_nc) gemm_dmma_kernel<true, true><<<grid, 256, 0, st>>>(gb);
+      else gemm_dmma_kernel<true, false><<<grid, 256, 0, st>>>(gb);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  return launch_mode_product_dfma(N, dims, Z, mode, U, J, X, st);
+}
+
+cudaError_t launch_mode_product_dfma(int N, const int64_t *dims, const double *Z, int mode,
+                                     const double *U, int64_t J, double *X, cudaStream_t st) {
   int64_t left = 1, right = 1;
   for (int k = 0; k < mode; ++k) left *= dims[k];
   for (int k = mode + 1; k < N; ++k) right *= dims[k];
