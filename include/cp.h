@@ -142,6 +142,58 @@ int cp_last_launch_count(void);
 int cp_profile_enable(int enable);
 int cp_profile_read(int64_t *launches, double *total_ms, double *alg_bytes);
 
+/* ---------------------------------------------------------------------------------------
+ * Normalization and ordering of the factors (eq:ALSnorm P:122-125; sort P:126):
+ *   lambda_r = (prod_n ||a_r^(n)||)^{1/N},  a_r^(n) <- lambda_r a_r^(n) / ||a_r^(n)||;
+ *   a component with a zero column is left unchanged (lambda_r = 0);
+ *   if sort != 0 the components are reordered by decreasing lambda (stable).
+ *   A [host] N device pointers (in/out);  lambda: device, R doubles, or NULL.
+ *   Workspace: cp_workspace_bytes(s) suffices. */
+int cp_normalize_sort(const cp_shape *s, double *const *A, int32_t sort, double *lambda, void *ws,
+                      size_t ws_bytes, cp_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Multigrid driver (host C++ on top of the calls above):
+ * the BAMG setup V-cycle CP-AMG-mult (Algorithm 1) with geometric coarsening
+ * and weighted least-squares interpolation (eq:LSQinterp, eq:interpweights
+ * P:236-247), the Cholesky-transformed Galerkin coarse tensors (eq:ctensor_transformed), the
+ * CP-FAS solve V-cycle (Algorithm 2), FMG-CP-FAS (Algorithm 3) and the
+ * setup/solve combination with the stagnation rules of P:486-492.  Every level's work runs in
+ * the kernels of this library; the host builds P, B = P^T P, its Cholesky factor and
+ * Phat = P L^{-T} (O(I * I_c)) and reads g once per cycle.  This call synchronizes the stream. */
+typedef struct {
+    int32_t nu1_setup, nu2_setup, nuc_setup, n_test; /* Table 1: 5, 5, 100, 2 */
+    int32_t nu1_solve, nu2_solve, nuc_solve;          /* 1, 1, 50 */
+    int32_t max_setup_cycles, min_setup_cycles;       /* 5, 3 */
+    double stagnation_eps;                            /* 0.1 (eq:stagnation) */
+    int32_t use_fmg, nu_fmg;                          /* "Multilevel + FMG"; coarsest ALS its */
+    int32_t max_cycles;                               /* 500 multilevel iterations */
+    double tol;                                       /* tau (1e-10) */
+    int32_t coarsest;                                 /* I_coarsest; 0 = 2R (reading R16) */
+    int32_t solve_stagnation_after;                   /* 5 */
+    int32_t max_trace;                                /* rows of the trace buffer */
+} cp_mg_params;
+
+void cp_mg_default_params(cp_mg_params *p);
+size_t cp_mg_workspace_bytes(const cp_shape *s, const cp_mg_params *p);
+/* Z: finest tensor;  A: [host] N device pointers, boot factor matrices (initial guess in,
+ * solution out);  T: [host] n_test*N device pointers, initial test factor matrices (block t,
+ * mode n at T[t*N + n]; read only);  A_fmg: [host] N device pointers to the coarsest-level
+ * random initial guess of FMG (ignored unless use_fmg);  report [host, 16 doubles]:
+ *   0 g, 1 f, 2 cycles (setup + FMG + solve), 3 setup cycles, 4 solve cycles, 5 levels,
+ *   6 status (0 converged, 1 cycle limit, CP_ENOTSPD), 7 trace rows, 8 rebuilds, 9 seconds;
+ * trace [host, max_trace x 4]: phase (0 setup, 1 FMG, 2 solve), cycle, g, seconds. */
+int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const double *const *T,
+                const double *const *A_fmg, const cp_mg_params *prm, double *report, double *trace,
+                void *ws, size_t ws_bytes, cp_stream_t stream);
+
+/* Standalone ALS (the paper's baseline): sweeps with normalization until g < tol or
+ * max_iters; g is evaluated every `check_every` sweeps.  report [host, 8]: 0 g, 1 f,
+ * 2 iterations, 3 status (0 converged, 1 iteration limit, CP_ENOTSPD), 4 seconds. */
+size_t cp_als_solve_workspace_bytes(const cp_shape *s);
+int cp_als_solve(const cp_shape *s, const double *Z, double *const *A, double tol, int32_t max_iters,
+                 int32_t check_every, double *report, void *ws, size_t ws_bytes, cp_stream_t stream);
+
 const char *cp_status_string(int code);
 int cp_version(void);
 

@@ -59,6 +59,8 @@ def lib():
         L.oracle_gradient.argtypes = [I, LP, I, DP, D, PP, PP, DP, PP]
         L.oracle_mode_product.argtypes = [I, LP, DP, I, DP, I64, DP]
         L.oracle_normalize_sort.argtypes = [I, LP, I, PP, DP]
+        L.oracle_normalize.argtypes = [I, LP, I, PP, DP, I]
+        L.oracle_normalize.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [I]
         L.oracle_set_threads.restype = None
         for name in ["oracle_mttkrp_rows", "oracle_mttkrp", "oracle_gram", "oracle_gamma",
@@ -212,10 +214,11 @@ def mode_product(Z, dims, mode, U):
     return X.reshape(list(reversed(nd))), nd
 
 
-def normalize_sort(dims, A):
+def normalize_sort(dims, A, sort=True):
+    """eq:ALSnorm normalization; sort=True also orders the components by decreasing lambda."""
     N = len(dims)
     R = A[0].shape[1]
     A = [np.array(_cm(a), order="F", copy=True) for a in A]
     lam = np.zeros(R)
-    lib().oracle_normalize_sort(N, _dims(dims), R, _ptr_array(A), _dp(lam))
+    lib().oracle_normalize(N, _dims(dims), R, _ptr_array(A), _dp(lam), 1 if sort else 0)
     return A, lam

@@ -392,7 +392,7 @@ int oracle_mode_product(int N, const int64_t *dims, const double *Z, int mode, c
  * lambda (R) receives the sorted lambdas.  A zero column leaves the factors unchanged
  * for that component (lambda_r = 0).
  */
-int oracle_normalize_sort(int N, const int64_t *dims, int R, double *const *A, double *lambda) {
+int oracle_normalize(int N, const int64_t *dims, int R, double *const *A, double *lambda, int sort) {
     if (check_shape(N, dims, R) || !A || !lambda) return OR_EINVAL;
     double *lam = (double *)malloc(sizeof(double) * (size_t)R);
     for (int r = 0; r < R; ++r) {
@@ -413,7 +413,7 @@ int oracle_normalize_sort(int N, const int64_t *dims, int R, double *const *A, d
     /* stable insertion sort of the component order by decreasing lambda */
     int *ord = (int *)malloc(sizeof(int) * (size_t)R);
     for (int r = 0; r < R; ++r) ord[r] = r;
-    for (int a = 1; a < R; ++a) {
+    for (int a = 1; sort && a < R; ++a) {
         int v = ord[a];
         int b = a - 1;
         while (b >= 0 && lam[ord[b]] < lam[v]) {
@@ -443,6 +443,10 @@ int oracle_num_threads(void) {
 #else
     return 1;
 #endif
+}
+
+int oracle_normalize_sort(int N, const int64_t *dims, int R, double *const *A, double *lambda) {
+    return oracle_normalize(N, dims, R, A, lambda, 1);
 }
 
 /* set the OpenMP thread count (tests check that results are bitwise thread-count independent) */

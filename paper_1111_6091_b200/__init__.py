@@ -201,6 +201,92 @@ def mode_product(Z, dims, mode, U, X=None, stream=None):
     return X, nd
 
 
+def normalize_sort(dims, A, sort=True, lam=None, ws=None, stream=None):
+    """eq:ALSnorm normalization (+ decreasing-lambda ordering) of the factors, in place."""
+    R = A[0].shape[1]
+    for k, a in enumerate(A):
+        _check_cm(a, dims[k], R, f"A[{k}]")
+    ws = _ws(ws, dims, R, A[0].device)
+    _check(lib().cp_normalize_sort(ctypes.byref(_shape(dims, R)), _ptr_array(A), ctypes.c_int32(1 if sort else 0),
+                                   _ptr(lam), _ptr(ws.buf), ctypes.c_size_t(ws.nbytes), _stream(stream)),
+           "cp_normalize_sort")
+    return A
+
+
+class MGParams(ctypes.Structure):
+    """cp_mg_params (include/cp.h); defaults = Table 1 of the paper."""
+    _fields_ = [("nu1_setup", ctypes.c_int32), ("nu2_setup", ctypes.c_int32), ("nuc_setup", ctypes.c_int32),
+                ("n_test", ctypes.c_int32), ("nu1_solve", ctypes.c_int32), ("nu2_solve", ctypes.c_int32),
+                ("nuc_solve", ctypes.c_int32), ("max_setup_cycles", ctypes.c_int32),
+                ("min_setup_cycles", ctypes.c_int32), ("stagnation_eps", ctypes.c_double),
+                ("use_fmg", ctypes.c_int32), ("nu_fmg", ctypes.c_int32), ("max_cycles", ctypes.c_int32),
+                ("tol", ctypes.c_double), ("coarsest", ctypes.c_int32), ("solve_stagnation_after", ctypes.c_int32),
+                ("max_trace", ctypes.c_int32)]
+
+    @classmethod
+    def default(cls, **kw):
+        p = cls()
+        lib().cp_mg_default_params(ctypes.byref(p))
+        for k, v in kw.items():
+            setattr(p, k, v)
+        return p
+
+
+def mg_levels(dims, R, coarsest=0):
+    """Level sizes of the hierarchy the driver builds (coarsen every mode with I_n > I_coarsest)."""
+    c = coarsest if coarsest > 0 else 2 * R
+    out = [tuple(int(d) for d in dims)]
+    while any(d > c for d in out[-1]):
+        out.append(tuple((d + 1) // 2 if d > c else d for d in out[-1]))
+    return out
+
+
+def mg_solve(Z, dims, A, T, A_fmg=None, params=None, stream=None):
+    """Multigrid CP solve (cp_mg_solve).  A: boot factors (in/out); T: list of n_test lists of N
+    test factor matrices; A_fmg: coarsest-level FMG initial guess (needed when use_fmg).
+    Returns (report dict, trace array)."""
+    import numpy as np
+    _check_Z(Z, dims)
+    N = len(dims)
+    R = A[0].shape[1]
+    params = params or MGParams.default()
+    if params.max_trace <= 0:
+        params.max_trace = 1024
+    flatT = [t for block in T for t in block]
+    if len(flatT) != params.n_test * N:
+        raise ValueError("T must hold n_test blocks of N factor matrices")
+    s = _shape(dims, R)
+    nbytes = int(lib().cp_mg_workspace_bytes(ctypes.byref(s), ctypes.byref(params)))
+    if nbytes == 0:
+        raise CPError(CP_EINVAL, "cp_mg_workspace_bytes")
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=Z.device)
+    report = (ctypes.c_double * 16)()
+    trace = (ctypes.c_double * (4 * params.max_trace))()
+    _check(lib().cp_mg_solve(ctypes.byref(s), _ptr(Z), _ptr_array(A), _ptr_array(flatT),
+                             _ptr_array(A_fmg) if A_fmg is not None else None, ctypes.byref(params),
+                             report, trace, _ptr(buf), ctypes.c_size_t(nbytes), _stream(stream)), "cp_mg_solve")
+    keys = ["g", "f", "cycles", "setup_cycles", "solve_cycles", "levels", "status", "trace_rows", "rebuilds",
+            "seconds", "fit_seconds"]
+    rep = {k: report[i] for i, k in enumerate(keys)}
+    tr = np.array(trace[: 4 * int(rep["trace_rows"])]).reshape(-1, 4)
+    return rep, tr
+
+
+def als_solve(Z, dims, A, tol=1e-10, max_iters=10000, check_every=1, stream=None):
+    """Standalone ALS with normalization until g < tol (cp_als_solve).  Returns a report dict."""
+    _check_Z(Z, dims)
+    R = A[0].shape[1]
+    s = _shape(dims, R)
+    nbytes = int(lib().cp_als_solve_workspace_bytes(ctypes.byref(s)))
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=Z.device)
+    report = (ctypes.c_double * 8)()
+    _check(lib().cp_als_solve(ctypes.byref(s), _ptr(Z), _ptr_array(A), ctypes.c_double(tol), ctypes.c_int32(max_iters),
+                              ctypes.c_int32(check_every), report, _ptr(buf), ctypes.c_size_t(nbytes),
+                              _stream(stream)), "cp_als_solve")
+    keys = ["g", "f", "iterations", "status", "seconds", "fit_seconds"]
+    return {k: report[i] for i, k in enumerate(keys)}
+
+
 def fit(Z, dims, A, normZ2, F=None, want_G=False, out=None, ws=None, stream=None):
     """f (direct), g and ||G^(n)||^2 at one iterate (cp_fit).  Returns (out, G list or None)."""
     _check_Z(Z, dims)

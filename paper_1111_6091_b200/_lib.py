@@ -13,8 +13,9 @@ _lib = None
 # every symbol include/cp.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = ["cp_workspace_bytes", "cp_norm2", "cp_mttkrp", "cp_als_sweep",
            "cp_mode_product_workspace_bytes", "cp_mode_product", "cp_fit",
-           "cp_last_launch_count", "cp_profile_enable", "cp_profile_read", "cp_status_string",
-           "cp_version"]
+           "cp_last_launch_count", "cp_profile_enable", "cp_profile_read", "cp_normalize_sort",
+           "cp_mg_default_params", "cp_mg_workspace_bytes", "cp_mg_solve",
+           "cp_als_solve_workspace_bytes", "cp_als_solve", "cp_status_string", "cp_version"]
 
 
 class CPError(RuntimeError):
@@ -59,6 +60,18 @@ def lib():
         L.cp_profile_enable.restype = ctypes.c_int
         L.cp_profile_read.argtypes = [vp, vp, vp]
         L.cp_profile_read.restype = ctypes.c_int
+        L.cp_normalize_sort.argtypes = [vp, vp, i32, vp, vp, sz, vp]
+        L.cp_normalize_sort.restype = ctypes.c_int
+        L.cp_mg_default_params.argtypes = [vp]
+        L.cp_mg_default_params.restype = None
+        L.cp_mg_workspace_bytes.argtypes = [vp, vp]
+        L.cp_mg_workspace_bytes.restype = sz
+        L.cp_mg_solve.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.cp_mg_solve.restype = ctypes.c_int
+        L.cp_als_solve_workspace_bytes.argtypes = [vp]
+        L.cp_als_solve_workspace_bytes.restype = sz
+        L.cp_als_solve.argtypes = [vp, vp, vp, ctypes.c_double, i32, i32, vp, vp, sz, vp]
+        L.cp_als_solve.restype = ctypes.c_int
         L.cp_status_string.argtypes = [ctypes.c_int]
         L.cp_status_string.restype = ctypes.c_char_p
         _lib = L

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "mg_kernels.cuh"
 #include "small_kernels.cuh"
 #include "stream_kernel.cuh"
 
@@ -539,6 +540,33 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
   finalize_fit_kernel<<<1, 256, 0, cs>>>(fa);
   CK_LAUNCH();
   g_launches = launches + 1;
+  return CP_OK;
+}
+
+int cp_normalize_sort(const cp_shape *s, double *const *A, int32_t sort, double *lambda, void *ws,
+                      size_t ws_bytes, cp_stream_t stream) {
+  g_launches = 0;
+  int st = check_shape(s, 1);
+  if (st) return st;
+  if (!A || !ws || !aligned(ws, 256)) return CP_EINVAL;
+  NormArgs a;
+  memset(&a, 0, sizeof(a));
+  a.N = s->N;
+  a.R = s->R;
+  a.sort = sort ? 1 : 0;
+  int64_t off = 0;
+  for (int n = 0; n < s->N; ++n) {
+    if (!A[n]) return CP_EINVAL;
+    a.dims[n] = s->dims[n];
+    a.A[n] = A[n];
+    a.off[n] = off;
+    off += s->dims[n] * s->R;
+  }
+  if ((size_t)off * sizeof(double) > ws_bytes) return CP_EWORKSPACE;
+  a.tmp = static_cast<double *>(ws);
+  a.lambda = lambda;
+  if (launch_normalize_sort(a, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess) return CP_ECUDA;
+  g_launches = 1;
   return CP_OK;
 }
 

@@ -8,22 +8,6 @@
 
 namespace cpk {
 
-// ---------------------------------------------------------------- block reduction (fixed tree)
-// blockDim.x == 256; returns the sum to every thread.
-__device__ double block_sum_256(double v, double *sred) {
-  const int tid = threadIdx.x;
-  __syncthreads();
-  sred[tid] = v;
-  __syncthreads();
-  for (int off = 128; off > 0; off >>= 1) {
-    if (tid < off) sred[tid] += sred[tid + off];
-    __syncthreads();
-  }
-  const double r = sred[0];
-  __syncthreads();
-  return r;
-}
-
 // sum of n strided values, 8 independent loads in flight, combined in a fixed order
 __device__ __forceinline__ double sum_strided(const double *p, int64_t stride, int n) {
   double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};

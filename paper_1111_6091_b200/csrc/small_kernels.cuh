@@ -4,6 +4,22 @@
 
 namespace cpk {
 
+// ---------------------------------------------------------------- block reduction (fixed tree)
+// blockDim.x == 256; returns the sum to every thread.
+__device__ __forceinline__ double block_sum_256(double v, double *sred) {
+  const int tid = threadIdx.x;
+  __syncthreads();
+  sred[tid] = v;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (tid < off) sred[tid] += sred[tid + off];
+    __syncthreads();
+  }
+  const double r = sred[0];
+  __syncthreads();
+  return r;
+}
+
 // Where the stream kernel left its partials, and how to sum them (fixed order).
 struct ReduceGeom {
   int R, Gc, RB, slots, mode0;  // mode0: partials are I1 x R per column group
