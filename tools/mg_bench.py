@@ -1,0 +1,55 @@
+"""Multigrid vs ALS solve times on a config (GPU).  python tools/mg_bench.py [c1|dense50] [R] [tol]"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import cpsynth  # noqa: E402
+import paper_1111_6091_b200 as cp  # noqa: E402
+
+
+def problem(name, R=None):
+    if name.startswith("dense"):
+        s = int(name[5:])
+        R = R or 3
+        dims = (s, s, s)
+        Z = cpsynth.dense_inverse_norm(s)
+        A0 = cpsynth.uniform_init(dims, R, seed=0)
+        T0 = [cpsynth.uniform_init(dims, R, seed=10 + t) for t in range(2)]
+        Af = cpsynth.uniform_init(cp.mg_levels(dims, R)[-1], R, seed=99)
+        return dims, R, Z, A0, T0, Af
+    d = cpsynth.make_config(name, with_transfer=False)
+    dims, R = d["dims"], d["R"]
+    T0 = [cpsynth.uniform_init(dims, R, seed=10 + t) for t in range(2)]
+    Af = cpsynth.uniform_init(cp.mg_levels(dims, R)[-1], R, seed=99)
+    return dims, R, d["Z"], d["A0"], T0, Af
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a.T)).cuda().t()
+
+
+def run(name, R=None, tol=1e-10, max_als=10000):
+    dims, R, Z, A0, T0, Af = problem(name, R)
+    Zd = torch.from_numpy(Z).cuda()
+    out = {"problem": name, "dims": list(dims), "R": R, "tol": tol}
+    for fmg in (0, 1):
+        Ad = [dev(a) for a in A0]
+        prm = cp.MGParams.default(use_fmg=fmg, tol=tol)
+        rep, tr = cp.mg_solve(Zd, dims, Ad, [[dev(t) for t in b] for b in T0], A_fmg=[dev(a) for a in Af], params=prm)
+        out["ml_fmg" if fmg else "ml"] = {k: rep[k] for k in ("g", "cycles", "setup_cycles", "solve_cycles", "levels",
+                                                              "status", "seconds", "fit_seconds")}
+    Ad = [dev(a) for a in A0]
+    out["als"] = cp.als_solve(Zd, dims, Ad, tol=tol, max_iters=max_als, check_every=1)
+    return out
+
+
+if __name__ == "__main__":
+    name = sys.argv[1] if len(sys.argv) > 1 else "c1"
+    R = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "-" else None
+    tol = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-10
+    run(name, R, tol)  # warm-up (kernel loading, plans)
+    print(json.dumps(run(name, R, tol)))
