@@ -84,7 +84,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   p.V = 1;
   for (int v : {8, 4, 2}) {
     if (v > vmax_env || p.I1 % v != 0) continue;
-    if (op == OP_MTTKRP && v * RT > vr_max && v > 2) continue;
+    if (op != OP_RESID && v * RT > vr_max && v > 2) continue;
     if (op == OP_RESID && (v > 4 || v * s.R > 64)) continue;
     p.V = v;
     break;
@@ -94,8 +94,12 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   // row-block width: mode 0 MTTKRP uses narrower blocks (fewer column groups -> smaller I1 x R
   // partials); every other pass keeps whole columns in one CTA.
   int64_t Wt = p.I1;
-  if (op == OP_MTTKRP && p.mode == 0) {
+  if (op != OP_RESID && p.mode == 0) {
     const int w0 = env_int("CP_MTTKRP_W0", 512);
+    if (p.I1 >= 2 * w0) Wt = w0;
+  }
+  if (op == OP_YL) {
+    const int w0 = env_int("CP_YL_W", 512);
     if (p.I1 >= 2 * w0) Wt = w0;
   }
   if (Wt > maxW) Wt = maxW;
@@ -149,8 +153,10 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   // mode-0 slot reduction reuses the Z ring: it must hold Wmax x R doubles
   while ((int64_t)nst * cps * p.Wmax < (int64_t)p.Wmax * s.R) ++nst;
   p.nstages = nst;
+  p.red_doubles = stream_red_doubles(s.R, op);
+  if (op == OP_YL && cpt > 1 && p.red_doubles < p.Wmax * s.R) p.red_doubles = p.Wmax * s.R;
   // ring | red | sS[32] | 3 x nst mbarriers | nst x 16-int headers
-  p.smem_bytes = (nst * stage_doubles + stream_red_doubles(s.R, op) + 32) * 8 + nst * 24 + nst * 64 + 64;
+  p.smem_bytes = (nst * stage_doubles + p.red_doubles + 32) * 8 + nst * 24 + nst * 64 + 64;
   if (p.smem_bytes > 200 * 1024) return false;
   const int occ = stream_occupancy(s.R, p.V, op, p.smem_bytes);
   const int ctas = env_int("CP_CTAS_PER_SM", 0);
@@ -217,6 +223,13 @@ struct Layout {
   int nsolve[CP_MAX_N], ngrad[CP_MAX_N];
   StreamPlan plans[CP_MAX_N];
   StreamPlan resid;
+  // dimension-tree sweep (N >= 3): pass 1 = OP_YL over Z (mode-1 segments), pass 2 = mode-2
+  // MTTKRP of Z viewed as I0 x I1 x J (J = prod_{k>=2} I_k)
+  bool tree;
+  StreamPlan yl_plan, p2_plan;
+  cp_shape s3;
+  int rpc2, sp2, nyr;
+  size_t yl, edge, mbuf, yr, segtab;
 };
 
 static size_t align_up(size_t x) { return (x + 31) & ~(size_t)31; }  // 256 B in doubles
@@ -242,6 +255,25 @@ static bool make_layout(Layout &L, const cp_shape &s) {
   for (int k = 0; k < s.N; ++k) L.prep_blocks += (int)ceil_div(s.dims[k], kPrepRows);
   (void)maxI;
   if (!make_stream_plan(L.resid, s, 0, OP_RESID, sms)) return false;
+  L.tree = (s.N >= 3) && env_int("CP_SWEEP_TREE", 1) != 0;
+  if (L.tree) {
+    if (!make_stream_plan(L.yl_plan, s, 1, OP_YL, sms)) return false;
+    memset(&L.s3, 0, sizeof(L.s3));
+    L.s3.N = 3;
+    L.s3.R = R;
+    L.s3.dims[0] = s.dims[0];
+    L.s3.dims[1] = s.dims[1];
+    L.s3.dims[2] = 1;
+    for (int k = 2; k < s.N; ++k) L.s3.dims[2] *= s.dims[k];
+    if (L.s3.dims[2] > 0x7fffffff) L.tree = false;
+  }
+  if (L.tree) {
+    if (!make_stream_plan(L.p2_plan, L.s3, 2, OP_MTTKRP, sms)) return false;
+    const size_t d = stream_part_doubles(L.p2_plan);
+    if (d > part) part = d;
+    row_blocking(L.p2_plan, &L.rpc2, &L.sp2);
+    L.nyr = (int)ceil_div(L.s3.dims[2], L.rpc2);
+  }
   L.norm_blocks = 2 * sms;
   size_t off = 0;
   L.status = off; off = align_up(off + 8);
@@ -259,6 +291,14 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     off = align_up(off + (size_t)s.dims[k] * (R + (R & 1)));
   }
   L.part = off; off = align_up(off + part);
+  if (L.tree) {
+    const StreamPlan &y = L.yl_plan;
+    L.yl = off; off = align_up(off + (size_t)s.dims[0] * s.dims[1] * R);
+    L.edge = off; off = align_up(off + (size_t)2 * y.Gc * y.RB * s.dims[0] * R);
+    L.mbuf = off; off = align_up(off + (size_t)maxI * R);
+    L.yr = off; off = align_up(off + (size_t)L.s3.dims[2] * R);
+    L.segtab = off; off = align_up(off + (size_t)s.dims[1]);  // int2 per segment
+  }
   L.total = off * sizeof(double);
   return true;
 }
@@ -400,23 +440,20 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
   if (launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
   int launches = 1;
   double *gp[2] = {w + L.gpart0, w + L.gpart1};
-  for (int n = 0; n < N; ++n) {
-    StreamPlan p = L.plans[n];
-    p.Z = Z;
-    for (int k = 0; k < N; ++k) p.At[k] = w + L.At[k];
-    p.part = w + L.part;
-    if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
+  int grid_of[CP_MAX_N] = {0};
+  // a4 for mode n from M given by rg (stream partials or a plain M buffer)
+  auto solve_mode = [&](int n, const ReduceGeom &rg, int rpc, int sp) -> bool {
     SolveArgs sa;
     memset(&sa, 0, sizeof(sa));
     sa.N = N;
     sa.R = R;
     sa.mode = n;
     sa.prev_mode = n - 1;
-    sa.nprev = (n > 0) ? L.nsolve[n - 1] : 0;
-    sa.rpc = L.rpc[n];
-    sa.sp = L.sp[n];
+    sa.nprev = (n > 0) ? grid_of[n - 1] : 0;
+    sa.rpc = rpc;
+    sa.sp = sp;
     sa.In = s->dims[n];
-    sa.rg = reduce_geom(p);
+    sa.rg = rg;
     sa.pg = pg;
     sa.F = (F != nullptr) ? F[n] : nullptr;
     sa.A = A[n];
@@ -427,16 +464,95 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     sa.dotM = w + L.dotM;
     sa.dotF = w + L.dotF + (size_t)n * L.gp_max;
     sa.status = w + L.status;
-    if (launch_solve(sa, L.nsolve[n], cs) != cudaSuccess) return CP_ECUDA;
-    launches += 2;
+    grid_of[n] = (int)ceil_div(s->dims[n], rpc);
+    ++launches;
+    return launch_solve(sa, grid_of[n], cs) == cudaSuccess;
+  };
+  const int RS = R + (R & 1);
+  const int rpc_d = 256 / R > 0 ? 256 / R : 1;
+  if (L.tree) {
+    // ---- dimension-tree sweep: two passes over Z instead of N ----
+    StreamPlan p1 = L.yl_plan;
+    p1.Z = Z;
+    for (int k = 0; k < N; ++k) p1.At[k] = w + L.At[k];
+    p1.yl = w + L.yl;
+    p1.edge = w + L.edge;
+    p1.part = nullptr;
+    if (launch_stream(p1, cs) != cudaSuccess) return CP_ECUDA;
+    ++launches;
+    YLGeom yg;
+    yg.R = R;
+    yg.Gc = p1.Gc;
+    yg.RB = p1.RB;
+    yg.Wmax = p1.Wmax;
+    yg.I0 = s->dims[0];
+    yg.I1 = s->dims[1];
+    yg.Q = p1.Q;
+    yg.Qn = p1.Qn;
+    yg.yl = w + L.yl;
+    yg.edge = w + L.edge;
+    double *mb = w + L.mbuf;
+    if (launch_yl_fixup(yg, cs) != cudaSuccess) return CP_ECUDA;
+    ++launches;
+    // mode 0: M0 = sum_{i1} Y_L(:, i1, :) * A^(1)(i1, :)   (A^(2..) old: Gauss-Seidel order)
+    if (launch_ymm0(yg, w + L.At[1], RS, mb, cs) != cudaSuccess) return CP_ECUDA;
+    ++launches;
+    if (!solve_mode(0, direct_geom(mb, s->dims[0], R), rpc_d, 1)) return CP_ECUDA;
+    // mode 1: M1 = sum_{i0} Y_L(i0, :, :) * A^(0)_new(i0, :)
+    if (launch_ymm1(yg, w + L.At[0], RS, mb, cs) != cudaSuccess) return CP_ECUDA;
+    ++launches;
+    if (!solve_mode(1, direct_geom(mb, s->dims[1], R), rpc_d, 1)) return CP_ECUDA;
+    // pass 2: modes >= 2 from Z x I0 x I1 contracted with the new A^(0), A^(1)
+    StreamPlan p2 = L.p2_plan;
+    p2.Z = Z;
+    p2.At[0] = w + L.At[0];
+    p2.At[1] = w + L.At[1];
+    p2.At[2] = nullptr;
+    p2.part = w + L.part;
+    if (launch_stream(p2, cs) != cudaSuccess) return CP_ECUDA;
+    ++launches;
+    if (N == 3) {
+      if (!solve_mode(2, reduce_geom(p2), L.rpc2, L.sp2)) return CP_ECUDA;
+    } else {
+      reduce_mttkrp_kernel<<<L.nyr, 256, 0, cs>>>(reduce_geom(p2), L.rpc2, L.sp2, w + L.yr);
+      CK_LAUNCH();
+      ++launches;
+      for (int m = 2; m < N; ++m) {
+        YRArgs ya;
+        memset(&ya, 0, sizeof(ya));
+        ya.N = N;
+        ya.R = R;
+        ya.RS = RS;
+        ya.mode = m;
+        for (int k = 0; k < N; ++k) {
+          ya.dims[k] = s->dims[k];
+          ya.At[k] = w + L.At[k];
+        }
+        ya.YR = w + L.yr;
+        ya.M = mb;
+        if (launch_yr(ya, cs) != cudaSuccess) return CP_ECUDA;
+        ++launches;
+        if (!solve_mode(m, direct_geom(mb, s->dims[m], R), rpc_d, 1)) return CP_ECUDA;
+      }
+    }
+  } else {
+    for (int n = 0; n < N; ++n) {
+      StreamPlan p = L.plans[n];
+      p.Z = Z;
+      for (int k = 0; k < N; ++k) p.At[k] = w + L.At[k];
+      p.part = w + L.part;
+      if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
+      ++launches;
+      if (!solve_mode(n, reduce_geom(p), L.rpc[n], L.sp[n])) return CP_ECUDA;
+    }
   }
   FinalizeArgs fa;
   memset(&fa, 0, sizeof(fa));
   fa.N = N;
   fa.R = R;
-  fa.nlast = L.nsolve[N - 1];
+  fa.nlast = grid_of[N - 1];
   fa.dot_stride = L.gp_max;
-  for (int n = 0; n < N; ++n) fa.nsolve[n] = L.nsolve[n];
+  for (int n = 0; n < N; ++n) fa.nsolve[n] = grid_of[n];
   fa.glast = gp[(N - 1) & 1];
   fa.dotM_last = w + L.dotM;
   fa.dotF = w + L.dotF;

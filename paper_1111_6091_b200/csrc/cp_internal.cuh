@@ -14,7 +14,10 @@ constexpr int kStreamThreads = kConsumers + 64;   // + TMA producer warp + weigh
 constexpr int kMaxRows = 512;                     // widest row block (V = 2: 2 rows / thread)
 constexpr int kMaxDigits = CP_MAX_N - 1;          // column multi-index digits (modes 1..N-1)
 
-enum StreamOp { OP_MTTKRP = 0, OP_RESID = 1 };
+// OP_YL: the first pass of the dimension-tree sweep -- the mode-1 contraction of Z with the
+// Khatri-Rao rows of modes 2..N-1, written per i_1 segment as an I_0 x R block (no contraction
+// with A^(0)); see stream_kernel.cuh.
+enum StreamOp { OP_MTTKRP = 0, OP_RESID = 1, OP_YL = 2 };
 
 // Plan of one streaming pass over Z (MTTKRP of one mode, or the residual pass of cp_fit).
 // Z is viewed as an I1 x Q column-major matrix (Q = P / I1 "columns" = mode-1 fibers).
@@ -47,6 +50,9 @@ struct StreamPlan {
   const double *Z;
   const double *At[CP_MAX_N];   // row-major (I_k x R) copies of the factors
   double *part;     // partial outputs (workspace)
+  double *yl;       // OP_YL: I0 x R block per fully owned segment (segment-major)
+  double *edge;     // OP_YL: per CTA 2 blocks for partially owned segments
+  int red_doubles;  // consumers' shared reduction area (doubles)
 };
 
 // Kernel table: one entry per (R, V, op) instantiation of stream_kernel.
@@ -55,10 +61,10 @@ struct StreamEntry {
   const void *kernel;
 };
 constexpr int stream_index(int R, int V, int op) {
-  return (R * 4 + (V == 8 ? 3 : (V == 4 ? 2 : V - 1))) * 2 + op;
+  return (R * 4 + (V == 8 ? 3 : (V == 4 ? 2 : V - 1))) * 3 + op;
 }
 // Consumer rank tile (see StreamTile in stream_kernel.cuh): ranks per thread and rank groups.
-__host__ __device__ constexpr int stream_rg(int R, int op) { return (op == 0 && R > 12) ? (R + 7) / 8 : 1; }
+__host__ __device__ constexpr int stream_rg(int R, int op) { return (op != 1 && R > 12) ? (R + 7) / 8 : 1; }
 __host__ __device__ constexpr int stream_rt(int R, int op) {
   return (stream_rg(R, op) > 1 && (((R + stream_rg(R, op) - 1) / stream_rg(R, op)) & 1))
              ? (R + stream_rg(R, op) - 1) / stream_rg(R, op) + 1
@@ -66,7 +72,7 @@ __host__ __device__ constexpr int stream_rt(int R, int op) {
 }
 // shared-memory reduction area of the consumers (doubles)
 __host__ __device__ constexpr int stream_red_doubles(int R, int op) { return 256 * stream_rt(R, op) + 8 > 8 * R + 8 ? 256 * stream_rt(R, op) + 8 : 8 * R + 8; }
-constexpr int kStreamTableSize = stream_index(CP_MAX_R, 8, 1) + 1;
+constexpr int kStreamTableSize = stream_index(CP_MAX_R, 8, 2) + 1;
 void register_stream_part0(StreamEntry *t);
 void register_stream_part1(StreamEntry *t);
 void register_stream_part2(StreamEntry *t);

@@ -23,6 +23,7 @@ __device__ __forceinline__ double sum_strided(const double *p, int64_t stride, i
 // ---------------------------------------------------------------- reduction of stream partials
 // Part j of sp of the fixed-order sum that forms M(i, r) from the stream kernel's partials.
 __device__ __forceinline__ double reduce_entry_part(const ReduceGeom &g, int64_t i, int r, int j, int sp) {
+  if (g.direct) return (j == 0) ? g.part[i + g.In_rows * r] : 0.0;
   if (g.mode0) {  // mode 0: one I1 x R partial per column group; chunk j of the groups
     const int c0 = (int)(((int64_t)g.Gc * j) / sp), c1 = (int)(((int64_t)g.Gc * (j + 1)) / sp);
     return sum_strided(g.part + (int64_t)c0 * g.I1 * g.R + i + g.I1 * r, g.I1 * g.R, c1 - c0);
@@ -378,6 +379,158 @@ __global__ void __launch_bounds__(256) norm2_final_kernel(const double *part, in
   for (int c = threadIdx.x; c < n; c += blockDim.x) s += part[c];
   const double t = block_sum_256(s, sred);
   if (threadIdx.x == 0) out[0] = t;
+}
+
+// ---------------------------------------------------------------- dimension-tree sweep helpers
+// After the Y_L pass, every segment i1 that a CTA boundary splits has its contributions in the
+// edge blocks of the CTAs c_lo..c_hi that cover it; block (c, chunk) completes the segment
+// holding v0(c) (the first boundary inside that segment does the work), summing the edge blocks
+// in CTA order into yl.  Afterwards yl holds Y_L(:, i1, :) for every i1.
+__global__ void __launch_bounds__(256) yl_fixup_kernel(const YLGeom y, int chunks) {
+  const int64_t c = blockIdx.x / chunks + 1;
+  const int chunk = blockIdx.x % chunks;
+  const int64_t v0c = (c * y.Q) / y.Gc;
+  const int64_t s = v0c / y.Qn;
+  if (v0c % y.Qn == 0) return;                      // boundary on a segment edge: nothing split
+  const int64_t v0p = ((c - 1) * y.Q) / y.Gc;
+  if (v0p > s * y.Qn) return;                       // an earlier boundary in s handles it
+  const int64_t clo = ((s * y.Qn + 1) * y.Gc - 1) / y.Q;
+  const int64_t chi = (((s + 1) * y.Qn) * y.Gc - 1) / y.Q;
+  const int64_t blk = y.I0 * y.R;
+  const int64_t e0 = (blk * chunk) / chunks, e1 = (blk * (chunk + 1)) / chunks;
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int64_t i0 = e % y.I0;
+    const int rb = (int)(i0 / y.Wmax);
+    double acc = 0.0;
+    for (int64_t cc = clo; cc <= chi; ++cc) {
+      const int64_t seg_first = ((cc * y.Q) / y.Gc) / y.Qn;
+      const int ed = (seg_first == s) ? 0 : 1;
+      acc += y.edge[((cc * y.RB + rb) * 2 + ed) * blk + e];
+    }
+    ((double *)y.yl)[s * blk + e] = acc;
+  }
+}
+
+// M0(i0, r) = sum_{i1} Y_L(i0, i1, r) A^(1)(i1, r): thread per (i0, r, split j of the i1
+// range); the sp partial sums combine in split order
+__global__ void __launch_bounds__(256) ymm0_kernel(const YLGeom y, const double *At1, int RS, int sp,
+                                                   double *M0) {
+  __shared__ double sred[256];
+  const int tid = threadIdx.x;
+  const int64_t ent = ((int64_t)blockIdx.x * blockDim.x + tid) / sp;
+  const int j = tid % sp;
+  double s = 0.0;
+  if (ent < y.I0 * y.R) {
+    const int64_t i0 = ent % y.I0;
+    const int r = (int)(ent / y.I0);
+    const int64_t blk = y.I0 * y.R;
+    const double *yp = y.yl + i0 + y.I0 * r;
+    const int64_t a = (y.I1 * j) / sp, b = (y.I1 * (j + 1)) / sp;
+    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t i1 = a;
+    for (; i1 + 3 < b; i1 += 4) {
+      s = fma(yp[i1 * blk], At1[i1 * RS + r], s);
+      s1 = fma(yp[(i1 + 1) * blk], At1[(i1 + 1) * RS + r], s1);
+      s2 = fma(yp[(i1 + 2) * blk], At1[(i1 + 2) * RS + r], s2);
+      s3 = fma(yp[(i1 + 3) * blk], At1[(i1 + 3) * RS + r], s3);
+    }
+    for (; i1 < b; ++i1) s = fma(yp[i1 * blk], At1[i1 * RS + r], s);
+    s = (s + s1) + (s2 + s3);
+  }
+  sred[tid] = s;
+  __syncthreads();
+  if (j == 0 && ent < y.I0 * y.R) {
+    double t = 0.0;
+    for (int k = 0; k < sp; ++k) t += sred[tid + k];
+    M0[ent] = t;  // ent = i0 + I0 * r: column-major I0 x R
+  }
+}
+
+// M1(i1, r) = sum_{i0} Y_L(i0, i1, r) A^(0)(i0, r): warp per (i1, r), lanes stride over i0
+// (contiguous), fixed shuffle tree
+__global__ void __launch_bounds__(256) ymm1_kernel(const YLGeom y, const double *At0, int RS, double *M1) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= y.I1 * y.R) return;
+  const int64_t i1 = w % y.I1;
+  const int r = (int)(w / y.I1);
+  const double *yp = y.yl + i1 * y.I0 * y.R + y.I0 * r;
+  double s = 0.0, s1 = 0.0;
+  int64_t i0 = lane;
+  for (; i0 + 32 < y.I0; i0 += 64) {
+    s = fma(yp[i0], At0[i0 * RS + r], s);
+    s1 = fma(yp[i0 + 32], At0[(i0 + 32) * RS + r], s1);
+  }
+  if (i0 < y.I0) s = fma(yp[i0], At0[i0 * RS + r], s);
+  s += s1;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) M1[i1 + y.I1 * r] = s;
+}
+
+// warp per (i_m, r): lanes stride over the other indices j of modes 2..N-1
+__global__ void __launch_bounds__(256) yr_kernel(const YRArgs a) {
+  const int64_t Im = a.dims[a.mode];
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= Im * a.R) return;
+  const int64_t im = w % Im;
+  const int r = (int)(w / Im);
+  int64_t J = 1;
+  for (int k = 2; k < a.N; ++k) J *= a.dims[k];
+  const int64_t nother = J / Im;
+  double s = 0.0;
+  for (int64_t o = lane; o < nother; o += 32) {
+    // o enumerates the indices of modes 2..N-1 except mode, lowest mode fastest
+    int64_t t = o, j = 0, stride = 1;
+    double wgt = 1.0;
+    for (int k = 2; k < a.N; ++k) {
+      int64_t ik;
+      if (k == a.mode) {
+        ik = im;
+      } else {
+        ik = t % a.dims[k];
+        t /= a.dims[k];
+        wgt *= a.At[k][ik * a.RS + r];
+      }
+      j += ik * stride;
+      stride *= a.dims[k];
+    }
+    s = fma(a.YR[j + J * r], wgt, s);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) a.M[im + Im * r] = s;
+}
+
+cudaError_t launch_yl_fixup(const YLGeom &y, cudaStream_t st) {
+  if (y.Gc < 2) return cudaSuccess;
+  int chunks = (int)((y.I0 * y.R + 2047) / 2048);
+  if (chunks > 16) chunks = 16;
+  yl_fixup_kernel<<<(unsigned)((y.Gc - 1) * chunks), 256, 0, st>>>(y, chunks);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ymm0(const YLGeom &y, const double *At1, int RS, double *M0, cudaStream_t st) {
+  int sp = (int)(y.I1 / 16);
+  if (sp < 1) sp = 1;
+  if (sp > 32) sp = 32;
+  while (256 % sp) --sp;
+  const int64_t threads = y.I0 * y.R * sp;
+  ymm0_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(y, At1, RS, sp, M0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ymm1(const YLGeom &y, const double *At0, int RS, double *M1, cudaStream_t st) {
+  const int64_t threads = y.I1 * y.R * 32;
+  ymm1_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(y, At0, RS, M1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_yr(const YRArgs &a, cudaStream_t st) {
+  const int64_t threads = a.dims[a.mode] * a.R * 32;
+  yr_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- host-side launchers

@@ -1,5 +1,7 @@
 // small_kernels.cuh -- argument structs of the R x R / reduction kernels (small_kernels.cu).
 #pragma once
+#include <cstring>
+
 #include "cp_internal.cuh"
 
 namespace cpk {
@@ -23,6 +25,7 @@ __device__ __forceinline__ double block_sum_256(double v, double *sred) {
 // Where the stream kernel left its partials, and how to sum them (fixed order).
 struct ReduceGeom {
   int R, Gc, RB, slots, mode0;  // mode0: partials are I1 x R per column group
+  int direct;                   // 1: part is M itself (In_rows x R, column-major)
   int64_t I1, Q, Qn, In;
   int64_t In_rows;  // rows of the output (I_mode)
   const double *part;
@@ -35,6 +38,7 @@ inline ReduceGeom reduce_geom(const StreamPlan &p) {
   g.RB = p.RB;
   g.slots = p.slots;
   g.mode0 = (p.mode == 0) ? 1 : 0;
+  g.direct = 0;
   g.I1 = p.I1;
   g.Q = p.Q;
   g.Qn = p.Qn;
@@ -126,6 +130,38 @@ __global__ void finalize_fit_kernel(const FitFinalArgs a);
 __global__ void norm2_kernel(const double *__restrict__ Z, int64_t P, double *part);
 __global__ void norm2_final_kernel(const double *part, int n, double *out);
 cudaError_t launch_solve(const SolveArgs &a, int grid, cudaStream_t st);
+
+// ---- dimension-tree sweep (NEXT-4): Y_L(i0, i1, r) = sum_{i_2..} z * prod_{k>=2} A^(k)(i_k, r)
+// written by the OP_YL stream pass (full segments in yl, shared ones in per-CTA edge blocks)
+struct YLGeom {
+  int R, Gc, RB, Wmax;
+  int64_t I0, I1, Q, Qn;
+  const double *yl, *edge;
+};
+inline ReduceGeom direct_geom(const double *M, int64_t rows, int R) {
+  ReduceGeom g;
+  memset(&g, 0, sizeof(g));
+  g.R = R;
+  g.direct = 1;
+  g.In_rows = rows;
+  g.part = M;
+  return g;
+}
+// completes the segments split between CTAs (edge blocks -> yl)
+cudaError_t launch_yl_fixup(const YLGeom &y, cudaStream_t st);
+// M0(i0, r) = sum_{i1} Y_L(i0, i1, r) A^(1)(i1, r)   (At1: row-major copy, stride RS)
+cudaError_t launch_ymm0(const YLGeom &y, const double *At1, int RS, double *M0, cudaStream_t st);
+// M1(i1, r) = sum_{i0} Y_L(i0, i1, r) A^(0)(i0, r)
+cudaError_t launch_ymm1(const YLGeom &y, const double *At0, int RS, double *M1, cudaStream_t st);
+// M_m(i_m, r) = sum_{j: i_m(j)} Y_R(j, r) prod_{k >= 2, k != m} A^(k)(i_k(j), r), j over modes 2..N-1
+struct YRArgs {
+  int N, R, RS, mode;
+  int64_t dims[CP_MAX_N];
+  const double *At[CP_MAX_N];
+  const double *YR;  // J x R column-major, J = prod_{k >= 2} I_k (mode 2 fastest)
+  double *M;
+};
+cudaError_t launch_yr(const YRArgs &a, cudaStream_t st);
 cudaError_t launch_prep(const PrepArgs &a, cudaStream_t st);
 
 // Fill the prep block offsets for a shape (blocks of kPrepRows rows per mode).

@@ -45,7 +45,7 @@ __device__ __forceinline__ StreamSmem carve(unsigned char *raw, const StreamPlan
   s.abuf = s.zbuf + (size_t)p.nstages * p.cps * p.Wmax;
   s.wbuf = s.abuf + (size_t)p.nstages * p.cps * p.RS;
   s.red = s.wbuf + (size_t)p.nstages * p.cps * WSTR;
-  s.sS = s.red + stream_red_doubles(R, OP);
+  s.sS = s.red + p.red_doubles;
   s.full = reinterpret_cast<uint64_t *>(s.sS + 32);
   s.wready = s.full + p.nstages;
   s.empty = s.wready + p.nstages;
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
         double z[V];
         load_rows<V>(zs + (size_t)col * Wb, u, Wb, z);
         const double *w = wsb + col * WSTR + r0;
-        if (OP == OP_MTTKRP) {
+        if (OP != OP_RESID) {  // MTTKRP and the Y_L pass: acc += z * w
           double wr[RT];
 #pragma unroll
           for (int r = 0; r + 1 < RT; r += 2) {
@@ -359,6 +359,47 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
       fph ^= 1u;
     }
 
+    if (OP == OP_YL && (flags & 1)) {
+      // ---- end of an i_1 segment: write the I0 x R block of accumulators (slots summed in
+      // order through shared memory); a segment shared with a neighbouring CTA goes to this
+      // CTA's edge blocks (0: its first segment, 1: its last) ----
+      const int64_t s_abs = v0 / p.Qn + slot;
+      const bool full = (s_abs * p.Qn >= v0) && ((s_abs + 1) * p.Qn <= v1);
+      double *dst = full ? p.yl + s_abs * p.I1 * R
+                         : p.edge + ((int64_t)blockIdx.x * 2 + (slot == 0 ? 0 : 1)) * p.I1 * R;
+      if (cpt > 1) {
+        double *sred = sm.red;  // Wb x R (red_doubles >= Wb * R for OP_YL)
+        for (int s2 = 1; s2 < cpt; ++s2) {
+          named_bar_sync(1, kConsumers);
+          if (active && sl == s2) {
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+#pragma unroll
+              for (int r = 0; r < RT; ++r)
+                if (r0 + r < R) sred[row_of<V>(u, v, Wb) + Wb * (r0 + r)] = acc[v][r];
+          }
+          named_bar_sync(1, kConsumers);
+          if (sl == 0) {
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+#pragma unroll
+              for (int r = 0; r < RT; ++r)
+                if (r0 + r < R) acc[v][r] += sred[row_of<V>(u, v, Wb) + Wb * (r0 + r)];
+          }
+        }
+      }
+      if (sl == 0) {
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int r = 0; r < RT; ++r)
+            if (r0 + r < R) dst[row0 + row_of<V>(u, v, Wb) + p.I1 * (r0 + r)] = acc[v][r];
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int r = 0; r < RT; ++r) acc[v][r] = 0.0;
+    }
     if (OP == OP_MTTKRP && p.mode != 0 && (flags & 1)) {
       // ---- end of an i_m segment: contract with A^(1) rows and reduce over the CTA ----
       double pr[RT];
