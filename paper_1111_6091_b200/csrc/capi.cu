@@ -196,7 +196,8 @@ static double stream_alg_bytes(const StreamPlan &p) {
     P *= (double)p.dims[k];
     if (k != p.mode || p.op == OP_RESID) fac += (double)p.dims[k] * p.R;
   }
-  const double out = (p.op == OP_RESID) ? 0.0 : (double)p.dims[p.mode] * p.R;
+  double out = (p.op == OP_RESID) ? 0.0 : (double)p.dims[p.mode] * p.R;
+  if (p.op == OP_YL) out = (double)p.dims[0] * p.dims[1] * p.R;  // Y_L (I0 x I1 x R) written
   return 8.0 * (P + fac + out);
 }
 
