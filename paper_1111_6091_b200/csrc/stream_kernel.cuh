@@ -362,13 +362,17 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
     if (OP == OP_YL && (flags & 1)) {
       // ---- end of an i_1 segment: write the I0 x R block of accumulators (slots summed in
       // order through shared memory); a segment shared with a neighbouring CTA goes to this
-      // CTA's edge blocks (0: its first segment, 1: its last) ----
+      // CTA's edge blocks (0: its first segment, 1: its last).  Index arithmetic uses opaque
+      // copies so that it stays inside this branch (no hoisted addresses in the loop). ----
+      const int Wq = opaque(Wb), uq = opaque(u);
+      const int64_t I1q = opaque(p.I1);
       const int64_t s_abs = v0 / p.Qn + slot;
       const bool full = (s_abs * p.Qn >= v0) && ((s_abs + 1) * p.Qn <= v1);
-      double *dst = full ? p.yl + s_abs * p.I1 * R
-                         : p.edge + ((int64_t)blockIdx.x * 2 + (slot == 0 ? 0 : 1)) * p.I1 * R;
+      double *dst = (full ? p.yl + s_abs * I1q * R
+                          : p.edge + ((int64_t)blockIdx.x * 2 + (slot == 0 ? 0 : 1)) * I1q * R) +
+                    row0 + (int64_t)I1q * r0;
       if (cpt > 1) {
-        double *sred = sm.red;  // Wb x R (red_doubles >= Wb * R for OP_YL)
+        double *sred = sm.red + Wq * r0;  // Wb x R (red_doubles >= Wb * R for OP_YL)
         for (int s2 = 1; s2 < cpt; ++s2) {
           named_bar_sync(1, kConsumers);
           if (active && sl == s2) {
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
             for (int v = 0; v < V; ++v)
 #pragma unroll
               for (int r = 0; r < RT; ++r)
-                if (r0 + r < R) sred[row_of<V>(u, v, Wb) + Wb * (r0 + r)] = acc[v][r];
+                if (r0 + r < R) sred[row_of<V>(uq, v, Wq) + Wq * r] = acc[v][r];
           }
           named_bar_sync(1, kConsumers);
           if (sl == 0) {
@@ -384,7 +388,7 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
             for (int v = 0; v < V; ++v)
 #pragma unroll
               for (int r = 0; r < RT; ++r)
-                if (r0 + r < R) acc[v][r] += sred[row_of<V>(u, v, Wb) + Wb * (r0 + r)];
+                if (r0 + r < R) acc[v][r] += sred[row_of<V>(uq, v, Wq) + Wq * r];
           }
         }
       }
@@ -393,7 +397,7 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
         for (int v = 0; v < V; ++v)
 #pragma unroll
           for (int r = 0; r < RT; ++r)
-            if (r0 + r < R) dst[row0 + row_of<V>(u, v, Wb) + p.I1 * (r0 + r)] = acc[v][r];
+            if (r0 + r < R) dst[row_of<V>(uq, v, Wq) + I1q * r] = acc[v][r];
       }
 #pragma unroll
       for (int v = 0; v < V; ++v)
@@ -407,8 +411,11 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
       for (int r = 0; r < RT; ++r) pr[r] = 0.0;
       if (active) {
 #pragma unroll
+        const int Wq = opaque(Wb), uq = opaque(u);
+        const double *a1b = p.At[0] + row0 * p.RS + r0;
+#pragma unroll
         for (int v = 0; v < V; ++v) {
-          const double *a1 = p.At[0] + (row0 + row_of<V>(u, v, Wb)) * p.RS + r0;
+          const double *a1 = a1b + (int64_t)row_of<V>(uq, v, Wq) * p.RS;
 #pragma unroll
           for (int r = 0; r < RT; ++r)
             if (r0 + r < R) pr[r] = fma(__ldg(a1 + r), acc[v][r], pr[r]);
