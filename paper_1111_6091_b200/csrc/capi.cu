@@ -266,7 +266,7 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     L.s3.dims[1] = s.dims[1];
     L.s3.dims[2] = 1;
     for (int k = 2; k < s.N; ++k) L.s3.dims[2] *= s.dims[k];
-    if (L.s3.dims[2] > 0x7fffffff) L.tree = false;
+    if (L.s3.dims[2] > 0x7fffffff || s.dims[0] * R > 0x7fffffff) L.tree = false;  // 32-bit Y_L block indices
   }
   if (L.tree) {
     if (!make_stream_plan(L.p2_plan, L.s3, 2, OP_MTTKRP, sms)) return false;
@@ -466,6 +466,24 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     sa.dotF = w + L.dotF + (size_t)n * L.gp_max;
     sa.status = w + L.status;
     grid_of[n] = (int)ceil_div(s->dims[n], rpc);
+    if (n == N - 1) {
+      // the sweep's last solve also evaluates f, f~ (finalize_body in its last block)
+      sa.fin_on = 1;
+      sa.ticket = reinterpret_cast<unsigned *>(w + L.status + kTicketSlot);
+      FinalizeArgs &fa = sa.fin;
+      fa.N = N;
+      fa.R = R;
+      fa.nlast = grid_of[N - 1];
+      fa.dot_stride = L.gp_max;
+      for (int k = 0; k < N; ++k) fa.nsolve[k] = grid_of[k];
+      fa.glast = gp[(N - 1) & 1];
+      fa.dotM_last = w + L.dotM;
+      fa.dotF = w + L.dotF;
+      fa.Ups = w + L.Ups;
+      fa.normZ2 = normZ2;
+      fa.status = w + L.status;
+      fa.out = out;
+    }
     ++launches;
     return launch_solve(sa, grid_of[n], cs) == cudaSuccess;
   };
@@ -496,11 +514,11 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     if (launch_yl_fixup(yg, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     // mode 0: M0 = sum_{i1} Y_L(:, i1, :) * A^(1)(i1, :)   (A^(2..) old: Gauss-Seidel order)
-    if (launch_ymm0(yg, w + L.At[1], RS, mb, cs) != cudaSuccess) return CP_ECUDA;
+    if (launch_ymm0(yg, A[1], mb, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     if (!solve_mode(0, direct_geom(mb, s->dims[0], R), rpc_d, 1)) return CP_ECUDA;
     // mode 1: M1 = sum_{i0} Y_L(i0, :, :) * A^(0)_new(i0, :)
-    if (launch_ymm1(yg, w + L.At[0], RS, mb, cs) != cudaSuccess) return CP_ECUDA;
+    if (launch_ymm1(yg, A[0], mb, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     if (!solve_mode(1, direct_geom(mb, s->dims[1], R), rpc_d, 1)) return CP_ECUDA;
     // pass 2: modes >= 2 from Z x I0 x I1 contracted with the new A^(0), A^(1)
@@ -547,23 +565,7 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
       if (!solve_mode(n, reduce_geom(p), L.rpc[n], L.sp[n])) return CP_ECUDA;
     }
   }
-  FinalizeArgs fa;
-  memset(&fa, 0, sizeof(fa));
-  fa.N = N;
-  fa.R = R;
-  fa.nlast = grid_of[N - 1];
-  fa.dot_stride = L.gp_max;
-  for (int n = 0; n < N; ++n) fa.nsolve[n] = grid_of[n];
-  fa.glast = gp[(N - 1) & 1];
-  fa.dotM_last = w + L.dotM;
-  fa.dotF = w + L.dotF;
-  fa.Ups = w + L.Ups;
-  fa.normZ2 = normZ2;
-  fa.status = w + L.status;
-  fa.out = out;
-  finalize_sweep_kernel<<<1, 256, 0, cs>>>(fa);
-  CK_LAUNCH();
-  g_launches = launches + 1;
+  g_launches = launches;
   return CP_OK;
 }
 

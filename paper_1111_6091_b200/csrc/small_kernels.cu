@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
   if (blockIdx.x == 0 && tid == 0 && a.status != nullptr) {
     a.status[0] = 0.0;
     a.status[1] = -1.0;
+    *reinterpret_cast<unsigned *>(a.status + kTicketSlot) = 0u;  // solve completion ticket
   }
   if (A == nullptr) return;
   double *At = a.At[k];
@@ -122,146 +123,10 @@ __device__ __forceinline__ double prep_gram(const PrepGrams &pg, int k, int e, i
   return sum_strided(pg.gpre + (int64_t)pg.blk_off[k] * RR + e, RR, pg.nblk[k]);
 }
 
-// ---------------------------------------------------------------- per-mode solve (sweep)
-// One warp factors Gamma = L L^T in registers (lane i holds row i) and forms L^{-1}; every
-// row of A^(n) is then x = L^{-T} (L^{-1} (m + f)) as two small triangular mat-vecs.
-template <int R>
-__global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
-  constexpr int RR = R * R;
-  constexpr int LS = R + 1;  // smem row stride of the R x R matrices
-  __shared__ double sL[R * LS];    // Gamma, then L (lower)
-  __shared__ double sLi[R * LS];   // L^{-1} (lower)
-  __shared__ double sUp[RR];
-  __shared__ double sM[256], sB[256], sX[256], scratch[256];
-  __shared__ int sfail;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (a.status[0] != 0.0) return;  // an earlier mode already failed
-
-  // total Gram of the previous mode from its per-CTA partials (fixed order)
-  if (a.gprev != nullptr) {
-    for (int e = tid; e < RR; e += blockDim.x) {
-      const double s = sum_strided(a.gprev + e, RR, a.nprev);
-      sUp[e] = s;
-      if (blockIdx.x == 0) a.Ups[(int64_t)a.prev_mode * RR + e] = s;
-    }
-  }
-  const int64_t In = a.In;
-  const int64_t i0 = (int64_t)blockIdx.x * a.rpc;
-  const int nrows = (int)((In - i0) < a.rpc ? (In - i0) : a.rpc);
-  // phase A (independent of Gamma): M rows from the stream partials
-  gather_rows(a.rg, i0, nrows, R, a.sp, sM, scratch);
-  __syncthreads();
-  // Gamma^(n) = *_{k != n} Upsilon^(k)   (eq:Gamma).  Upsilon^(k): k > n from the prep
-  // partials (factor not yet updated in this sweep), k = n-1 from the previous solve's
-  // partials, k < n-1 from the totals the earlier solves wrote.
-  for (int e = tid; e < RR; e += blockDim.x) {
-    double gm = 1.0;
-    for (int k = 0; k < a.N; ++k) {
-      if (k == a.mode) continue;
-      double u;
-      if (k > a.mode) u = prep_gram(a.pg, k, e, RR);
-      else if (k == a.prev_mode) u = sUp[e];
-      else u = a.Ups[(int64_t)k * RR + e];
-      gm *= u;
-    }
-    sL[(e % R) * LS + (e / R)] = gm;
-  }
-  for (int e = tid; e < nrows * R; e += blockDim.x) {
-    const int ii = e / R, r = e - (e / R) * R;
-    sB[e] = sM[e] + (a.F != nullptr ? a.F[(i0 + ii) + In * r] : 0.0);
-  }
-  if (tid == 0) sfail = 0;
-  __syncthreads();
-  if (warp == 0) {
-    // Cholesky, right-looking, lane i = row i (no pivoting; fail on a pivot <= 0 or NaN)
-    double g[R];
-#pragma unroll
-    for (int k = 0; k < R; ++k) g[k] = (lane < R) ? sL[lane * LS + k] : 0.0;
-    bool ok = true;
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const double piv = __shfl_sync(0xffffffffu, g[j], j);
-      if (!(piv > 0.0)) {
-        ok = false;
-        break;
-      }
-      const double ljj = sqrt(piv);
-      const double inv = 1.0 / ljj;
-      if (lane == j) g[j] = ljj;
-      else if (lane > j) g[j] *= inv;
-#pragma unroll
-      for (int k = j + 1; k < R; ++k) {
-        const double lkj = __shfl_sync(0xffffffffu, g[j], k);
-        if (lane >= k) g[k] = fma(-g[j], lkj, g[k]);
-      }
-    }
-    if (!ok) {
-      if (lane == 0) sfail = 1;
-    } else {
-#pragma unroll
-      for (int k = 0; k < R; ++k)
-        if (lane < R) sL[lane * LS + k] = (k <= lane) ? g[k] : 0.0;
-      __syncwarp();
-      // L^{-1}: lane c forms column c by forward substitution
-      double x[R];
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        double s = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-        for (int k = 0; k < i; ++k) s = fma(-sL[i * LS + k], x[k], s);
-        x[i] = (i >= lane) ? s / sL[i * LS + i] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-        if (lane < R) sLi[i * LS + lane] = x[i];
-    }
-  }
-  __syncthreads();
-  if (sfail) {
-    if (blockIdx.x == 0 && tid == 0) {
-      a.status[0] = (double)CP_ENOTSPD;
-      a.status[1] = (double)a.mode;
-    }
-    return;
-  }
-  // y = L^{-1} b, then x = L^{-T} y, thread per (row, r)
-  for (int e = tid; e < nrows * R; e += blockDim.x) {
-    const int ii = e / R, r = e - (e / R) * R;
-    double y = 0.0;
-    for (int k = 0; k <= r; ++k) y = fma(sLi[r * LS + k], sB[ii * R + k], y);
-    scratch[e] = y;
-  }
-  __syncthreads();
-  double dm = 0.0, df = 0.0;
-  for (int e = tid; e < nrows * R; e += blockDim.x) {
-    const int ii = e / R, r = e - (e / R) * R;
-    double x = 0.0;
-    for (int k = r; k < R; ++k) x = fma(sLi[k * LS + r], scratch[ii * R + k], x);
-    const int64_t i = i0 + ii;
-    a.A[i + In * r] = x;
-    a.At[i * (R + (R & 1)) + r] = x;
-    sX[e] = x;
-    dm = fma(sM[e], x, dm);
-    if (a.F != nullptr) df = fma(a.F[i + In * r], x, df);
-  }
-  // partial Gram of the new rows, and the CTA's <M,A>, <F,A> (fixed order)
-  const double dms = block_sum_256(dm, scratch);
-  const double dfs = block_sum_256(df, scratch);
-  for (int e = tid; e < RR; e += blockDim.x) {
-    const int r = e % R, s = e / R;
-    double gg = 0.0;
-    for (int ii = 0; ii < nrows; ++ii) gg = fma(sX[ii * R + r], sX[ii * R + s], gg);
-    a.gcur[(int64_t)blockIdx.x * RR + e] = gg;
-  }
-  if (tid == 0) {
-    a.dotM[blockIdx.x] = dms;
-    a.dotF[blockIdx.x] = dfs;
-  }
-}
-
 // ---------------------------------------------------------------- sweep finalize: f, f_tilde
-__global__ void __launch_bounds__(256) finalize_sweep_kernel(const FinalizeArgs a) {
-  __shared__ double sred[256];
+// f = 1/2 ||Z||^2 - <M^(N), A^(N)> + 1/2 1^T (*_k Upsilon^(k)) 1 (reading R6) and
+// f~ = f - sum_n <F^(n), A^(n)> (reading R5); run by one 256-thread block.
+__device__ void finalize_body(const FinalizeArgs &a, double *sred) {
   const int R = a.R, RR = R * R, tid = threadIdx.x;
   if (a.status[0] != 0.0) {
     if (tid == 0) {
@@ -295,6 +160,165 @@ __global__ void __launch_bounds__(256) finalize_sweep_kernel(const FinalizeArgs 
     a.out[1] = f - fa;
     a.out[2] = 0.0;
     a.out[3] = -1.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) finalize_sweep_kernel(const FinalizeArgs a) {
+  __shared__ double sred[256];
+  finalize_body(a, sred);
+}
+
+// ---------------------------------------------------------------- per-mode solve (sweep)
+// One warp factors Gamma = L L^T in registers (lane i holds row i) and forms L^{-1}; every
+// row of A^(n) is then x = L^{-T} (L^{-1} (m + f)) as two small triangular mat-vecs.  With
+// a.fin_on (the sweep's last solve) the last block to finish also runs finalize_body
+// (completion ticket; every sum keeps its fixed order, so results stay bitwise reproducible).
+template <int R>
+__global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
+  constexpr int RR = R * R;
+  constexpr int LS = R + 1;  // smem row stride of the R x R matrices
+  __shared__ double sL[R * LS];    // Gamma, then L (lower)
+  __shared__ double sLi[R * LS];   // L^{-1} (lower)
+  __shared__ double sDi[R];        // 1 / L(j, j)
+  __shared__ double sUp[RR];
+  __shared__ double sM[256], sB[256], sX[256], scratch[256];
+  __shared__ int sfail;
+  __shared__ unsigned sticket;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool live = (a.status[0] == 0.0);  // an earlier mode already failed: straight to the ticket
+  if (live) {
+    // total Gram of the previous mode from its per-CTA partials (fixed order)
+    if (a.gprev != nullptr) {
+      for (int e = tid; e < RR; e += blockDim.x) {
+        const double s = sum_strided(a.gprev + e, RR, a.nprev);
+        sUp[e] = s;
+        if (blockIdx.x == 0) a.Ups[(int64_t)a.prev_mode * RR + e] = s;
+      }
+    }
+    const int64_t In = a.In;
+    const int64_t i0 = (int64_t)blockIdx.x * a.rpc;
+    const int nrows = (int)((In - i0) < a.rpc ? (In - i0) : a.rpc);
+    // phase A (independent of Gamma): M rows from the stream partials
+    gather_rows(a.rg, i0, nrows, R, a.sp, sM, scratch);
+    __syncthreads();
+    // Gamma^(n) = *_{k != n} Upsilon^(k)   (eq:Gamma).  Upsilon^(k): k > n from the prep
+    // partials (factor not yet updated in this sweep), k = n-1 from the previous solve's
+    // partials, k < n-1 from the totals the earlier solves wrote.
+    for (int e = tid; e < RR; e += blockDim.x) {
+      double gm = 1.0;
+      for (int k = 0; k < a.N; ++k) {
+        if (k == a.mode) continue;
+        double u;
+        if (k > a.mode) u = prep_gram(a.pg, k, e, RR);
+        else if (k == a.prev_mode) u = sUp[e];
+        else u = a.Ups[(int64_t)k * RR + e];
+        gm *= u;
+      }
+      sL[(e % R) * LS + (e / R)] = gm;
+    }
+    for (int e = tid; e < nrows * R; e += blockDim.x) {
+      const int ii = e / R, r = e - (e / R) * R;
+      sB[e] = sM[e] + (a.F != nullptr ? a.F[(i0 + ii) + In * r] : 0.0);
+    }
+    if (tid == 0) sfail = 0;
+    __syncthreads();
+    if (warp == 0) {
+      // Cholesky, right-looking, lane i = row i (no pivoting; fail on a pivot <= 0 or NaN).
+      // 1/L(j,j) = rsqrt(pivot) and L(j,j) = pivot * rsqrt(pivot): no divisions on the chain.
+      double g[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) g[k] = (lane < R) ? sL[lane * LS + k] : 0.0;
+      bool ok = true;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const double piv = __shfl_sync(0xffffffffu, g[j], j);
+        if (!(piv > 0.0)) {
+          ok = false;
+          break;
+        }
+        const double inv = rsqrt(piv);
+        if (lane == 0) sDi[j] = inv;
+        if (lane == j) g[j] = piv * inv;
+        else if (lane > j) g[j] *= inv;
+#pragma unroll
+        for (int k = j + 1; k < R; ++k) {
+          const double lkj = __shfl_sync(0xffffffffu, g[j], k);
+          if (lane >= k) g[k] = fma(-g[j], lkj, g[k]);
+        }
+      }
+      if (!ok) {
+        if (lane == 0) sfail = 1;
+      } else {
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          if (lane < R) sL[lane * LS + k] = (k <= lane) ? g[k] : 0.0;
+        __syncwarp();
+        // L^{-1}: lane c forms column c by forward substitution
+        double x[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+          for (int k = 0; k < i; ++k) s = fma(-sL[i * LS + k], x[k], s);
+          x[i] = (i >= lane) ? s * sDi[i] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+          if (lane < R) sLi[i * LS + lane] = x[i];
+      }
+    }
+    __syncthreads();
+    if (sfail) {
+      if (blockIdx.x == 0 && tid == 0) {
+        a.status[0] = (double)CP_ENOTSPD;
+        a.status[1] = (double)a.mode;
+      }
+    } else {
+      // y = L^{-1} b, then x = L^{-T} y, thread per (row, r)
+      for (int e = tid; e < nrows * R; e += blockDim.x) {
+        const int ii = e / R, r = e - (e / R) * R;
+        double y = 0.0;
+        for (int k = 0; k <= r; ++k) y = fma(sLi[r * LS + k], sB[ii * R + k], y);
+        scratch[e] = y;
+      }
+      __syncthreads();
+      double dm = 0.0, df = 0.0;
+      for (int e = tid; e < nrows * R; e += blockDim.x) {
+        const int ii = e / R, r = e - (e / R) * R;
+        double x = 0.0;
+        for (int k = r; k < R; ++k) x = fma(sLi[k * LS + r], scratch[ii * R + k], x);
+        const int64_t i = i0 + ii;
+        a.A[i + In * r] = x;
+        a.At[i * (R + (R & 1)) + r] = x;
+        sX[e] = x;
+        dm = fma(sM[e], x, dm);
+        if (a.F != nullptr) df = fma(a.F[i + In * r], x, df);
+      }
+      // partial Gram of the new rows, and the CTA's <M,A>, <F,A> (fixed order)
+      const double dms = block_sum_256(dm, scratch);
+      const double dfs = block_sum_256(df, scratch);
+      for (int e = tid; e < RR; e += blockDim.x) {
+        const int r = e % R, s = e / R;
+        double gg = 0.0;
+        for (int ii = 0; ii < nrows; ++ii) gg = fma(sX[ii * R + r], sX[ii * R + s], gg);
+        a.gcur[(int64_t)blockIdx.x * RR + e] = gg;
+      }
+      if (tid == 0) {
+        a.dotM[blockIdx.x] = dms;
+        a.dotF[blockIdx.x] = dfs;
+      }
+    }
+  }
+  if (a.fin_on) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) sticket = atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    if (sticket == gridDim.x - 1) {
+      __threadfence();
+      finalize_body(a.fin, scratch);
+      if (tid == 0) *a.ticket = 0u;
+    }
   }
 }
 
@@ -385,8 +409,11 @@ __global__ void __launch_bounds__(256) norm2_final_kernel(const double *part, in
 // After the Y_L pass, every segment i1 that a CTA boundary splits has its contributions in the
 // edge blocks of the CTAs c_lo..c_hi that cover it; block (c, chunk) completes the segment
 // holding v0(c) (the first boundary inside that segment does the work), summing the edge blocks
-// in CTA order into yl.  Afterwards yl holds Y_L(:, i1, :) for every i1.
+// in CTA order into yl.  Afterwards yl holds Y_L(:, i1, :) for every i1.  The contributing
+// edge blocks are located once per block (shared table); the element loop is plain 32-bit math.
 __global__ void __launch_bounds__(256) yl_fixup_kernel(const YLGeom y, int chunks) {
+  constexpr int kMaxContrib = 64;
+  __shared__ int64_t soff[kMaxContrib];
   const int64_t c = blockIdx.x / chunks + 1;
   const int chunk = blockIdx.x % chunks;
   const int64_t v0c = (c * y.Q) / y.Gc;
@@ -396,76 +423,84 @@ __global__ void __launch_bounds__(256) yl_fixup_kernel(const YLGeom y, int chunk
   if (v0p > s * y.Qn) return;                       // an earlier boundary in s handles it
   const int64_t clo = ((s * y.Qn + 1) * y.Gc - 1) / y.Q;
   const int64_t chi = (((s + 1) * y.Qn) * y.Gc - 1) / y.Q;
+  const int nc = (int)(chi - clo + 1);
   const int64_t blk = y.I0 * y.R;
-  const int64_t e0 = (blk * chunk) / chunks, e1 = (blk * (chunk + 1)) / chunks;
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    const int64_t i0 = e % y.I0;
-    const int rb = (int)(i0 / y.Wmax);
+  for (int k = threadIdx.x; k < nc && k < kMaxContrib; k += blockDim.x) {
+    const int64_t cc = clo + k;
+    const int64_t seg_first = ((cc * y.Q) / y.Gc) / y.Qn;
+    soff[k] = (cc * y.RB * 2 + ((seg_first == s) ? 0 : 1)) * blk;
+  }
+  __syncthreads();
+  const int I0 = (int)y.I0;
+  const int e0 = (int)((blk * chunk) / chunks), e1 = (int)((blk * (chunk + 1)) / chunks);
+  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int rb = (y.RB == 1) ? 0 : (e % I0) / y.Wmax;
+    const double *src = y.edge + (int64_t)rb * 2 * blk + e;
     double acc = 0.0;
-    for (int64_t cc = clo; cc <= chi; ++cc) {
+    int k = 0;
+    for (; k < nc && k < kMaxContrib; ++k) acc += src[soff[k]];
+    for (; k < nc; ++k) {  // (more than kMaxContrib CTAs share one segment: tiny tensors only)
+      const int64_t cc = clo + k;
       const int64_t seg_first = ((cc * y.Q) / y.Gc) / y.Qn;
-      const int ed = (seg_first == s) ? 0 : 1;
-      acc += y.edge[((cc * y.RB + rb) * 2 + ed) * blk + e];
+      acc += src[(cc * y.RB * 2 + ((seg_first == s) ? 0 : 1)) * blk];
     }
     ((double *)y.yl)[s * blk + e] = acc;
   }
 }
 
-// M0(i0, r) = sum_{i1} Y_L(i0, i1, r) A^(1)(i1, r): thread per (i0, r, split j of the i1
-// range); the sp partial sums combine in split order
-__global__ void __launch_bounds__(256) ymm0_kernel(const YLGeom y, const double *At1, int RS, int sp,
-                                                   double *M0) {
-  __shared__ double sred[256];
-  const int tid = threadIdx.x;
-  const int64_t ent = ((int64_t)blockIdx.x * blockDim.x + tid) / sp;
-  const int j = tid % sp;
-  double s = 0.0;
-  if (ent < y.I0 * y.R) {
-    const int64_t i0 = ent % y.I0;
-    const int r = (int)(ent / y.I0);
-    const int64_t blk = y.I0 * y.R;
-    const double *yp = y.yl + i0 + y.I0 * r;
-    const int64_t a = (y.I1 * j) / sp, b = (y.I1 * (j + 1)) / sp;
-    double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+// M0(i0, r) = sum_{i1} Y_L(i0, i1, r) A^(1)(i1, r).  Block (32-row tile of i0, r): lane -> i0
+// (coalesced Y_L reads), warp w -> the w-th eighth of the i1 range; the 8 warp partials combine
+// in warp order.  A1 is the column-major factor (I1 x R).
+__global__ void __launch_bounds__(256) ymm0_kernel(const YLGeom y, const double *A1, double *M0) {
+  __shared__ double sred[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int r = blockIdx.y;
+  const int64_t i0 = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t blk = y.I0 * y.R;
+  const int64_t a = (y.I1 * w) / 8, b = (y.I1 * (w + 1)) / 8;
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (i0 < y.I0) {
+    const double *yp = y.yl + y.I0 * r + i0;
+    const double *ap = A1 + y.I1 * r;
     int64_t i1 = a;
-    for (; i1 + 3 < b; i1 += 4) {
-      s = fma(yp[i1 * blk], At1[i1 * RS + r], s);
-      s1 = fma(yp[(i1 + 1) * blk], At1[(i1 + 1) * RS + r], s1);
-      s2 = fma(yp[(i1 + 2) * blk], At1[(i1 + 2) * RS + r], s2);
-      s3 = fma(yp[(i1 + 3) * blk], At1[(i1 + 3) * RS + r], s3);
+    for (; i1 + 8 <= b; i1 += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s[j] = fma(yp[(i1 + j) * blk], ap[i1 + j], s[j]);
     }
-    for (; i1 < b; ++i1) s = fma(yp[i1 * blk], At1[i1 * RS + r], s);
-    s = (s + s1) + (s2 + s3);
+    for (int j = 0; i1 < b; ++i1, ++j) s[j] = fma(yp[i1 * blk], ap[i1], s[j]);
   }
-  sred[tid] = s;
+  sred[w][lane] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
   __syncthreads();
-  if (j == 0 && ent < y.I0 * y.R) {
+  if (w == 0 && i0 < y.I0) {
     double t = 0.0;
-    for (int k = 0; k < sp; ++k) t += sred[tid + k];
-    M0[ent] = t;  // ent = i0 + I0 * r: column-major I0 x R
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sred[k][lane];
+    M0[i0 + y.I0 * r] = t;
   }
 }
 
 // M1(i1, r) = sum_{i0} Y_L(i0, i1, r) A^(0)(i0, r): warp per (i1, r), lanes stride over i0
-// (contiguous), fixed shuffle tree
-__global__ void __launch_bounds__(256) ymm1_kernel(const YLGeom y, const double *At0, int RS, double *M1) {
+// (contiguous in Y_L and in the column-major A0), 8 independent partial sums per lane, fixed
+// shuffle tree
+__global__ void __launch_bounds__(256) ymm1_kernel(const YLGeom y, const double *A0, double *M1) {
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= y.I1 * y.R) return;
   const int64_t i1 = w % y.I1;
   const int r = (int)(w / y.I1);
   const double *yp = y.yl + i1 * y.I0 * y.R + y.I0 * r;
-  double s = 0.0, s1 = 0.0;
+  const double *ap = A0 + y.I0 * r;
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int64_t i0 = lane;
-  for (; i0 + 32 < y.I0; i0 += 64) {
-    s = fma(yp[i0], At0[i0 * RS + r], s);
-    s1 = fma(yp[i0 + 32], At0[(i0 + 32) * RS + r], s1);
-  }
-  if (i0 < y.I0) s = fma(yp[i0], At0[i0 * RS + r], s);
-  s += s1;
+  for (; i0 + 7 * 32 < y.I0; i0 += 8 * 32) {
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (lane == 0) M1[i1 + y.I1 * r] = s;
+    for (int j = 0; j < 8; ++j) s[j] = fma(yp[i0 + 32 * j], ap[i0 + 32 * j], s[j]);
+  }
+  for (int j = 0; i0 < y.I0; i0 += 32, ++j) s[j] = fma(yp[i0], ap[i0], s[j]);
+  double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+  if (lane == 0) M1[i1 + y.I1 * r] = t;
 }
 
 // warp per (i_m, r): lanes stride over the other indices j of modes 2..N-1
@@ -511,19 +546,14 @@ cudaError_t launch_yl_fixup(const YLGeom &y, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_ymm0(const YLGeom &y, const double *At1, int RS, double *M0, cudaStream_t st) {
-  int sp = (int)(y.I1 / 16);
-  if (sp < 1) sp = 1;
-  if (sp > 32) sp = 32;
-  while (256 % sp) --sp;
-  const int64_t threads = y.I0 * y.R * sp;
-  ymm0_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(y, At1, RS, sp, M0);
+cudaError_t launch_ymm0(const YLGeom &y, const double *A1, double *M0, cudaStream_t st) {
+  ymm0_kernel<<<dim3((unsigned)((y.I0 + 31) / 32), (unsigned)y.R), 256, 0, st>>>(y, A1, M0);
   return cudaGetLastError();
 }
 
-cudaError_t launch_ymm1(const YLGeom &y, const double *At0, int RS, double *M1, cudaStream_t st) {
+cudaError_t launch_ymm1(const YLGeom &y, const double *A0, double *M1, cudaStream_t st) {
   const int64_t threads = y.I1 * y.R * 32;
-  ymm1_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(y, At0, RS, M1);
+  ymm1_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(y, A0, M1);
   return cudaGetLastError();
 }
 

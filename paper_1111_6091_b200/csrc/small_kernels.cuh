@@ -83,6 +83,18 @@ struct PrepGrams {
   int nblk[CP_MAX_N];
 };
 
+struct FinalizeArgs {
+  int N, R, nlast, dot_stride;
+  int nsolve[CP_MAX_N];
+  const double *glast, *dotM_last, *dotF;
+  double *Ups;
+  const double *normZ2;
+  double *status, *out;
+};
+
+// status area (8 doubles): [0] status, [1] failed mode, [kTicketSlot] completion ticket (u32)
+constexpr int kTicketSlot = 4;
+
 struct SolveArgs {
   int N, R, mode, prev_mode, nprev, rpc, sp;
   int64_t In;
@@ -96,15 +108,9 @@ struct SolveArgs {
   double *gcur;         // this kernel's per-CTA partial Grams
   double *dotM, *dotF;  // per-CTA <M,A>, <F,A>
   double *status;       // [0] status, [1] failed mode
-};
-
-struct FinalizeArgs {
-  int N, R, nlast, dot_stride;
-  int nsolve[CP_MAX_N];
-  const double *glast, *dotM_last, *dotF;
-  double *Ups;
-  const double *normZ2;
-  double *status, *out;
+  int fin_on;           // last solve of the sweep: the last block to finish runs the finalize
+  unsigned *ticket;
+  FinalizeArgs fin;
 };
 
 struct GradArgs {
@@ -149,10 +155,10 @@ inline ReduceGeom direct_geom(const double *M, int64_t rows, int R) {
 }
 // completes the segments split between CTAs (edge blocks -> yl)
 cudaError_t launch_yl_fixup(const YLGeom &y, cudaStream_t st);
-// M0(i0, r) = sum_{i1} Y_L(i0, i1, r) A^(1)(i1, r)   (At1: row-major copy, stride RS)
-cudaError_t launch_ymm0(const YLGeom &y, const double *At1, int RS, double *M0, cudaStream_t st);
-// M1(i1, r) = sum_{i0} Y_L(i0, i1, r) A^(0)(i0, r)
-cudaError_t launch_ymm1(const YLGeom &y, const double *At0, int RS, double *M1, cudaStream_t st);
+// M0(i0, r) = sum_{i1} Y_L(i0, i1, r) A^(1)(i1, r)   (A1: column-major I1 x R)
+cudaError_t launch_ymm0(const YLGeom &y, const double *A1, double *M0, cudaStream_t st);
+// M1(i1, r) = sum_{i0} Y_L(i0, i1, r) A^(0)(i0, r)   (A0: column-major I0 x R)
+cudaError_t launch_ymm1(const YLGeom &y, const double *A0, double *M1, cudaStream_t st);
 // M_m(i_m, r) = sum_{j: i_m(j)} Y_R(j, r) prod_{k >= 2, k != m} A^(k)(i_k(j), r), j over modes 2..N-1
 struct YRArgs {
   int N, R, RS, mode;
