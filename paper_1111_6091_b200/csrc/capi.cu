@@ -32,6 +32,14 @@ const StreamEntry &stream_entry(int R, int V, int op) {
   return g_table[stream_index(R, V, op)];
 }
 
+static StreamEntry g_mma_table[kMmaTableSize];
+static std::once_flag g_mma_once;
+
+const StreamEntry &stream_mma_entry(int nt, int mt, int op) {
+  std::call_once(g_mma_once, [] { register_stream_mma(g_mma_table); });
+  return g_mma_table[mma_index(nt, mt, op)];
+}
+
 static int device_sms() {
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 148;
@@ -43,6 +51,11 @@ static int device_sms() {
 static int env_int(const char *name, int dflt) {
   const char *v = getenv(name);
   return (v && *v) ? atoi(v) : dflt;
+}
+
+bool pdl_enabled() {
+  static const bool on = env_int("CP_PDL", 1) != 0;
+  return on;
 }
 
 static int stream_occupancy(int R, int V, int op, int smem) {
@@ -60,7 +73,73 @@ static int stream_occupancy(int R, int V, int op, int smem) {
   return n > 0 ? n : 1;
 }
 
+static int stream_mma_occupancy(int nt, int mt, int op, int smem) {
+  const StreamEntry &e = stream_mma_entry(nt, mt, op);
+  int n = 0;
+  if (cudaFuncSetAttribute(e.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, e.kernel, kStreamThreads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  return n > 0 ? n : 1;
+}
+
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// v-order digits (see StreamPlan); false if a radix does not fit 32 bits
+static bool plan_digits(StreamPlan &p, const cp_shape &s) {
+  int64_t qstride[CP_MAX_N];
+  qstride[1] = 1;
+  for (int k = 2; k < s.N; ++k) qstride[k] = qstride[k - 1] * s.dims[k - 1];
+  int j = 0;
+  for (int k = 1; k < s.N; ++k)
+    if (k != p.mode) p.ord[j++] = k;
+  if (p.mode != 0) p.ord[j++] = p.mode;
+  p.nd = j;
+  for (int t = 0; t < p.nd; ++t) {
+    if (s.dims[p.ord[t]] > 0x7fffffff) return false;
+    p.rad[t] = (int)s.dims[p.ord[t]];
+    p.qsd[t] = qstride[p.ord[t]];
+  }
+  return true;
+}
+
+// FP64 tensor-core consumer geometry (stream_mma.cuh): row block, k-split and m-tiles per warp
+static bool plan_mma(StreamPlan &p, const cp_shape &s, int op) {
+  if (env_int("CP_STREAM_MMA", 1) == 0 || op == OP_RESID || s.R > 32 || (p.I1 & 1)) return false;
+  p.nt = (s.R + 7) / 8;
+  int mt_max = (p.nt <= 2) ? 8 : 4;
+  const int mt_env = env_int("CP_MMA_MTMAX", 4);  // measured: MT = 8 (64 accumulators) serializes the A loads
+  if (mt_max > mt_env) mt_max = mt_env;
+  int64_t Wt = p.I1;
+  if (ceil_div(p.I1, 8) > 8 * mt_max) Wt = 64 * mt_max;
+  p.RB = (int)ceil_div(p.I1, Wt);
+  int64_t W = ceil_div(p.I1, p.RB);
+  W = ceil_div(W, 8) * 8;
+  p.Wmax = (int)W;
+  const int mtiles = (int)(W / 8);
+  double best = -1.0;
+  for (int ks = 1; ks <= 8; ks *= 2) {
+    const int wpg = kConsumerWarps / ks;
+    const int mt = (mtiles + wpg - 1) / wpg;
+    if (mt > mt_max) continue;
+    const double eff = (double)mtiles * ks / (8.0 * mt) - 0.02 * (ks > 1);
+    if (eff > best + 1e-9) {
+      best = eff;
+      p.ks = ks;
+      p.mt = mt;
+    }
+  }
+  if (best < 0) return false;
+  p.mma = 1;
+  p.V = 2;
+  p.zcs = (int)(ceil_div(W, 16) * 16 + 8);  // = 8 (mod 16) doubles: conflict-free A fragments
+  return true;
+}
 
 bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms) {
   memset(&p, 0, sizeof(p));
@@ -75,38 +154,6 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   }
   p.I1 = s.dims[0];
   p.Q = P / p.I1;
-  // rows per consumer thread: the largest V dividing I1 with V * RT <= 32 accumulators, which
-  // keeps the kernel at <= 96 registers and 2 CTAs/SM (measured: 2 CTAs/SM beat 1 CTA/SM with
-  // a larger register tile, profiles/README.md); residual pass: V <= 4 and V * R <= 64
-  const int RT = stream_rt(s.R, op), RG = stream_rg(s.R, op);
-  const int vmax_env = env_int("CP_MAX_V", 8);
-  const int vr_max = env_int("CP_MAX_VR", 32);
-  p.V = 1;
-  for (int v : {8, 4, 2}) {
-    if (v > vmax_env || p.I1 % v != 0) continue;
-    if (op != OP_RESID && v * RT > vr_max && v > 2) continue;
-    if (op == OP_RESID && (v > 4 || v * s.R > 64)) continue;
-    p.V = v;
-    break;
-  }
-  int maxW = (kConsumers / RG) * p.V;  // one column per sub-tile at most
-  if (maxW > kMaxRows) maxW = kMaxRows;
-  // row-block width: mode 0 MTTKRP uses narrower blocks (fewer column groups -> smaller I1 x R
-  // partials); every other pass keeps whole columns in one CTA.
-  int64_t Wt = p.I1;
-  if (op != OP_RESID && p.mode == 0) {
-    const int w0 = env_int("CP_MTTKRP_W0", 512);
-    if (p.I1 >= 2 * w0) Wt = w0;
-  }
-  if (op == OP_YL) {
-    const int w0 = env_int("CP_YL_W", 512);
-    if (p.I1 >= 2 * w0) Wt = w0;
-  }
-  if (Wt > maxW) Wt = maxW;
-  p.RB = (int)ceil_div(p.I1, Wt);
-  int64_t W = ceil_div(p.I1, p.RB);
-  while (W % p.V) ++W;
-  p.Wmax = (int)W;
   if (p.mode == 0) {
     p.In = 1;
     p.Qn = p.Q;
@@ -118,47 +165,99 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     for (int k = 1; k < mode; ++k) L *= s.dims[k];
     p.L = L;
   }
-  // v-order digits (see StreamPlan)
-  {
-    int64_t qstride[CP_MAX_N];
-    qstride[1] = 1;
-    for (int k = 2; k < s.N; ++k) qstride[k] = qstride[k - 1] * s.dims[k - 1];
-    int j = 0;
-    for (int k = 1; k < s.N; ++k)
-      if (k != p.mode) p.ord[j++] = k;
-    if (p.mode != 0) p.ord[j++] = p.mode;
-    p.nd = j;
-    for (int t = 0; t < p.nd; ++t) {
-      if (s.dims[p.ord[t]] > 0x7fffffff) return false;
-      p.rad[t] = (int)s.dims[p.ord[t]];
-      p.qsd[t] = qstride[p.ord[t]];
-    }
-  }
-  const int U = p.Wmax / p.V;
-  const int cpt = (kConsumers / (U * RG)) > 0 ? (kConsumers / (U * RG)) : 1;
-  const int stage_target = env_int("CP_STAGE_BYTES", 40960);  // tools/sweep4.sh
-  int cps = stage_target / (p.Wmax * 8);
-  if (cps < 1) cps = 1;
-  if (cps >= cpt) cps = (cps / cpt) * cpt;
-  else cps = cpt;
-  if (cps > 64) cps = 64;
-  if (cps > p.Q) cps = (int)p.Q;
-  p.cps = cps;
+  if (!plan_digits(p, s)) return false;
+  const int RT = stream_rt(s.R, op), RG = stream_rg(s.R, op);
   const int WSTR = (s.R % 2 == 0) ? s.R + 2 : s.R + 1;
   p.RS = s.R + (s.R & 1);
-  const int stage_doubles = cps * p.Wmax + cps * p.RS + cps * WSTR;
+  const int stage_target = env_int("CP_STAGE_BYTES", 40960);
+  int cps, cpt = 1;
+  if (plan_mma(p, s, op)) {
+    // stage: a multiple of 4 KS columns (k-steps of every k-group)
+    const int unit = 4 * p.ks;
+    cps = stage_target / (p.zcs * 8);
+    cps = (cps / unit) * unit;
+    if (cps < unit) cps = unit;
+    if (cps > 64) cps = 64;
+    p.zst = cps * p.zcs;
+    const bool has_f0 = (p.ord[0] != p.mode);
+    p.direct_w = (has_f0 && (p.nd == 1 || (p.nd == 2 && p.ord[1] == p.mode))) ? 1 : 0;
+    const int RP = 8 * p.nt;
+    if (op == OP_YL) p.red_doubles = (p.ks - 1) * p.Wmax * RP + 8;
+    else if (p.mode != 0) p.red_doubles = kConsumerWarps * RP + 8;
+    else p.red_doubles = 8;
+  } else {
+    // rows per consumer thread: the largest V dividing I1 with V * RT <= 32 accumulators, which
+    // keeps the kernel at <= 96 registers and 2 CTAs/SM; residual pass: V <= 4 and V * R <= 64
+    const int vmax_env = env_int("CP_MAX_V", 8);
+    const int vr_max = env_int("CP_MAX_VR", 32);
+    p.V = 1;
+    for (int v : {8, 4, 2}) {
+      if (v > vmax_env || p.I1 % v != 0) continue;
+      if (op != OP_RESID && v * RT > vr_max && v > 2) continue;
+      if (op == OP_RESID && (v > 4 || v * s.R > 64)) continue;
+      p.V = v;
+      break;
+    }
+    int maxW = (kConsumers / RG) * p.V;  // one column per sub-tile at most
+    if (maxW > kMaxRows) maxW = kMaxRows;
+    // row-block width: mode 0 MTTKRP uses narrower blocks (fewer column groups -> smaller I1 x R
+    // partials); every other pass keeps whole columns in one CTA.
+    int64_t Wt = p.I1;
+    if (op != OP_RESID && p.mode == 0) {
+      const int w0 = env_int("CP_MTTKRP_W0", 512);
+      if (p.I1 >= 2 * w0) Wt = w0;
+    }
+    if (op == OP_YL) {
+      const int w0 = env_int("CP_YL_W", 512);
+      if (p.I1 >= 2 * w0) Wt = w0;
+    }
+    if (Wt > maxW) Wt = maxW;
+    p.RB = (int)ceil_div(p.I1, Wt);
+    int64_t W = ceil_div(p.I1, p.RB);
+    while (W % p.V) ++W;
+    p.Wmax = (int)W;
+    const int U = p.Wmax / p.V;
+    cpt = (kConsumers / (U * RG)) > 0 ? (kConsumers / (U * RG)) : 1;
+    cps = stage_target / (p.Wmax * 8);
+    if (cps < 1) cps = 1;
+    if (cps >= cpt) cps = (cps / cpt) * cpt;
+    else cps = cpt;
+    if (cps > 64) cps = 64;
+    p.zst = cps * p.Wmax;
+    // consumers' shared reduction area (stream_kernel.cuh): residual pass: one double per warp;
+    // mode >= 1 MTTKRP: one RT-vector per warp when every warp holds a single rank group (RG = 1
+    // or U a multiple of 32 in every row block), else one per thread; Y_L pass with several
+    // column slots: G regions of Wmax x R (G <= cpt - 1, within the generic budget); mode-0
+    // MTTKRP reduces through the Z ring instead.
+    const int generic = 256 * RT + 8;
+    int red = 8;
+    if (op == OP_MTTKRP && p.mode != 0) {
+      const int64_t Wlast = p.I1 - (int64_t)(p.RB - 1) * p.Wmax;
+      const bool warp_uniform = (RG == 1) || ((p.Wmax / p.V) % 32 == 0 && (Wlast / p.V) % 32 == 0);
+      red = warp_uniform ? kConsumerWarps * RT + 8 : generic;
+    } else if (op == OP_YL && cpt > 1) {
+      int G = generic / (p.Wmax * s.R);
+      if (G > cpt - 1) G = cpt - 1;
+      if (G < 1) G = 1;
+      red = G * p.Wmax * s.R;
+    }
+    p.red_doubles = red;
+  }
+  if (cps > p.Q) cps = (int)p.Q;
+  p.cps = cps;
+  const int stage_doubles = p.zst + cps * p.RS + cps * WSTR;
   int nst = env_int("CP_RING_BYTES", 96 * 1024) / (stage_doubles * 8);
   if (nst < 2) nst = 2;
   if (nst > 8) nst = 8;
-  // mode-0 slot reduction reuses the Z ring: it must hold Wmax x R doubles
-  while ((int64_t)nst * cps * p.Wmax < (int64_t)p.Wmax * s.R) ++nst;
+  // mode-0 slot / k-group reduction reuses the Z ring: it must hold the reduced blocks
+  const int64_t need = p.mma ? (int64_t)(p.ks - 1) * p.Wmax * 8 * p.nt : (int64_t)p.Wmax * s.R;
+  while ((int64_t)nst * p.zst < need) ++nst;
   p.nstages = nst;
-  p.red_doubles = stream_red_doubles(s.R, op);
-  if (op == OP_YL && cpt > 1 && p.red_doubles < p.Wmax * s.R) p.red_doubles = p.Wmax * s.R;
-  // ring | red | sS[32] | 3 x nst mbarriers | nst x 16-int headers
+  p.dbg = env_int("CP_STREAM_DBG", 0);
   p.smem_bytes = (nst * stage_doubles + p.red_doubles + 32) * 8 + nst * 24 + nst * 64 + 64;
   if (p.smem_bytes > 200 * 1024) return false;
-  const int occ = stream_occupancy(s.R, p.V, op, p.smem_bytes);
+  const int occ = p.mma ? stream_mma_occupancy(p.nt, p.mt, op, p.smem_bytes)
+                        : stream_occupancy(s.R, p.V, op, p.smem_bytes);
   const int ctas = env_int("CP_CTAS_PER_SM", 0);
   const int64_t Gtot = (int64_t)num_sms * (ctas > 0 ? (ctas < occ ? ctas : occ) : occ);
   int64_t Gc = Gtot / p.RB;
@@ -202,7 +301,7 @@ static double stream_alg_bytes(const StreamPlan &p) {
 }
 
 cudaError_t launch_stream(const StreamPlan &p, cudaStream_t st) {
-  const StreamEntry &e = stream_entry(p.R, p.V, p.op);
+  const StreamEntry &e = p.mma ? stream_mma_entry(p.nt, p.mt, p.op) : stream_entry(p.R, p.V, p.op);
   ++g_launches;
   const bool prof = g_prof_on && g_prof_n < kProfMax;
   if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], st);
@@ -345,12 +444,6 @@ static int check_ws(const Layout &L, void *ws, size_t ws_bytes) {
 
 static int ret_cuda(cudaError_t e) { return e == cudaSuccess ? CP_OK : CP_ECUDA; }
 
-#define CK_LAUNCH()                                  \
-  do {                                               \
-    cudaError_t _e = cudaGetLastError();             \
-    if (_e != cudaSuccess) return CP_ECUDA;          \
-  } while (0)
-
 }  // namespace cpk
 
 using namespace cpk;
@@ -382,10 +475,8 @@ int cp_norm2(const cp_shape *s, const double *Z, double *out, void *ws, size_t w
   const int nb = 2 * device_sms();
   double *part = static_cast<double *>(ws);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
-  norm2_kernel<<<nb, 512, 0, cs>>>(Z, P, part);
-  CK_LAUNCH();
-  norm2_final_kernel<<<1, 256, 0, cs>>>(part, nb, out);
-  CK_LAUNCH();
+  if (launch_k(norm2_kernel, dim3(nb), dim3(512), 0, cs, Z, P, part) != cudaSuccess) return CP_ECUDA;
+  if (launch_k(norm2_final_kernel, dim3(1), dim3(256), 0, cs, (const double *)part, nb, out) != cudaSuccess) return CP_ECUDA;
   g_launches = 2;
   return CP_OK;
 }
@@ -413,8 +504,8 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
   p.part = w + L.part;
   if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
   const ReduceGeom g = reduce_geom(p);
-  reduce_mttkrp_kernel<<<L.nsolve[mode], 256, 0, cs>>>(g, L.rpc[mode], L.sp[mode], M);
-  CK_LAUNCH();
+  if (launch_k(reduce_mttkrp_kernel, dim3(L.nsolve[mode]), dim3(256), 0, cs, g, L.rpc[mode], L.sp[mode], M) != cudaSuccess)
+    return CP_ECUDA;
   g_launches = 3;
   return CP_OK;
 }
@@ -533,8 +624,8 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     if (N == 3) {
       if (!solve_mode(2, reduce_geom(p2), L.rpc2, L.sp2)) return CP_ECUDA;
     } else {
-      reduce_mttkrp_kernel<<<L.nyr, 256, 0, cs>>>(reduce_geom(p2), L.rpc2, L.sp2, w + L.yr);
-      CK_LAUNCH();
+      if (launch_k(reduce_mttkrp_kernel, dim3(L.nyr), dim3(256), 0, cs, reduce_geom(p2), L.rpc2, L.sp2, w + L.yr) != cudaSuccess)
+        return CP_ECUDA;
       ++launches;
       for (int m = 2; m < N; ++m) {
         YRArgs ya;
@@ -642,8 +733,7 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
     ga.Ups = w + L.Ups;
     ga.G = (G != nullptr) ? G[n] : nullptr;
     ga.gpart = w + L.gradp + (size_t)n * L.grad_max;
-    gradient_kernel<<<L.ngrad[n], 256, 0, cs>>>(ga);
-    CK_LAUNCH();
+    if (launch_k(gradient_kernel, dim3(L.ngrad[n]), dim3(256), 0, cs, ga) != cudaSuccess) return CP_ECUDA;
     launches += 2;
   }
   FitFinalArgs fa;
@@ -656,8 +746,7 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
   fa.gpart = w + L.gradp;
   fa.normZ2 = normZ2;
   fa.out = out;
-  finalize_fit_kernel<<<1, 256, 0, cs>>>(fa);
-  CK_LAUNCH();
+  if (launch_k(finalize_fit_kernel, dim3(1), dim3(256), 0, cs, fa) != cudaSuccess) return CP_ECUDA;
   g_launches = launches + 1;
   return CP_OK;
 }

@@ -2,6 +2,7 @@
 // Product code: nothing here is shared with, or derived from, oracle/.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "../../include/cp.h"
@@ -53,6 +54,13 @@ struct StreamPlan {
   double *yl;       // OP_YL: I0 x R block per fully owned segment (segment-major)
   double *edge;     // OP_YL: per CTA 2 blocks for partially owned segments
   int red_doubles;  // consumers' shared reduction area (doubles)
+  // FP64 tensor-core consumers (stream_mma.cuh): mma = 1 selects stream_mma_kernel<NT, MT, OP>
+  int mma;
+  int ks, mt, nt;   // k-split groups, m-tiles (8 rows) per warp, n-tiles (8 ranks)
+  int zcs;          // shared-memory column stride of a Z stage (doubles); 0: the block width Wb
+  int zst;          // doubles per Z stage in shared memory
+  int direct_w;     // Khatri-Rao rows are the staged factor rows (no weight warp)
+  int dbg;          // experiments only (env CP_STREAM_DBG): 1 = consumers skip the FMAs, 2 = weight warp skips forming
 };
 
 // Kernel table: one entry per (R, V, op) instantiation of stream_kernel.
@@ -78,11 +86,42 @@ void register_stream_part1(StreamEntry *t);
 void register_stream_part2(StreamEntry *t);
 void register_stream_part3(StreamEntry *t);
 const StreamEntry &stream_entry(int R, int V, int op);
+// FP64 tensor-core variants stream_mma_kernel<NT, MT, OP> (OP_MTTKRP, OP_YL)
+constexpr int mma_index(int nt, int mt, int op) { return ((nt - 1) * 8 + (mt - 1)) * 2 + (op == 2 ? 1 : 0); }
+constexpr int kMmaTableSize = mma_index(4, 8, 2) + 1;
+void register_stream_mma(StreamEntry *t);
+const StreamEntry &stream_mma_entry(int nt, int mt, int op);
 
 // Host: build the plan (geometry only; pointers filled by the caller).
 bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms);
 size_t stream_part_doubles(const StreamPlan &p);
 cudaError_t launch_stream(const StreamPlan &p, cudaStream_t st);
+
+// Programmatic dependent launch (PDL): the sweep's kernels are launched with programmatic
+// stream serialization, so a kernel's blocks are scheduled while its predecessor drains.  Every
+// kernel launched that way starts with griddep(): allow the next kernel to launch, then wait
+// until the predecessor grid has completed and its writes are visible (before any global
+// access and before any early return, so completion stays transitive along the stream).
+__device__ __forceinline__ void griddep() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+bool pdl_enabled();  // env CP_PDL (default 1)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {

@@ -66,6 +66,7 @@ __device__ void gather_rows(const ReduceGeom &g, int64_t i0, int nrows, int R, i
 }
 
 __global__ void __launch_bounds__(256) reduce_mttkrp_kernel(const ReduceGeom g, int rpc, int sp, double *M) {
+  griddep();
   __shared__ double sM[256], scratch[256];
   const int64_t i0 = (int64_t)blockIdx.x * rpc;
   const int nrows = (int)((g.In_rows - i0) < rpc ? (g.In_rows - i0) : rpc);
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(256) reduce_mttkrp_kernel(const ReduceGeom g, 
 // One block per (mode k, chunk of kPrepRows rows): At^(k) rows (row-major copy, padded stride
 // RS) and the chunk's partial Gram A_chunk^T A_chunk, summed later in chunk order.
 __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
+  griddep();
   __shared__ double sA[kPrepRows * 33];  // chunk x R, column-major (r * kPrepRows + ii)
   int k = 0;
   while (k + 1 < a.N && (int)blockIdx.x >= a.blk_off[k + 1]) ++k;
@@ -164,6 +166,7 @@ __device__ void finalize_body(const FinalizeArgs &a, double *sred) {
 }
 
 __global__ void __launch_bounds__(256) finalize_sweep_kernel(const FinalizeArgs a) {
+  griddep();
   __shared__ double sred[256];
   finalize_body(a, sred);
 }
@@ -175,6 +178,7 @@ __global__ void __launch_bounds__(256) finalize_sweep_kernel(const FinalizeArgs 
 // (completion ticket; every sum keeps its fixed order, so results stay bitwise reproducible).
 template <int R>
 __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
+  griddep();
   constexpr int RR = R * R;
   constexpr int LS = R + 1;  // smem row stride of the R x R matrices
   __shared__ double sL[R * LS];    // Gamma, then L (lower)
@@ -325,6 +329,7 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
 // ---------------------------------------------------------------- gradient (cp_fit)
 // G^(n)(i,r) = -M(i,r) + sum_s A(i,s) Gamma(s,r) - F(i,r)   (eq:gradEqn; FAS residual with F)
 __global__ void __launch_bounds__(256) gradient_kernel(const GradArgs a) {
+  griddep();
   __shared__ double sG[32 * 32];
   __shared__ double sM[256], scratch[256];
   const int R = a.R, RR = R * R, tid = threadIdx.x;
@@ -354,6 +359,7 @@ __global__ void __launch_bounds__(256) gradient_kernel(const GradArgs a) {
 }
 
 __global__ void __launch_bounds__(256) finalize_fit_kernel(const FitFinalArgs a) {
+  griddep();
   __shared__ double sred[256];
   const int tid = threadIdx.x;
   double rs = 0.0;
@@ -376,6 +382,7 @@ __global__ void __launch_bounds__(256) finalize_fit_kernel(const FitFinalArgs a)
 // ---------------------------------------------------------------- ||Z||^2
 __global__ void __launch_bounds__(512) norm2_kernel(const double *__restrict__ Z, int64_t P,
                                                     double *part) {
+  griddep();
   __shared__ double sred[512];
   const int tid = threadIdx.x;
   double s0 = 0.0, s1 = 0.0;
@@ -398,6 +405,7 @@ __global__ void __launch_bounds__(512) norm2_kernel(const double *__restrict__ Z
 }
 
 __global__ void __launch_bounds__(256) norm2_final_kernel(const double *part, int n, double *out) {
+  griddep();
   __shared__ double sred[256];
   double s = 0.0;
   for (int c = threadIdx.x; c < n; c += blockDim.x) s += part[c];
@@ -412,6 +420,7 @@ __global__ void __launch_bounds__(256) norm2_final_kernel(const double *part, in
 // in CTA order into yl.  Afterwards yl holds Y_L(:, i1, :) for every i1.  The contributing
 // edge blocks are located once per block (shared table); the element loop is plain 32-bit math.
 __global__ void __launch_bounds__(256) yl_fixup_kernel(const YLGeom y, int chunks) {
+  griddep();
   constexpr int kMaxContrib = 64;
   __shared__ int64_t soff[kMaxContrib];
   const int64_t c = blockIdx.x / chunks + 1;
@@ -452,6 +461,7 @@ __global__ void __launch_bounds__(256) yl_fixup_kernel(const YLGeom y, int chunk
 // (coalesced Y_L reads), warp w -> the w-th eighth of the i1 range; the 8 warp partials combine
 // in warp order.  A1 is the column-major factor (I1 x R).
 __global__ void __launch_bounds__(256) ymm0_kernel(const YLGeom y, const double *A1, double *M0) {
+  griddep();
   __shared__ double sred[8][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int r = blockIdx.y;
@@ -483,6 +493,7 @@ __global__ void __launch_bounds__(256) ymm0_kernel(const YLGeom y, const double 
 // (contiguous in Y_L and in the column-major A0), 8 independent partial sums per lane, fixed
 // shuffle tree
 __global__ void __launch_bounds__(256) ymm1_kernel(const YLGeom y, const double *A0, double *M1) {
+  griddep();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= y.I1 * y.R) return;
@@ -505,6 +516,7 @@ __global__ void __launch_bounds__(256) ymm1_kernel(const YLGeom y, const double 
 
 // warp per (i_m, r): lanes stride over the other indices j of modes 2..N-1
 __global__ void __launch_bounds__(256) yr_kernel(const YRArgs a) {
+  griddep();
   const int64_t Im = a.dims[a.mode];
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -542,32 +554,27 @@ cudaError_t launch_yl_fixup(const YLGeom &y, cudaStream_t st) {
   if (y.Gc < 2) return cudaSuccess;
   int chunks = (int)((y.I0 * y.R + 2047) / 2048);
   if (chunks > 16) chunks = 16;
-  yl_fixup_kernel<<<(unsigned)((y.Gc - 1) * chunks), 256, 0, st>>>(y, chunks);
-  return cudaGetLastError();
+  return launch_k(yl_fixup_kernel, dim3((unsigned)((y.Gc - 1) * chunks)), dim3(256), 0, st, y, chunks);
 }
 
 cudaError_t launch_ymm0(const YLGeom &y, const double *A1, double *M0, cudaStream_t st) {
-  ymm0_kernel<<<dim3((unsigned)((y.I0 + 31) / 32), (unsigned)y.R), 256, 0, st>>>(y, A1, M0);
-  return cudaGetLastError();
+  return launch_k(ymm0_kernel, dim3((unsigned)((y.I0 + 31) / 32), (unsigned)y.R), dim3(256), 0, st, y, A1, M0);
 }
 
 cudaError_t launch_ymm1(const YLGeom &y, const double *A0, double *M1, cudaStream_t st) {
   const int64_t threads = y.I1 * y.R * 32;
-  ymm1_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(y, A0, M1);
-  return cudaGetLastError();
+  return launch_k(ymm1_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, y, A0, M1);
 }
 
 cudaError_t launch_yr(const YRArgs &a, cudaStream_t st) {
   const int64_t threads = a.dims[a.mode] * a.R * 32;
-  yr_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(yr_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, a);
 }
 
 // ---------------------------------------------------------------- host-side launchers
 template <int R>
 static cudaError_t launch_solve_t(const SolveArgs &a, int grid, cudaStream_t st) {
-  solve_kernel_t<R><<<grid, 256, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(solve_kernel_t<R>, dim3(grid), dim3(256), 0, st, a);
 }
 
 cudaError_t launch_solve(const SolveArgs &a, int grid, cudaStream_t st) {
@@ -587,8 +594,7 @@ cudaError_t launch_solve(const SolveArgs &a, int grid, cudaStream_t st) {
 }
 
 cudaError_t launch_prep(const PrepArgs &a, cudaStream_t st) {
-  prep_kernel<<<a.blk_off[a.N], 256, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(prep_kernel, dim3(a.blk_off[a.N]), dim3(256), 0, st, a);
 }
 
 }  // namespace cpk

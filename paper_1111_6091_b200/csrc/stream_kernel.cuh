@@ -19,6 +19,9 @@
 //    (warp shuffles + shared memory), writing one R-vector partial per (CTA, segment).
 #pragma once
 #include "cp_internal.cuh"
+#ifdef CP_STREAM_TIMING
+#include <cstdio>
+#endif
 
 namespace cpk {
 
@@ -42,7 +45,7 @@ __device__ __forceinline__ StreamSmem carve(unsigned char *raw, const StreamPlan
   constexpr int WSTR = (R % 2 == 0) ? R + 2 : R + 1;
   StreamSmem s;
   s.zbuf = reinterpret_cast<double *>(raw);
-  s.abuf = s.zbuf + (size_t)p.nstages * p.cps * p.Wmax;
+  s.abuf = s.zbuf + (size_t)p.nstages * p.zst;
   s.wbuf = s.abuf + (size_t)p.nstages * p.cps * p.RS;
   s.red = s.wbuf + (size_t)p.nstages * p.cps * WSTR;
   s.sS = s.red + p.red_doubles;
@@ -108,6 +111,9 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
   }
   int64_t seg_left = p.Qn - (v0 % p.Qn);
   int seg_slot = 0;
+#ifdef CP_STREAM_TIMING
+  long long tm_wait = 0, tm_n = 0, tm0 = clock64();
+#endif
   int stage = 0;
   uint32_t eph = 1;
   int64_t v = v0;
@@ -121,8 +127,15 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
 #pragma unroll
     for (int j = 0; j < kMaxDigits; ++j)
       if (j < nd) q0 += (int64_t)B[j] * p.qsd[j];
+#ifdef CP_STREAM_TIMING
+    long long tw0 = clock64();
+#endif
     mbar_wait(&sm.empty[stage], eph);
-    double *zs = sm.zbuf + (size_t)stage * p.cps * p.Wmax;
+#ifdef CP_STREAM_TIMING
+    tm_wait += clock64() - tw0;
+    ++tm_n;
+#endif
+    double *zs = sm.zbuf + (size_t)stage * p.zst;
     double *as = sm.abuf + (size_t)stage * p.cps * p.RS;
     if (V >= 2) {
       if (lane == 0)
@@ -131,11 +144,12 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       __syncwarp();
       // Z columns: q advances by qsd[0] per column within a stage (digit 0 only).  Strided
       // columns are issued by all 32 lanes (one bulk copy per column).
-      if (p.RB == 1 && p.qsd[0] == 1) {
+      if (p.RB == 1 && p.qsd[0] == 1 && p.zcs == 0) {
         if (lane == 0) bulk_g2s(zs, p.Z + q0 * p.I1, (uint32_t)(ncols * Wb * 8), &sm.full[stage]);
       } else {
+        const int zstride = p.zcs ? p.zcs : Wb;
         for (int col = lane; col < ncols; col += 32)
-          bulk_g2s(zs + (size_t)col * Wb, p.Z + (q0 + col * p.qsd[0]) * p.I1 + row0,
+          bulk_g2s(zs + (size_t)col * zstride, p.Z + (q0 + col * p.qsd[0]) * p.I1 + row0,
                    (uint32_t)(Wb * 8), &sm.full[stage]);
       }
       if (has_f0 && lane == 31)
@@ -180,13 +194,18 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       eph ^= 1u;
     }
   }
+#ifdef CP_STREAM_TIMING
+  if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 101))
+    printf("[cta %d] producer: total %lld wait_empty %lld stages %lld\n", blockIdx.x, clock64() - tm0, tm_wait, tm_n);
+#endif
 }
 
 // ------------------------------------------------------------------------ weight warp (warp 9)
 // w_q[r] = A^(k0)(i_k0, r) * S[r],  S[r] = prod_{j >= 1, ord[j] != mode} A^(ord[j])(B_j, r).
-template <int R>
-__device__ void form_weights(const StreamPlan &p, int lane, const StreamSmem &sm) {
-  constexpr int WSTR = (R % 2 == 0) ? R + 2 : R + 1;
+static __device__ __noinline__ void form_weights(const StreamPlan &p, int lane, const StreamSmem &sm) {
+  const int R = p.R;
+  const int WSTR = (R % 2 == 0) ? R + 2 : R + 1;
+  if (p.direct_w) return;  // consumers read the staged factor rows themselves
   const int nd = p.nd;
   const bool has_f0 = (p.ord[0] != p.mode);
   int Bc[kMaxDigits];
@@ -194,8 +213,17 @@ __device__ void form_weights(const StreamPlan &p, int lane, const StreamSmem &sm
   for (int j = 0; j < kMaxDigits; ++j) Bc[j] = -1;
   int stage = 0;
   uint32_t fph = 0;
+#ifdef CP_STREAM_TIMING
+  long long tm_wait = 0, tm0 = clock64();
+#endif
   for (;;) {
+#ifdef CP_STREAM_TIMING
+    long long tw0 = clock64();
+#endif
     mbar_wait(&sm.full[stage], fph);
+#ifdef CP_STREAM_TIMING
+    tm_wait += clock64() - tw0;
+#endif
     const int *h = sm.hdr + stage * kHdrInts;
     const int ncols = h[0];
     const int flags = h[1];
@@ -218,13 +246,29 @@ __device__ void form_weights(const StreamPlan &p, int lane, const StreamSmem &sm
     }
     const double *as = sm.abuf + (size_t)stage * p.cps * p.RS;
     double *ws = sm.wbuf + (size_t)stage * p.cps * WSTR;
-    for (int e = lane; e < ncols * R; e += 32) {
-      const int col = e / R, r = e - (e / R) * R;
-      ws[col * WSTR + r] = (has_f0 ? as[col * p.RS + r] : 1.0) * sm.sS[r];
+    {
+      // lane -> (column, rank) pairs e = lane + 32 i without divisions in the loop
+      int col = lane / R, r = lane - (lane / R) * R;
+      const int dcol = 32 / R, dr = 32 - (32 / R) * R;
+      for (; col < ncols;) {
+        ws[col * WSTR + r] = (has_f0 ? as[col * p.RS + r] : 1.0) * sm.sS[r];
+        col += dcol;
+        r += dr;
+        if (r >= R) {
+          r -= R;
+          ++col;
+        }
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.wready[stage]);
-    if (flags & 2) break;
+    if (flags & 2) {
+#ifdef CP_STREAM_TIMING
+      if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 101))
+        printf("[cta %d] weights: total %lld wait_full %lld\n", blockIdx.x, clock64() - tm0, tm_wait);
+#endif
+      break;
+    }
     if (++stage == p.nstages) {
       stage = 0;
       fph ^= 1u;
@@ -257,13 +301,14 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
     fence_mbar_init();
   }
   __syncthreads();
+  griddep();  // (PDL) predecessor's At / factor writes visible from here on
 
   if (warp == kConsumerWarps) {
     produce<R, V>(p, lane, v0, v1, row0, Wb, sm);
     return;
   }
   if (warp == kConsumerWarps + 1) {
-    form_weights<R>(p, lane, sm);
+    form_weights(p, lane, sm);
     return;
   }
 
@@ -299,16 +344,26 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
 
   int stage = 0;
   uint32_t fph = 0;
+#ifdef CP_STREAM_TIMING
+  long long tm_wait = 0, tm_loop = 0, tm0 = clock64();
+#endif
   for (;;) {
+#ifdef CP_STREAM_TIMING
+    long long tw0 = clock64();
+#endif
     mbar_wait(&sm.wready[stage], fph);
+#ifdef CP_STREAM_TIMING
+    long long tw1 = clock64();
+    tm_wait += tw1 - tw0;
+#endif
     // (the weight warp observed full[stage] before arriving on wready: the TMA bytes are visible)
     const int *h = sm.hdr + stage * kHdrInts;
     const int ncols = h[0];
     const int flags = h[1];
     const int slot = h[2];
-    const double *zs = sm.zbuf + (size_t)stage * p.cps * p.Wmax;
+    const double *zs = sm.zbuf + (size_t)stage * p.zst;
     const double *wsb = sm.wbuf + (size_t)stage * p.cps * WSTR;
-    if (active) {
+    if (active && !(p.dbg & 1)) {
       for (int col = sl; col < ncols; col += cpt) {
         double z[V];
         load_rows<V>(zs + (size_t)col * Wb, u, Wb, z);
@@ -353,6 +408,9 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
       }
     }
     __syncwarp();
+#ifdef CP_STREAM_TIMING
+    tm_loop += clock64() - tw1;
+#endif
     if (lane == 0) mbar_arrive(&sm.empty[stage]);
     if (++stage == p.nstages) {
       stage = 0;
@@ -372,10 +430,14 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
                           : p.edge + ((int64_t)blockIdx.x * 2 + (slot == 0 ? 0 : 1)) * I1q * R) +
                     row0 + (int64_t)I1q * r0;
       if (cpt > 1) {
-        double *sred = sm.red + Wq * r0;  // Wb x R (red_doubles >= Wb * R for OP_YL)
-        for (int s2 = 1; s2 < cpt; ++s2) {
+        // slots 1..cpt-1 added to slot 0 in slot order, G slots per round (G regions of
+        // Wb x R doubles in the reduction area)
+        const int reg = Wq * R;
+        const int G = p.red_doubles / reg;
+        for (int s1 = 1; s1 < cpt; s1 += G) {
           named_bar_sync(1, kConsumers);
-          if (active && sl == s2) {
+          if (active && sl >= s1 && sl < s1 + G) {
+            double *sred = sm.red + (sl - s1) * reg + Wq * r0;
 #pragma unroll
             for (int v = 0; v < V; ++v)
 #pragma unroll
@@ -384,11 +446,15 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
           }
           named_bar_sync(1, kConsumers);
           if (sl == 0) {
+            const int n = (cpt - s1 < G) ? cpt - s1 : G;
+            for (int k = 0; k < n; ++k) {
+              const double *sred = sm.red + k * reg + Wq * r0;
 #pragma unroll
-            for (int v = 0; v < V; ++v)
+              for (int v = 0; v < V; ++v)
 #pragma unroll
-              for (int r = 0; r < RT; ++r)
-                if (r0 + r < R) acc[v][r] += sred[row_of<V>(uq, v, Wq) + Wq * r];
+                for (int r = 0; r < RT; ++r)
+                  if (r0 + r < R) acc[v][r] += sred[row_of<V>(uq, v, Wq) + Wq * r];
+            }
           }
         }
       }
@@ -425,8 +491,8 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
       for (int v = 0; v < V; ++v)
 #pragma unroll
         for (int r = 0; r < RT; ++r) acc[v][r] = 0.0;
-      if (U % 32 == 0) {
-        // every lane of a warp shares (g, sl): warp shuffles, then one row per warp
+      if (RG == 1 || U % 32 == 0) {
+        // every lane of a warp shares the rank group g: warp shuffles, then one row per warp
 #pragma unroll
         for (int r = 0; r < RT; ++r) {
 #pragma unroll
@@ -461,30 +527,42 @@ __global__ void __launch_bounds__(kStreamThreads, (V * StreamTile<R, OP>::RT <= 
     }
     if (flags & 2) break;
   }
+#ifdef CP_STREAM_TIMING
+  if ((tid == 0 || tid == 224) && (blockIdx.x == 0 || blockIdx.x == 101))
+    printf("[cta %d tid %d] consumer: total %lld wait_wready %lld loop %lld\n", blockIdx.x, tid, clock64() - tm0, tm_wait, tm_loop);
+#endif
 
   if (OP == OP_MTTKRP && p.mode == 0) {
     // ---- mode 0: write this CTA's I1 x R partial for its row block (slots summed in order) ----
     double *out = p.part + (int64_t)c * p.I1 * R;
     if (cpt > 1) {
-      named_bar_sync(1, kConsumers);  // every consumer is past the ring: reuse it
-      double *sred = sm.zbuf;         // Wb x R
-      for (int s2 = 1; s2 < cpt; ++s2) {
-        if (active && sl == s2) {
+      // every consumer is past the ring: reuse it for the slot reduction (slot order, G slots
+      // per round)
+      const int reg = Wb * R;
+      int G = (int)(((int64_t)p.nstages * p.cps * p.Wmax) / reg);
+      if (G < 1) G = 1;
+      for (int s1 = 1; s1 < cpt; s1 += G) {
+        named_bar_sync(1, kConsumers);
+        if (active && sl >= s1 && sl < s1 + G) {
+          double *sred = sm.zbuf + (sl - s1) * reg + Wb * r0;
 #pragma unroll
           for (int v = 0; v < V; ++v)
 #pragma unroll
             for (int r = 0; r < RT; ++r)
-              if (r0 + r < R) sred[row_of<V>(u, v, Wb) + Wb * (r0 + r)] = acc[v][r];
+              if (r0 + r < R) sred[row_of<V>(u, v, Wb) + Wb * r] = acc[v][r];
         }
         named_bar_sync(1, kConsumers);
         if (sl == 0) {
+          const int n = (cpt - s1 < G) ? cpt - s1 : G;
+          for (int k = 0; k < n; ++k) {
+            const double *sred = sm.zbuf + k * reg + Wb * r0;
 #pragma unroll
-          for (int v = 0; v < V; ++v)
+            for (int v = 0; v < V; ++v)
 #pragma unroll
-            for (int r = 0; r < RT; ++r)
-              if (r0 + r < R) acc[v][r] += sred[row_of<V>(u, v, Wb) + Wb * (r0 + r)];
+              for (int r = 0; r < RT; ++r)
+                if (r0 + r < R) acc[v][r] += sred[row_of<V>(u, v, Wb) + Wb * r];
+          }
         }
-        named_bar_sync(1, kConsumers);
       }
     }
     if (sl == 0) {
@@ -519,8 +597,7 @@ cudaError_t launch_stream_t(const StreamPlan &p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  kern<<<p.Gc * p.RB, kStreamThreads, p.smem_bytes, st>>>(p);
-  return cudaGetLastError();
+  return launch_k(kern, dim3(p.Gc * p.RB), dim3(kStreamThreads), (size_t)p.smem_bytes, st, p);
 }
 
 }  // namespace cpk

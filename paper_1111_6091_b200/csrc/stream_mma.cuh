@@ -1,0 +1,312 @@
+// stream_mma.cuh -- the Z-streaming MTTKRP / Y_L pass with FP64 tensor-core consumers.
+//
+// Same pipeline as stream_kernel.cuh (TMA producer warp, weight warp, mbarrier rings, v-order
+// odometer, stage boundaries), but the consumers treat each stage as a dense contraction
+//     C(rows, ranks) += Z_stage(rows, cols) * W(cols, ranks)
+// -- Z(:, i_1, :) A^(2) for the Y_L pass, Z(:, :, j) A^(1) for the mode-2 pass (eq:gradEqn,
+// eq:Phi): one mma.sync.m8n8k4.f64 (SASS DMMA) does 8 rows x 8 ranks x 4 columns
+// per warp instruction, with the accumulators in registers for the whole pass.
+//  * warps: KS k-groups of 8/KS warps; k-group kg takes the k-steps (4 columns) kk = kg mod KS
+//    of every stage; warp wi of a group owns m-tiles wi*MT .. wi*MT+MT-1 (8 rows each) and all
+//    NT n-tiles (8 ranks each; ranks >= R are masked to zero).
+//  * shared memory: Z columns at a padded stride zcs = 8 (mod 16) doubles -> the A-fragment
+//    reads (8 rows x 4 columns) take the minimal two 128-B wavefronts; the producer issues one
+//    bulk copy per column.  B fragments come from the staged factor rows (direct_w: the
+//    Khatri-Rao rows are the factor rows) or from the weight warp's rows.
+//  * ragged stages (fewer than 4 columns in a k-step): A and B masked to zero in registers.
+//  * epilogues: Y_L pass -- the k-groups' C blocks are summed in group order in shared memory
+//    and written as the I0 x R block of the segment (yl, or the CTA's edge block); MTTKRP
+//    mode >= 1 -- C contracted with the A^(1) rows, reduced over lanes and warps in a fixed
+//    order into one R-vector per (CTA, segment); mode 0 -- the CTA's I1 x R partial.
+#pragma once
+#include "stream_kernel.cuh"
+
+namespace cpk {
+
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// k-groups 1..KS-1 add their C blocks into group 0's registers (group order); red holds
+// (KS-1) regions of Wb x (8 NT) doubles.  All consumers call it.
+template <int NT, int MT>
+__device__ __forceinline__ void mma_ksum(double (&acc)[MT][NT][2], double *red, int KS, int kg, int wi, int Wb,
+                                         int gq, int tq) {
+  if (KS == 1) return;
+  const int RP = 8 * NT;
+  named_bar_sync(1, kConsumers);
+  if (kg > 0) {
+    double *dst = red + (size_t)(kg - 1) * Wb * RP;
+#pragma unroll
+    for (int j = 0; j < MT; ++j) {
+      const int m = (wi * MT + j) * 8 + gq;
+      if (m < Wb) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          dst[(size_t)(n * 8 + 2 * tq) * Wb + m] = acc[j][n][0];
+          dst[(size_t)(n * 8 + 2 * tq + 1) * Wb + m] = acc[j][n][1];
+        }
+      }
+    }
+  }
+  named_bar_sync(1, kConsumers);
+  if (kg == 0) {
+    for (int g = 1; g < KS; ++g) {
+      const double *src = red + (size_t)(g - 1) * Wb * RP;
+#pragma unroll
+      for (int j = 0; j < MT; ++j) {
+        const int m = (wi * MT + j) * 8 + gq;
+        if (m < Wb) {
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            acc[j][n][0] += src[(size_t)(n * 8 + 2 * tq) * Wb + m];
+            acc[j][n][1] += src[(size_t)(n * 8 + 2 * tq + 1) * Wb + m];
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int NT, int MT, int OP>
+__global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __grid_constant__ StreamPlan p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  StreamSmem sm;
+  {
+    // carve (as carve<R, OP> in stream_kernel.cuh, with the runtime weight stride)
+    const int R = p.R;
+    const int WSTR = (R % 2 == 0) ? R + 2 : R + 1;
+    sm.zbuf = reinterpret_cast<double *>(smem_raw);
+    sm.abuf = sm.zbuf + (size_t)p.nstages * p.zst;
+    sm.wbuf = sm.abuf + (size_t)p.nstages * p.cps * p.RS;
+    sm.red = sm.wbuf + (size_t)p.nstages * p.cps * WSTR;
+    sm.sS = sm.red + p.red_doubles;
+    sm.full = reinterpret_cast<uint64_t *>(sm.sS + 32);
+    sm.wready = sm.full + p.nstages;
+    sm.empty = sm.wready + p.nstages;
+    sm.hdr = reinterpret_cast<int *>(sm.empty + p.nstages);
+  }
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int rb = blockIdx.x % p.RB;
+  const int c = blockIdx.x / p.RB;
+  const int64_t v0 = (int64_t)c * p.Q / p.Gc;
+  const int64_t v1 = (int64_t)(c + 1) * p.Q / p.Gc;
+  const int64_t row0 = (int64_t)rb * p.Wmax;
+  const int Wb = (int)((p.I1 - row0) < p.Wmax ? (p.I1 - row0) : p.Wmax);
+
+  if (tid == 0) {
+    for (int s = 0; s < p.nstages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.wready[s], 1);
+      mbar_init(&sm.empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  griddep();  // (PDL) predecessor's At / factor writes visible from here on
+
+  if (warp == kConsumerWarps) {
+    produce<8, 2>(p, lane, v0, v1, row0, Wb, sm);  // (template args only select the TMA path)
+    return;
+  }
+  if (warp == kConsumerWarps + 1) {
+    form_weights(p, lane, sm);  // (returns at once when direct_w)
+    return;
+  }
+
+  // ============================ consumer warps (tensor cores) ============================
+  const int R = p.R;
+  const int KS = p.ks;
+  const int wpg = kConsumerWarps / KS;  // warps per k-group
+  const int kg = warp / wpg, wi = warp - (warp / wpg) * wpg;
+  const int gq = lane >> 2, tq = lane & 3;  // fragment coordinates
+  const int zcs = p.zcs;
+  const int wstride = p.direct_w ? p.RS : ((R % 2 == 0) ? R + 2 : R + 1);
+  const int arow0 = wi * MT * 8 + gq;  // first A row of this lane (m-tile j adds 8 j)
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int j = 0; j < MT; ++j)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
+
+  // B-fragment rank mask (ranks >= R are zero)
+  bool nok[NT];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) nok[n] = (n * 8 + gq) < R;
+
+  int stage = 0;
+  uint32_t fph = 0;
+  for (;;) {
+    mbar_wait(p.direct_w ? &sm.full[stage] : &sm.wready[stage], fph);
+    const int *h = sm.hdr + stage * kHdrInts;
+    const int ncols = h[0];
+    const int flags = h[1];
+    const int slot = h[2];
+    const double *zs = sm.zbuf + (size_t)stage * p.zst + arow0;
+    const double *ws = (p.direct_w ? sm.abuf + (size_t)stage * p.cps * p.RS
+                                   : sm.wbuf + (size_t)stage * p.cps * wstride) + gq;
+    // full k-steps (4 landed columns): only the rank mask applies
+    int k0 = 4 * kg;
+    for (; k0 + 4 <= ncols; k0 += 4 * KS) {
+      const int col = k0 + tq;
+      const double *za = zs + col * zcs;
+      const double *wb = ws + col * wstride;
+      double a[MT], b[NT];
+#pragma unroll
+      for (int j = 0; j < MT; ++j) a[j] = za[8 * j];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) b[n] = wb[8 * n];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) b[n] = nok[n] ? b[n] : 0.0;
+#pragma unroll
+      for (int j = 0; j < MT; ++j)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) dmma_8x8x4(acc[j][n][0], acc[j][n][1], a[j], b[n]);
+    }
+    if (k0 < ncols) {
+      // ragged last k-step: columns >= ncols read column 0 of the stage (always landed) and
+      // are zeroed in registers (branch-free)
+      const int col = k0 + tq;
+      const bool ok = col < ncols;
+      const int colc = ok ? col : 0;
+      const double *za = zs + colc * zcs;
+      const double *wb = ws + colc * wstride;
+      double a[MT], b[NT];
+#pragma unroll
+      for (int j = 0; j < MT; ++j) a[j] = za[8 * j];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) b[n] = wb[8 * n];
+#pragma unroll
+      for (int j = 0; j < MT; ++j) a[j] = ok ? a[j] : 0.0;
+#pragma unroll
+      for (int n = 0; n < NT; ++n) b[n] = (ok && nok[n]) ? b[n] : 0.0;
+#pragma unroll
+      for (int j = 0; j < MT; ++j)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) dmma_8x8x4(acc[j][n][0], acc[j][n][1], a[j], b[n]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    if (++stage == p.nstages) {
+      stage = 0;
+      fph ^= 1u;
+    }
+
+    if (OP == OP_YL && (flags & 1)) {
+      // ---- end of an i_1 segment: the CTA's I0-block x R block of Y_L(:, i_1, :) ----
+      const int Wq = opaque(Wb);
+      const int64_t I1q = opaque(p.I1);
+      mma_ksum<NT, MT>(acc, sm.red, KS, kg, wi, Wq, gq, tq);
+      if (kg == 0) {
+        const int64_t s_abs = v0 / p.Qn + slot;
+        const bool full = (s_abs * p.Qn >= v0) && ((s_abs + 1) * p.Qn <= v1);
+        double *dst = (full ? p.yl + s_abs * I1q * R
+                            : p.edge + ((int64_t)blockIdx.x * 2 + (slot == 0 ? 0 : 1)) * I1q * R) +
+                      row0;
+#pragma unroll
+        for (int j = 0; j < MT; ++j) {
+          const int m = arow0 + 8 * j;
+          if (m < Wq) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+              const int r = n * 8 + 2 * tq;
+              if (r < R) dst[m + I1q * r] = acc[j][n][0];
+              if (r + 1 < R) dst[m + I1q * (r + 1)] = acc[j][n][1];
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < MT; ++j)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
+    }
+    if (OP == OP_MTTKRP && p.mode != 0 && (flags & 1)) {
+      // ---- end of an i_m segment: contract with the A^(1) rows, reduce lanes and warps ----
+      const int Wq = opaque(Wb);
+      double pr[NT][2];
+#pragma unroll
+      for (int n = 0; n < NT; ++n) pr[n][0] = pr[n][1] = 0.0;
+      const double *a1b = p.At[0] + row0 * p.RS;
+#pragma unroll
+      for (int j = 0; j < MT; ++j) {
+        const int m = arow0 + 8 * j;
+        if (m < Wq) {
+          const double *a1 = a1b + (int64_t)m * p.RS;
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const int r = n * 8 + 2 * tq;
+            if (r < R) pr[n][0] = fma(__ldg(a1 + r), acc[j][n][0], pr[n][0]);
+            if (r + 1 < R) pr[n][1] = fma(__ldg(a1 + r + 1), acc[j][n][1], pr[n][1]);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < MT; ++j)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
+      // lanes sharing tq hold the same ranks: fixed xor tree over gq
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+          for (int off = 4; off < 32; off <<= 1) pr[n][hh] += __shfl_xor_sync(0xffffffffu, pr[n][hh], off);
+      if (gq == 0) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          sm.red[warp * 8 * NT + n * 8 + 2 * tq] = pr[n][0];
+          sm.red[warp * 8 * NT + n * 8 + 2 * tq + 1] = pr[n][1];
+        }
+      }
+      named_bar_sync(1, kConsumers);
+      if (tid < R) {
+        double sum = 0.0;
+        for (int w8 = 0; w8 < kConsumerWarps; ++w8) sum += sm.red[w8 * 8 * NT + tid];
+        p.part[((int64_t)blockIdx.x * p.slots + slot) * R + tid] = sum;
+      }
+      named_bar_sync(1, kConsumers);
+    }
+    if (flags & 2) break;
+  }
+
+  if (OP == OP_MTTKRP && p.mode == 0) {
+    // ---- mode 0: this CTA's I1 x R partial for its row block (k-groups summed in order
+    // through the Z ring, which every consumer is done with) ----
+    mma_ksum<NT, MT>(acc, sm.zbuf, KS, kg, wi, Wb, gq, tq);
+    if (kg == 0) {
+      double *out = p.part + (int64_t)c * p.I1 * R + row0;
+#pragma unroll
+      for (int j = 0; j < MT; ++j) {
+        const int m = arow0 + 8 * j;
+        if (m < Wb) {
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            const int r = n * 8 + 2 * tq;
+            if (r < R) out[m + p.I1 * r] = acc[j][n][0];
+            if (r + 1 < R) out[m + p.I1 * (r + 1)] = acc[j][n][1];
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int NT, int MT, int OP>
+cudaError_t launch_stream_mma_t(const StreamPlan &p, cudaStream_t st) {
+  auto kern = stream_mma_kernel<NT, MT, OP>;
+  static bool attr_done = false;  // per instantiation
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  return launch_k(kern, dim3(p.Gc * p.RB), dim3(kStreamThreads), (size_t)p.smem_bytes, st, p);
+}
+
+}  // namespace cpk
