@@ -270,8 +270,8 @@ def main():
         tr = json.load(open(TRAFFIC_PATH)).get(args.workload)
         if tr:
             traffic = tr.get("dram_bytes_per_launch")
-    roofline = {"kernel": "stream_kernel (the two Z passes of the dimension-tree sweep: Y_L pass + "
-                          "mode-2 MTTKRP pass)", "bound": "hbm",
+    roofline = {"kernel": "stream_mma_kernel (the two Z passes of the dimension-tree sweep, FP64 "
+                          "tensor-core consumers: Y_L pass + mode-2 MTTKRP pass)", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_source": peak_src, "alg_bytes_per_launch": bytes_per_launch,

@@ -245,16 +245,41 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   }
   if (cps > p.Q) cps = (int)p.Q;
   p.cps = cps;
-  const int stage_doubles = p.zst + cps * p.RS + cps * WSTR;
-  int nst = env_int("CP_RING_BYTES", 96 * 1024) / (stage_doubles * 8);
-  if (nst < 2) nst = 2;
-  if (nst > 8) nst = 8;
-  // mode-0 slot / k-group reduction reuses the Z ring: it must hold the reduced blocks
-  const int64_t need = p.mma ? (int64_t)(p.ks - 1) * p.Wmax * 8 * p.nt : (int64_t)p.Wmax * s.R;
-  while ((int64_t)nst * p.zst < need) ++nst;
+  p.zst = cps * (p.mma ? p.zcs : p.Wmax);
+  if (p.mma) {
+    // staged factor rows keep the At stride (one bulk copy per stage) and the weight rows the
+    // DFMA kernel's stride.  Padding either to 8 (mod 16) doubles removes the B-fragment bank
+    // conflicts but measured slower (per-row copies; smaller stages): CP_MMA_PAD_A/_W
+    int st = p.RS;
+    while (st % 16 != 8) ++st;
+    p.ars = env_int("CP_MMA_PAD_A", 0) ? st : p.RS;
+    p.wstr = env_int("CP_MMA_PAD_W", 0) ? st : WSTR;
+  } else {
+    p.ars = p.RS;
+    p.wstr = WSTR;
+  }
+  // ring: CP_RING_BYTES (default 96 KB) of stages, at least 2; the MMA kernels also keep the whole
+  // CTA within the 2-CTAs/SM shared-memory budget (113 KB) by shrinking the stage if needed
+  const int cap = env_int("CP_SMEM_CAP", 113 * 1024);
+  const int unit = p.mma ? 4 * p.ks : 1;
+  int stage_doubles = 0, nst = 2;
+  for (;;) {
+    stage_doubles = p.zst + cps * p.ars + cps * p.wstr;
+    nst = env_int("CP_RING_BYTES", 96 * 1024) / (stage_doubles * 8);
+    if (nst < 2) nst = 2;
+    if (nst > 8) nst = 8;
+    // mode-0 slot / k-group reduction reuses the Z ring: it must hold the reduced blocks
+    const int64_t need = p.mma ? (int64_t)(p.ks - 1) * p.Wmax * 8 * p.nt : (int64_t)p.Wmax * s.R;
+    while ((int64_t)nst * p.zst < need) ++nst;
+    const int bytes = (nst * stage_doubles + p.red_doubles + 32) * 8 + nst * 88 + 64;
+    if (!p.mma || bytes <= cap || cps <= unit) break;
+    cps -= unit;
+    p.cps = cps;
+    p.zst = cps * p.zcs;
+  }
   p.nstages = nst;
   p.dbg = env_int("CP_STREAM_DBG", 0);
-  p.smem_bytes = (nst * stage_doubles + p.red_doubles + 32) * 8 + nst * 24 + nst * 64 + 64;
+  p.smem_bytes = (nst * stage_doubles + p.red_doubles + 32) * 8 + nst * 88 + 64;
   if (p.smem_bytes > 200 * 1024) return false;
   const int occ = p.mma ? stream_mma_occupancy(p.nt, p.mt, op, p.smem_bytes)
                         : stream_occupancy(s.R, p.V, op, p.smem_bytes);

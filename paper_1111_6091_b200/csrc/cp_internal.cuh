@@ -60,6 +60,7 @@ struct StreamPlan {
   int zcs;          // shared-memory column stride of a Z stage (doubles); 0: the block width Wb
   int zst;          // doubles per Z stage in shared memory
   int direct_w;     // Khatri-Rao rows are the staged factor rows (no weight warp)
+  int ars, wstr;    // shared-memory row strides of the staged factor rows / the weight rows
   int dbg;          // experiments only (env CP_STREAM_DBG): 1 = consumers skip the FMAs, 2 = weight warp skips forming
 };
 

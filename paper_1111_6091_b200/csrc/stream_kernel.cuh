@@ -46,8 +46,9 @@ __device__ __forceinline__ StreamSmem carve(unsigned char *raw, const StreamPlan
   StreamSmem s;
   s.zbuf = reinterpret_cast<double *>(raw);
   s.abuf = s.zbuf + (size_t)p.nstages * p.zst;
-  s.wbuf = s.abuf + (size_t)p.nstages * p.cps * p.RS;
-  s.red = s.wbuf + (size_t)p.nstages * p.cps * WSTR;
+  s.wbuf = s.abuf + (size_t)p.nstages * p.cps * p.ars;
+  s.red = s.wbuf + (size_t)p.nstages * p.cps * p.wstr;
+  (void)WSTR;
   s.sS = s.red + p.red_doubles;
   s.full = reinterpret_cast<uint64_t *>(s.sS + 32);
   s.wready = s.full + p.nstages;
@@ -136,7 +137,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
     ++tm_n;
 #endif
     double *zs = sm.zbuf + (size_t)stage * p.zst;
-    double *as = sm.abuf + (size_t)stage * p.cps * p.RS;
+    double *as = sm.abuf + (size_t)stage * p.cps * p.ars;
     if (V >= 2) {
       if (lane == 0)
         mbar_expect_tx(&sm.full[stage],
@@ -152,8 +153,16 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
           bulk_g2s(zs + (size_t)col * zstride, p.Z + (q0 + col * p.qsd[0]) * p.I1 + row0,
                    (uint32_t)(Wb * 8), &sm.full[stage]);
       }
-      if (has_f0 && lane == 31)
-        bulk_g2s(as, A0 + (int64_t)B[0] * p.RS, (uint32_t)(ncols * p.RS * 8), &sm.full[stage]);
+      if (has_f0) {
+        if (p.ars == p.RS) {
+          if (lane == 31)
+            bulk_g2s(as, A0 + (int64_t)B[0] * p.RS, (uint32_t)(ncols * p.RS * 8), &sm.full[stage]);
+        } else {  // padded rows (conflict-free B fragments): one copy per factor row
+          for (int col = lane; col < ncols; col += 32)
+            bulk_g2s(as + (size_t)col * p.ars, A0 + ((int64_t)B[0] + col) * p.RS, (uint32_t)(p.RS * 8),
+                     &sm.full[stage]);
+        }
+      }
       __syncwarp();
     } else {
       // scalar fallback (odd I1: columns are not 16-B aligned): the warp copies elements
@@ -204,7 +213,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
 // w_q[r] = A^(k0)(i_k0, r) * S[r],  S[r] = prod_{j >= 1, ord[j] != mode} A^(ord[j])(B_j, r).
 static __device__ __noinline__ void form_weights(const StreamPlan &p, int lane, const StreamSmem &sm) {
   const int R = p.R;
-  const int WSTR = (R % 2 == 0) ? R + 2 : R + 1;
+  const int WSTR = p.wstr;
   if (p.direct_w) return;  // consumers read the staged factor rows themselves
   const int nd = p.nd;
   const bool has_f0 = (p.ord[0] != p.mode);
@@ -244,14 +253,14 @@ static __device__ __noinline__ void form_weights(const StreamPlan &p, int lane, 
       if (lane < R) sm.sS[lane] = s;
       __syncwarp();
     }
-    const double *as = sm.abuf + (size_t)stage * p.cps * p.RS;
+    const double *as = sm.abuf + (size_t)stage * p.cps * p.ars;
     double *ws = sm.wbuf + (size_t)stage * p.cps * WSTR;
     {
       // lane -> (column, rank) pairs e = lane + 32 i without divisions in the loop
       int col = lane / R, r = lane - (lane / R) * R;
       const int dcol = 32 / R, dr = 32 - (32 / R) * R;
       for (; col < ncols;) {
-        ws[col * WSTR + r] = (has_f0 ? as[col * p.RS + r] : 1.0) * sm.sS[r];
+        ws[col * WSTR + r] = (has_f0 ? as[col * p.ars + r] : 1.0) * sm.sS[r];
         col += dcol;
         r += dr;
         if (r >= R) {

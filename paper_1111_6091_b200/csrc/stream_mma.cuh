@@ -75,13 +75,11 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StreamSmem sm;
   {
-    // carve (as carve<R, OP> in stream_kernel.cuh, with the runtime weight stride)
-    const int R = p.R;
-    const int WSTR = (R % 2 == 0) ? R + 2 : R + 1;
+    // carve (as carve<R, OP> in stream_kernel.cuh)
     sm.zbuf = reinterpret_cast<double *>(smem_raw);
     sm.abuf = sm.zbuf + (size_t)p.nstages * p.zst;
-    sm.wbuf = sm.abuf + (size_t)p.nstages * p.cps * p.RS;
-    sm.red = sm.wbuf + (size_t)p.nstages * p.cps * WSTR;
+    sm.wbuf = sm.abuf + (size_t)p.nstages * p.cps * p.ars;
+    sm.red = sm.wbuf + (size_t)p.nstages * p.cps * p.wstr;
     sm.sS = sm.red + p.red_doubles;
     sm.full = reinterpret_cast<uint64_t *>(sm.sS + 32);
     sm.wready = sm.full + p.nstages;
@@ -125,7 +123,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   const int kg = warp / wpg, wi = warp - (warp / wpg) * wpg;
   const int gq = lane >> 2, tq = lane & 3;  // fragment coordinates
   const int zcs = p.zcs;
-  const int wstride = p.direct_w ? p.RS : ((R % 2 == 0) ? R + 2 : R + 1);
+  const int wstride = p.direct_w ? p.ars : p.wstr;
   const int arow0 = wi * MT * 8 + gq;  // first A row of this lane (m-tile j adds 8 j)
 
   double acc[MT][NT][2];
@@ -148,8 +146,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     const int flags = h[1];
     const int slot = h[2];
     const double *zs = sm.zbuf + (size_t)stage * p.zst + arow0;
-    const double *ws = (p.direct_w ? sm.abuf + (size_t)stage * p.cps * p.RS
-                                   : sm.wbuf + (size_t)stage * p.cps * wstride) + gq;
+    const double *ws = (p.direct_w ? sm.abuf : sm.wbuf) + (size_t)stage * p.cps * wstride + gq;
     // full k-steps (4 landed columns): only the rank mask applies
     int k0 = 4 * kg;
     for (; k0 + 4 <= ncols; k0 += 4 * KS) {

@@ -56,7 +56,7 @@ def main():
                 else:
                     vals.append("-")
             lines.append(f"| {label or os.path.basename(rep)} | {name} | " + " | ".join(vals) + " |")
-            if "stream_kernel" in name and label:
+            if "stream_" in name and label:
                 def val(key):
                     i = hdr.index(key)
                     v = float(r[i].replace(",", ""))
