@@ -38,6 +38,15 @@ RAGGED = [
     ((96, 5, 6, 7), 10),
     ((2, 2, 2, 2, 2, 2, 2, 2), 3),  # N = CP_MAX_N
 ]
+# shapes that exercise the tensor-core consumer geometry (stream_mma.cuh): NT = 3, 4 n-tiles with
+# masked ranks, ragged m-tiles, two row blocks with a ragged last block, k-split groups
+MMA_SHAPES = [
+    ((130, 9, 6), 20),       # NT = 3, 17 m-tiles over 8 warps x MT 3
+    ((258, 7, 5), 25),       # NT = 4, two row blocks (136 + 122 rows)
+    ((40, 36, 30), 20),      # k-split: KS = 4 groups of 2 warps
+    ((96, 10, 12), 24),      # NT = 3, KS = 2
+]
+RAGGED = RAGGED + MMA_SHAPES
 
 _cfg_cache = {}
 
@@ -154,6 +163,14 @@ def _well_posed(dims, R):
 @pytest.mark.parametrize("dims,R", [r for r in RAGGED if r[1] <= 16 and len(r[0]) <= 5 and _well_posed(*r)])
 def test_sweep_single_step_ragged(dims, R):
     Z, A = cpsynth.random_problem(dims, R, seed=100 + R)
+    nz2 = float(np.vdot(Z, Z))
+    for _, Ag, og, Ao, oo in _sweep_pair(Z, dims, A, nsweeps=2, nz2=nz2):
+        _check_sweep(Ag, og, Ao, oo, nz2)
+
+
+@pytest.mark.parametrize("dims,R", [r for r in MMA_SHAPES if _well_posed(*r)])
+def test_sweep_single_step_mma_shapes(dims, R):
+    Z, A = cpsynth.random_problem(dims, R, seed=300 + R)
     nz2 = float(np.vdot(Z, Z))
     for _, Ag, og, Ao, oo in _sweep_pair(Z, dims, A, nsweeps=2, nz2=nz2):
         _check_sweep(Ag, og, Ao, oo, nz2)
