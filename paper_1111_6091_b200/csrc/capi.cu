@@ -109,8 +109,11 @@ static bool plan_digits(StreamPlan &p, const cp_shape &s) {
 }
 
 // FP64 tensor-core consumer geometry (stream_mma.cuh): row block, k-split and m-tiles per warp
+static bool plan_mma_ok(const StreamPlan &p, const cp_shape &s, int op) {
+  return !(env_int("CP_STREAM_MMA", 1) == 0 || op == OP_RESID || s.R > 32 || (p.I1 & 1));
+}
 static bool plan_mma(StreamPlan &p, const cp_shape &s, int op) {
-  if (env_int("CP_STREAM_MMA", 1) == 0 || op == OP_RESID || s.R > 32 || (p.I1 & 1)) return false;
+  if (!plan_mma_ok(p, s, op)) return false;
   p.nt = (s.R + 7) / 8;
   int mt_max = (p.nt <= 2) ? 8 : 4;
   const int mt_env = env_int("CP_MMA_MTMAX", 4);  // measured: MT = 8 (64 accumulators) serializes the A loads
@@ -169,7 +172,8 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   const int RT = stream_rt(s.R, op), RG = stream_rg(s.R, op);
   const int WSTR = (s.R % 2 == 0) ? s.R + 2 : s.R + 1;
   p.RS = s.R + (s.R & 1);
-  const int stage_target = env_int("CP_STAGE_BYTES", 40960);
+  // stage size: tools/sweep*.sh (DFMA consumers), tools/plan_sweep.py (MMA: 2 stages of ~52 KB)
+  const int stage_target = env_int("CP_STAGE_BYTES", (op != OP_RESID && plan_mma_ok(p, s, op)) ? 53248 : 40960);
   int cps, cpt = 1;
   if (plan_mma(p, s, op)) {
     // stage: a multiple of 4 KS columns (k-steps of every k-group)
@@ -179,8 +183,15 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     if (cps < unit) cps = unit;
     if (cps > 64) cps = 64;
     p.zst = cps * p.zcs;
+    // B fragments straight from the staged factor rows, times the slow digits' rows (also
+    // staged): no weight warp whenever digit 0 is a factor mode
     const bool has_f0 = (p.ord[0] != p.mode);
-    p.direct_w = (has_f0 && (p.nd == 1 || (p.nd == 2 && p.ord[1] == p.mode))) ? 1 : 0;
+    bool slow = false;
+    for (int j = 1; j < p.nd; ++j)
+      if (p.ord[j] != p.mode) slow = true;
+    p.direct_w = has_f0 ? 1 : 0;
+    p.srows = (has_f0 && slow && env_int("CP_MMA_SROWS", 1)) ? 1 : 0;
+    if (has_f0 && slow && !p.srows) p.direct_w = 0;
     const int RP = 8 * p.nt;
     if (op == OP_YL) p.red_doubles = (p.ks - 1) * p.Wmax * RP + 8;
     else if (p.mode != 0) p.red_doubles = kConsumerWarps * RP + 8;
@@ -254,6 +265,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     while (st % 16 != 8) ++st;
     p.ars = env_int("CP_MMA_PAD_A", 0) ? st : p.RS;
     p.wstr = env_int("CP_MMA_PAD_W", 0) ? st : WSTR;
+    if (p.direct_w && env_int("CP_MMA_WSTR0", 1)) p.wstr = 0;  // no weight rows
   } else {
     p.ars = p.RS;
     p.wstr = WSTR;
@@ -264,7 +276,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   const int unit = p.mma ? 4 * p.ks : 1;
   int stage_doubles = 0, nst = 2;
   for (;;) {
-    stage_doubles = p.zst + cps * p.ars + cps * p.wstr;
+    stage_doubles = p.zst + cps * p.ars + cps * p.wstr + (p.srows ? kMaxDigits * p.RS : 0);
     nst = env_int("CP_RING_BYTES", 96 * 1024) / (stage_doubles * 8);
     if (nst < 2) nst = 2;
     if (nst > 8) nst = 8;

@@ -61,6 +61,7 @@ struct StreamPlan {
   int zst;          // doubles per Z stage in shared memory
   int direct_w;     // Khatri-Rao rows are the staged factor rows (no weight warp)
   int ars, wstr;    // shared-memory row strides of the staged factor rows / the weight rows
+  int srows;        // the producer also stages the slow digits' factor rows (kMaxDigits per stage)
   int dbg;          // experiments only (env CP_STREAM_DBG): 1 = consumers skip the FMAs, 2 = weight warp skips forming
 };
 

@@ -35,7 +35,7 @@ constexpr int kHdrInts = 16;  // per-stage header: ncols, flags, slot, -, digits
 
 // Shared-memory carve-up of one CTA (all offsets in doubles except the tail).
 struct StreamSmem {
-  double *zbuf, *abuf, *wbuf, *red, *sS;
+  double *zbuf, *abuf, *wbuf, *sbuf, *red, *sS;
   uint64_t *full, *wready, *empty;
   int *hdr;
 };
@@ -47,7 +47,8 @@ __device__ __forceinline__ StreamSmem carve(unsigned char *raw, const StreamPlan
   s.zbuf = reinterpret_cast<double *>(raw);
   s.abuf = s.zbuf + (size_t)p.nstages * p.zst;
   s.wbuf = s.abuf + (size_t)p.nstages * p.cps * p.ars;
-  s.red = s.wbuf + (size_t)p.nstages * p.cps * p.wstr;
+  s.sbuf = s.wbuf + (size_t)p.nstages * p.cps * p.wstr;
+  s.red = s.sbuf + (p.srows ? (size_t)p.nstages * kMaxDigits * p.RS : 0);
   (void)WSTR;
   s.sS = s.red + p.red_doubles;
   s.full = reinterpret_cast<uint64_t *>(s.sS + 32);
@@ -139,10 +140,24 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
     double *zs = sm.zbuf + (size_t)stage * p.zst;
     double *as = sm.abuf + (size_t)stage * p.cps * p.ars;
     if (V >= 2) {
+      int nslow = 0;
+      if (p.srows) {
+#pragma unroll
+        for (int j = 1; j < kMaxDigits; ++j)
+          if (j < nd && p.ord[j] != p.mode) ++nslow;
+      }
       if (lane == 0)
         mbar_expect_tx(&sm.full[stage],
-                       (uint32_t)(ncols * Wb * 8 + (has_f0 ? ncols * p.RS * 8 : 0)));
+                       (uint32_t)(ncols * Wb * 8 + (has_f0 ? ncols * p.RS * 8 : 0) + nslow * p.RS * 8));
       __syncwarp();
+      if (p.srows) {
+        // the factor rows of the slow digits (constant over the stage), one copy each
+#pragma unroll
+        for (int j = 1; j < kMaxDigits; ++j)
+          if (j < nd && p.ord[j] != p.mode && lane == j)
+            bulk_g2s(sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.RS, p.At[p.ord[j]] + (int64_t)B[j] * p.RS,
+                     (uint32_t)(p.RS * 8), &sm.full[stage]);
+      }
       // Z columns: q advances by qsd[0] per column within a stage (digit 0 only).  Strided
       // columns are issued by all 32 lanes (one bulk copy per column).
       if (p.RB == 1 && p.qsd[0] == 1 && p.zcs == 0) {

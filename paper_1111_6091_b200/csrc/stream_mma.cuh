@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     sm.zbuf = reinterpret_cast<double *>(smem_raw);
     sm.abuf = sm.zbuf + (size_t)p.nstages * p.zst;
     sm.wbuf = sm.abuf + (size_t)p.nstages * p.cps * p.ars;
-    sm.red = sm.wbuf + (size_t)p.nstages * p.cps * p.wstr;
+    sm.sbuf = sm.wbuf + (size_t)p.nstages * p.cps * p.wstr;
+    sm.red = sm.sbuf + (p.srows ? (size_t)p.nstages * kMaxDigits * p.RS : 0);
     sm.sS = sm.red + p.red_doubles;
     sm.full = reinterpret_cast<uint64_t *>(sm.sS + 32);
     sm.wready = sm.full + p.nstages;
@@ -147,6 +148,21 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     const int slot = h[2];
     const double *zs = sm.zbuf + (size_t)stage * p.zst + arow0;
     const double *ws = (p.direct_w ? sm.abuf : sm.wbuf) + (size_t)stage * p.cps * wstride + gq;
+    // Khatri-Rao rows = staged factor rows x S, S = product of the slow digits' rows (staged by
+    // the producer; S = 1 when there are none)
+    double sl[NT];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) sl[n] = 1.0;
+    if (p.srows) {
+#pragma unroll
+      for (int j = 1; j < kMaxDigits; ++j) {
+        if (j < p.nd && p.ord[j] != p.mode) {
+          const double *sr = sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.RS + gq;
+#pragma unroll
+          for (int n = 0; n < NT; ++n) sl[n] *= sr[8 * n];
+        }
+      }
+    }
     // full k-steps (4 landed columns): only the rank mask applies
     int k0 = 4 * kg;
     for (; k0 + 4 <= ncols; k0 += 4 * KS) {
@@ -159,7 +175,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #pragma unroll
       for (int n = 0; n < NT; ++n) b[n] = wb[8 * n];
 #pragma unroll
-      for (int n = 0; n < NT; ++n) b[n] = nok[n] ? b[n] : 0.0;
+      for (int n = 0; n < NT; ++n) b[n] = nok[n] ? b[n] * sl[n] : 0.0;
 #pragma unroll
       for (int j = 0; j < MT; ++j)
 #pragma unroll
@@ -181,7 +197,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #pragma unroll
       for (int j = 0; j < MT; ++j) a[j] = ok ? a[j] : 0.0;
 #pragma unroll
-      for (int n = 0; n < NT; ++n) b[n] = (ok && nok[n]) ? b[n] : 0.0;
+      for (int n = 0; n < NT; ++n) b[n] = (ok && nok[n]) ? b[n] * sl[n] : 0.0;
 #pragma unroll
       for (int j = 0; j < MT; ++j)
 #pragma unroll
