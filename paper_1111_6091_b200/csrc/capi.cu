@@ -434,7 +434,7 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     L.edge = off; off = align_up(off + (size_t)2 * y.Gc * y.RB * s.dims[0] * R);
     L.mbuf = off; off = align_up(off + (size_t)maxI * R);
     L.yr = off; off = align_up(off + (size_t)L.s3.dims[2] * R);
-    L.segtab = off; off = align_up(off + (size_t)s.dims[1]);  // int2 per segment
+    L.segtab = off; off = align_up(off + (size_t)(s.dims[1] * y.RB + 1) / 2);  // u32 ticket per (segment, row block)
   }
   L.total = off * sizeof(double);
   return true;
@@ -566,6 +566,11 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
   PrepArgs pa;
   PrepGrams pg;
   fill_prep(*s, L, w, (const double *const *)A, -1, true, w + L.status, pa, pg);
+  const bool yl_inline = L.tree && L.yl_plan.mma && env_int("CP_YL_INLINE_FIX", 1);
+  if (yl_inline) {  // Y_L segment tickets (stream_mma.cuh yl_complete_segment)
+    pa.zero = reinterpret_cast<unsigned *>(w + L.segtab);
+    pa.nzero = (int)(s->dims[1] * L.yl_plan.RB);
+  }
   if (launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
   int launches = 1;
   double *gp[2] = {w + L.gpart0, w + L.gpart1};
@@ -624,6 +629,7 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     for (int k = 0; k < N; ++k) p1.At[k] = w + L.At[k];
     p1.yl = w + L.yl;
     p1.edge = w + L.edge;
+    p1.segcnt = yl_inline ? reinterpret_cast<unsigned *>(w + L.segtab) : nullptr;
     p1.part = nullptr;
     if (launch_stream(p1, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
@@ -639,8 +645,10 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     yg.yl = w + L.yl;
     yg.edge = w + L.edge;
     double *mb = w + L.mbuf;
-    if (launch_yl_fixup(yg, cs) != cudaSuccess) return CP_ECUDA;
-    ++launches;
+    if (!yl_inline) {
+      if (launch_yl_fixup(yg, cs) != cudaSuccess) return CP_ECUDA;
+      ++launches;
+    }
     // mode 0: M0 = sum_{i1} Y_L(:, i1, :) * A^(1)(i1, :)   (A^(2..) old: Gauss-Seidel order)
     if (launch_ymm0(yg, A[1], mb, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;

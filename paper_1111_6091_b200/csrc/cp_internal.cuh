@@ -53,6 +53,7 @@ struct StreamPlan {
   double *part;     // partial outputs (workspace)
   double *yl;       // OP_YL: I0 x R block per fully owned segment (segment-major)
   double *edge;     // OP_YL: per CTA 2 blocks for partially owned segments
+  unsigned *segcnt; // OP_YL (MMA): per (segment, row block) completion tickets (zeroed by prep), or null
   int red_doubles;  // consumers' shared reduction area (doubles)
   // FP64 tensor-core consumers (stream_mma.cuh): mma = 1 selects stream_mma_kernel<NT, MT, OP>
   int mma;

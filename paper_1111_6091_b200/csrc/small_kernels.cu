@@ -96,6 +96,8 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
     a.status[1] = -1.0;
     *reinterpret_cast<unsigned *>(a.status + kTicketSlot) = 0u;  // solve completion ticket
   }
+  if (blockIdx.x == 0 && a.zero != nullptr)
+    for (int i = tid; i < a.nzero; i += blockDim.x) a.zero[i] = 0u;
   if (A == nullptr) return;
   double *At = a.At[k];
   const int64_t i0 = (int64_t)b * kPrepRows;

@@ -74,6 +74,8 @@ struct PrepArgs {
   double *At[CP_MAX_N];
   double *gpre;    // per-block partial Grams (may be null: no Grams)
   double *status;  // may be null
+  unsigned *zero;  // zeroed by block 0 (Y_L segment tickets), may be null
+  int nzero;
 };
 
 // Where the prep kernel left the partial Grams of the input factors.

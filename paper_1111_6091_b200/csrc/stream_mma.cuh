@@ -70,6 +70,59 @@ __device__ __forceinline__ void mma_ksum(double (&acc)[MT][NT][2], double *red, 
   }
 }
 
+// A segment split between CTAs: every contributor, after writing its edge block, takes a ticket
+// on the segment's counter; the last one sums the contributors' edge blocks in CTA order into yl
+// (the fixed order of yl_fixup_kernel, so results do not depend on which CTA finishes last) and
+// resets the counter.  Called by all consumer threads.
+__device__ __forceinline__ void yl_complete_segment(const StreamPlan &p, int64_t s, int rb, int64_t row0, int Wb,
+                                                 double *scratch) {
+  __shared__ int s_last, s_clo, s_chi, s_edclo;
+  const int tid = threadIdx.x;
+  __threadfence();  // this thread's edge stores before the ticket
+  named_bar_sync(1, kConsumers);
+  if (tid == 0) {
+    const int64_t clo = ((s * p.Qn + 1) * p.Gc - 1) / p.Q;
+    const int64_t chi = (((s + 1) * p.Qn) * p.Gc - 1) / p.Q;
+    const unsigned old = atomicAdd(p.segcnt + s * p.RB + rb, 1u);
+    s_last = (old == (unsigned)(chi - clo)) ? 1 : 0;
+    s_clo = (int)clo;
+    s_chi = (int)chi;
+    s_edclo = ((clo * p.Q) / p.Gc == s * p.Qn) ? 0 : 1;  // s is clo's first segment, else its last
+  }
+  named_bar_sync(1, kConsumers);
+  if (s_last) {
+    __threadfence();
+    const int R = p.R;
+    const int64_t blk = p.I1 * R;
+    const int clo = s_clo, chi = s_chi, edclo = s_edclo;
+    const int n = Wb * R;
+    // 8 elements per thread in flight per contributor (the loop is latency-bound)
+    for (int e0 = tid; e0 < n; e0 += 8 * kConsumers) {
+      int64_t off[8];
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * kConsumers;
+        const int ec = e < n ? e : 0;
+        const int r = ec / Wb, i = ec - (ec / Wb) * Wb;
+        off[u] = row0 + i + p.I1 * r;
+        acc[u] = 0.0;
+      }
+      for (int c = clo; c <= chi; ++c) {
+        const int ed = (c == clo) ? edclo : 0;
+        const double *src = p.edge + (((int64_t)c * p.RB + rb) * 2 + ed) * blk;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] += __ldcg(src + off[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e0 + u * kConsumers < n) p.yl[s * blk + off[u]] = acc[u];
+    }
+    if (tid == 0) p.segcnt[s * p.RB + rb] = 0u;
+  }
+  (void)scratch;
+}
+
 template <int NT, int MT, int OP>
 __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __grid_constant__ StreamPlan p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -215,9 +268,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
       const int Wq = opaque(Wb);
       const int64_t I1q = opaque(p.I1);
       mma_ksum<NT, MT>(acc, sm.red, KS, kg, wi, Wq, gq, tq);
+      const int64_t s_abs = v0 / p.Qn + slot;
+      const bool full = (s_abs * p.Qn >= v0) && ((s_abs + 1) * p.Qn <= v1);
       if (kg == 0) {
-        const int64_t s_abs = v0 / p.Qn + slot;
-        const bool full = (s_abs * p.Qn >= v0) && ((s_abs + 1) * p.Qn <= v1);
         double *dst = (full ? p.yl + s_abs * I1q * R
                             : p.edge + ((int64_t)blockIdx.x * 2 + (slot == 0 ? 0 : 1)) * I1q * R) +
                       row0;
@@ -238,6 +291,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
       for (int j = 0; j < MT; ++j)
 #pragma unroll
         for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
+      if (!full && p.segcnt != nullptr) yl_complete_segment(p, s_abs, rb, row0, Wq, sm.red);
     }
     if (OP == OP_MTTKRP && p.mode != 0 && (flags & 1)) {
       // ---- end of an i_m segment: contract with the A^(1) rows, reduce lanes and warps ----
