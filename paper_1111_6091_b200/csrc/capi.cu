@@ -366,7 +366,7 @@ struct Layout {
   StreamPlan yl_plan, p2_plan;
   cp_shape s3;
   int rpc2, sp2, nyr;
-  size_t yl, edge, mbuf, yr, segtab;
+  size_t yl, edge, mbuf, yr, segtab, m0part;
 };
 
 static size_t align_up(size_t x) { return (x + 31) & ~(size_t)31; }  // 256 B in doubles
@@ -409,6 +409,20 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     const size_t d = stream_part_doubles(L.p2_plan);
     if (d > part) part = d;
     row_blocking(L.p2_plan, &L.rpc2, &L.sp2);
+    {
+      // the tree's mode-0 solve (ymm0 partials) and its direct-M solves (rpc 256 / R)
+      int rpc0, sp0;
+      ymm0_solve_blocking(R, s.dims[1], &rpc0, &sp0);
+      const int n0 = (int)ceil_div(s.dims[0], rpc0);
+      if (n0 > L.gp_max) L.gp_max = n0;
+      const int rpcd = 256 / R > 0 ? 256 / R : 1;
+      for (int k = 0; k < s.N; ++k) {
+        const int nk = (int)ceil_div(s.dims[k], rpcd);
+        if (nk > L.gp_max) L.gp_max = nk;
+      }
+      const int n2 = (int)ceil_div(s.dims[2], L.rpc2);
+      if (n2 > L.gp_max) L.gp_max = n2;
+    }
     L.nyr = (int)ceil_div(L.s3.dims[2], L.rpc2);
   }
   L.norm_blocks = 2 * sms;
@@ -433,6 +447,7 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     L.yl = off; off = align_up(off + (size_t)s.dims[0] * s.dims[1] * R);
     L.edge = off; off = align_up(off + (size_t)2 * y.Gc * y.RB * s.dims[0] * R);
     L.mbuf = off; off = align_up(off + (size_t)maxI * R);
+    L.m0part = off; off = align_up(off + (size_t)32 * s.dims[0] * R);  // ymm0 range partials (<= 32)
     L.yr = off; off = align_up(off + (size_t)L.s3.dims[2] * R);
     L.segtab = off; off = align_up(off + (size_t)(s.dims[1] * y.RB + 1) / 2);  // u32 ticket per (segment, row block)
   }
@@ -650,9 +665,24 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
       ++launches;
     }
     // mode 0: M0 = sum_{i1} Y_L(:, i1, :) * A^(1)(i1, :)   (A^(2..) old: Gauss-Seidel order)
-    if (launch_ymm0(yg, A[1], mb, cs) != cudaSuccess) return CP_ECUDA;
+    if (launch_ymm0(yg, A[1], w + L.m0part, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
-    if (!solve_mode(0, direct_geom(mb, s->dims[0], R), rpc_d, 1)) return CP_ECUDA;
+    {
+      // the mode-0 solve sums the ymm0 range partials (mode-0 partial layout, fixed order)
+      ReduceGeom g0;
+      memset(&g0, 0, sizeof(g0));
+      g0.R = R;
+      g0.Gc = ymm0_ranges(R, s->dims[1]);
+      g0.RB = 1;
+      g0.slots = 1;
+      g0.mode0 = 1;
+      g0.I1 = s->dims[0];
+      g0.In_rows = s->dims[0];
+      g0.part = w + L.m0part;
+      int rpc0, sp0;
+      ymm0_solve_blocking(R, s->dims[1], &rpc0, &sp0);
+      if (!solve_mode(0, g0, rpc0, sp0)) return CP_ECUDA;
+    }
     // mode 1: M1 = sum_{i0} Y_L(i0, :, :) * A^(0)_new(i0, :)
     if (launch_ymm1(yg, A[0], mb, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;

@@ -459,61 +459,90 @@ __global__ void __launch_bounds__(256) yl_fixup_kernel(const YLGeom y, int chunk
   }
 }
 
-// M0(i0, r) = sum_{i1} Y_L(i0, i1, r) A^(1)(i1, r).  Block (32-row tile of i0, r): lane -> i0
-// (coalesced Y_L reads), warp w -> the w-th eighth of the i1 range; the 8 warp partials combine
-// in warp order.  A1 is the column-major factor (I1 x R).
-__global__ void __launch_bounds__(256) ymm0_kernel(const YLGeom y, const double *A1, double *M0) {
+// Partials of M0(i0, r) = sum_{i1} Y_L(i0, i1, r) A^(1)(i1, r).  Block (b, r) sums the i1 of
+// range b (of S ranges); warp w takes the i1 = w (mod 8) of the range and reads whole 4-KB
+// Y_L(:, i1, r) rows (lane -> i0 = lane + 32 k, 16 k per chunk of 512 rows); the 8 warp sums
+// combine in warp order into part[b][r][i0] -- the layout of the mode-0 MTTKRP partials, summed
+// in range order by the mode-0 solve (ReduceGeom mode0, Gc = S).
+__global__ void __launch_bounds__(256) ymm0_kernel(const YLGeom y, const double *A1, int S, double *part) {
   griddep();
-  __shared__ double sred[8][32];
+  __shared__ double sred[8][512];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int r = blockIdx.y;
-  const int64_t i0 = (int64_t)blockIdx.x * 32 + lane;
+  const int b = blockIdx.x, r = blockIdx.y;
   const int64_t blk = y.I0 * y.R;
-  const int64_t a = (y.I1 * w) / 8, b = (y.I1 * (w + 1)) / 8;
-  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (i0 < y.I0) {
-    const double *yp = y.yl + y.I0 * r + i0;
-    const double *ap = A1 + y.I1 * r;
-    int64_t i1 = a;
-    for (; i1 + 8 <= b; i1 += 8) {
+  const int64_t a0 = (y.I1 * b) / S, a1 = (y.I1 * (b + 1)) / S;
+  const double *ap = A1 + y.I1 * r;
+  for (int64_t c0 = 0; c0 < y.I0; c0 += 512) {
+    double acc[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) s[j] = fma(yp[(i1 + j) * blk], ap[i1 + j], s[j]);
+    for (int k = 0; k < 16; ++k) acc[k] = 0.0;
+    const double *yr0 = y.yl + y.I0 * r + c0 + lane;
+    const int nk = (int)((y.I0 - c0 + 31 - lane) / 32);  // rows of this lane in the chunk
+    for (int64_t i1 = a0 + w; i1 < a1; i1 += 8) {
+      const double av = ap[i1];
+      const double *yp = yr0 + i1 * blk;
+      if (nk >= 16) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = fma(yp[32 * k], av, acc[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k < nk) acc[k] = fma(yp[32 * k], av, acc[k]);
+      }
     }
-    for (int j = 0; i1 < b; ++i1, ++j) s[j] = fma(yp[i1 * blk], ap[i1], s[j]);
-  }
-  sred[w][lane] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
-  __syncthreads();
-  if (w == 0 && i0 < y.I0) {
-    double t = 0.0;
+    __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += sred[k][lane];
-    M0[i0 + y.I0 * r] = t;
+    for (int k = 0; k < 16; ++k) sred[w][lane + 32 * k] = acc[k];
+    __syncthreads();
+    for (int e = threadIdx.x; e < 512 && c0 + e < y.I0; e += blockDim.x) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += sred[k][e];
+      part[((int64_t)b * y.R + r) * y.I0 + c0 + e] = t;
+    }
   }
 }
 
-// M1(i1, r) = sum_{i0} Y_L(i0, i1, r) A^(0)(i0, r): warp per (i1, r), lanes stride over i0
-// (contiguous in Y_L and in the column-major A0), 8 independent partial sums per lane, fixed
-// shuffle tree
+// M1(i1, r) = sum_{i0} Y_L(i0, i1, r) A^(0)(i0, r): warp per (r, 4 consecutive i1), lanes stride
+// over i0 (contiguous in Y_L and in the column-major A0; each A0 value feeds 4 rows), 4
+// independent partial sums per row, fixed shuffle tree
 __global__ void __launch_bounds__(256) ymm1_kernel(const YLGeom y, const double *A0, double *M1) {
   griddep();
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (w >= y.I1 * y.R) return;
-  const int64_t i1 = w % y.I1;
-  const int r = (int)(w / y.I1);
-  const double *yp = y.yl + i1 * y.I0 * y.R + y.I0 * r;
+  const int64_t nq = (y.I1 + 3) / 4;
+  if (wg >= nq * y.R) return;
+  const int r = (int)(wg / nq);
+  const int64_t i1b = (wg - (int64_t)r * nq) * 4;
+  const int64_t blk = y.I0 * y.R;
   const double *ap = A0 + y.I0 * r;
-  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int64_t i0 = lane;
-  for (; i0 + 7 * 32 < y.I0; i0 += 8 * 32) {
+  const double *yp = y.yl + i1b * blk + y.I0 * r;
+  int nu = (int)(y.I1 - i1b);
+  if (nu > 4) nu = 4;
+  double s[4][4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) s[j] = fma(yp[i0 + 32 * j], ap[i0 + 32 * j], s[j]);
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s[u][j] = 0.0;
+  for (int64_t i0 = lane; i0 < y.I0; i0 += 128) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t idx = i0 + 32 * j;
+      if (idx < y.I0) {
+        const double a = ap[idx];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < nu) s[u][j] = fma(yp[u * blk + idx], a, s[u][j]);
+      }
+    }
   }
-  for (int j = 0; i0 < y.I0; i0 += 32, ++j) s[j] = fma(yp[i0], ap[i0], s[j]);
-  double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
-  if (lane == 0) M1[i1 + y.I1 * r] = t;
+  for (int u = 0; u < 4; ++u) {
+    double t = (s[u][0] + s[u][1]) + (s[u][2] + s[u][3]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (lane == 0 && u < nu) M1[i1b + u + y.I1 * r] = t;
+  }
 }
 
 // warp per (i_m, r): lanes stride over the other indices j of modes 2..N-1
@@ -559,12 +588,30 @@ cudaError_t launch_yl_fixup(const YLGeom &y, cudaStream_t st) {
   return launch_k(yl_fixup_kernel, dim3((unsigned)((y.Gc - 1) * chunks)), dim3(256), 0, st, y, chunks);
 }
 
-cudaError_t launch_ymm0(const YLGeom &y, const double *A1, double *M0, cudaStream_t st) {
-  return launch_k(ymm0_kernel, dim3((unsigned)((y.I0 + 31) / 32), (unsigned)y.R), dim3(256), 0, st, y, A1, M0);
+int ymm0_ranges(int R, int64_t I1) {
+  int S = (296 + R - 1) / R;  // about two blocks per SM
+  if (S > 32) S = 32;
+  if (S > I1) S = (int)I1;
+  return S < 1 ? 1 : S;
+}
+
+void ymm0_solve_blocking(int R, int64_t I1, int *rpc, int *sp) {
+  int s = ymm0_ranges(R, I1) / 4;
+  if (s < 1) s = 1;
+  if (s > 8) s = 8;
+  while (s > 1 && R * s > 256) --s;
+  int r = 256 / (R * s);
+  *sp = s;
+  *rpc = r < 1 ? 1 : r;
+}
+
+cudaError_t launch_ymm0(const YLGeom &y, const double *A1, double *part, cudaStream_t st) {
+  const int S = ymm0_ranges(y.R, y.I1);
+  return launch_k(ymm0_kernel, dim3((unsigned)S, (unsigned)y.R), dim3(256), 0, st, y, A1, S, part);
 }
 
 cudaError_t launch_ymm1(const YLGeom &y, const double *A0, double *M1, cudaStream_t st) {
-  const int64_t threads = y.I1 * y.R * 32;
+  const int64_t threads = ((y.I1 + 3) / 4) * y.R * 32;
   return launch_k(ymm1_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, y, A0, M1);
 }
 

@@ -157,8 +157,12 @@ inline ReduceGeom direct_geom(const double *M, int64_t rows, int R) {
 }
 // completes the segments split between CTAs (edge blocks -> yl)
 cudaError_t launch_yl_fixup(const YLGeom &y, cudaStream_t st);
-// M0(i0, r) = sum_{i1} Y_L(i0, i1, r) A^(1)(i1, r)   (A1: column-major I1 x R)
-cudaError_t launch_ymm0(const YLGeom &y, const double *A1, double *M0, cudaStream_t st);
+// partials of M0(i0, r) = sum_{i1} Y_L(i0, i1, r) A^(1)(i1, r) (A1: column-major I1 x R):
+// part[b][r][i0] for b < ymm0_ranges(y) -- summed in b order by the mode-0 solve
+int ymm0_ranges(int R, int64_t I1);
+// row blocking (rows per CTA, threads per entry) of the mode-0 solve that sums those partials
+void ymm0_solve_blocking(int R, int64_t I1, int *rpc, int *sp);
+cudaError_t launch_ymm0(const YLGeom &y, const double *A1, double *part, cudaStream_t st);
 // M1(i1, r) = sum_{i0} Y_L(i0, i1, r) A^(0)(i0, r)   (A0: column-major I0 x R)
 cudaError_t launch_ymm1(const YLGeom &y, const double *A0, double *M1, cudaStream_t st);
 // M_m(i_m, r) = sum_{j: i_m(j)} Y_R(j, r) prod_{k >= 2, k != m} A^(k)(i_k(j), r), j over modes 2..N-1
