@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "gamma_job.cuh"
 #include "mg_kernels.cuh"
 #include "small_kernels.cuh"
 #include "stream_kernel.cuh"
@@ -273,6 +274,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   // ring: CP_RING_BYTES (default 96 KB) of stages, at least 2; the MMA kernels also keep the whole
   // CTA within the 2-CTAs/SM shared-memory budget (113 KB) by shrinking the stage if needed
   const int cap = env_int("CP_SMEM_CAP", 113 * 1024);
+  p.gjsm = (p.mma && p.direct_w) ? gamma_job_smem_doubles(s.R) : 0;  // Gamma job (gamma_job.cuh)
   const int unit = p.mma ? 4 * p.ks : 1;
   int stage_doubles = 0, nst = 2;
   for (;;) {
@@ -283,7 +285,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     // mode-0 slot / k-group reduction reuses the Z ring: it must hold the reduced blocks
     const int64_t need = p.mma ? (int64_t)(p.ks - 1) * p.Wmax * 8 * p.nt : (int64_t)p.Wmax * s.R;
     while ((int64_t)nst * p.zst < need) ++nst;
-    const int bytes = (nst * stage_doubles + p.red_doubles + 32) * 8 + nst * 88 + 64;
+    const int bytes = (nst * stage_doubles + p.red_doubles + p.gjsm + 32) * 8 + nst * 88 + 64;
     if (!p.mma || bytes <= cap || cps <= unit) break;
     cps -= unit;
     p.cps = cps;
@@ -291,7 +293,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   }
   p.nstages = nst;
   p.dbg = env_int("CP_STREAM_DBG", 0);
-  p.smem_bytes = (nst * stage_doubles + p.red_doubles + 32) * 8 + nst * 88 + 64;
+  p.smem_bytes = (nst * stage_doubles + p.red_doubles + p.gjsm + 32) * 8 + nst * 88 + 64;
   if (p.smem_bytes > 200 * 1024) return false;
   const int occ = p.mma ? stream_mma_occupancy(p.nt, p.mt, op, p.smem_bytes)
                         : stream_occupancy(s.R, p.V, op, p.smem_bytes);
@@ -366,7 +368,7 @@ struct Layout {
   StreamPlan yl_plan, p2_plan;
   cp_shape s3;
   int rpc2, sp2, nyr;
-  size_t yl, edge, mbuf, yr, segtab, m0part;
+  size_t yl, edge, mbuf, yr, segtab, m0part, linv;
 };
 
 static size_t align_up(size_t x) { return (x + 31) & ~(size_t)31; }  // 256 B in doubles
@@ -448,6 +450,7 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     L.edge = off; off = align_up(off + (size_t)2 * y.Gc * y.RB * s.dims[0] * R);
     L.mbuf = off; off = align_up(off + (size_t)maxI * R);
     L.m0part = off; off = align_up(off + (size_t)32 * s.dims[0] * R);  // ymm0 range partials (<= 32)
+    L.linv = off; off = align_up(off + (size_t)s.N * R * R);  // L^{-1} of every Gamma^(n)
     L.yr = off; off = align_up(off + (size_t)L.s3.dims[2] * R);
     L.segtab = off; off = align_up(off + (size_t)(s.dims[1] * y.RB + 1) / 2);  // u32 ticket per (segment, row block)
   }
@@ -591,7 +594,7 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
   double *gp[2] = {w + L.gpart0, w + L.gpart1};
   int grid_of[CP_MAX_N] = {0};
   // a4 for mode n from M given by rg (stream partials or a plain M buffer)
-  auto solve_mode = [&](int n, const ReduceGeom &rg, int rpc, int sp) -> bool {
+  auto solve_mode = [&](int n, const ReduceGeom &rg, int rpc, int sp, const double *linv = nullptr) -> bool {
     SolveArgs sa;
     memset(&sa, 0, sizeof(sa));
     sa.N = N;
@@ -613,6 +616,8 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     sa.dotM = w + L.dotM;
     sa.dotF = w + L.dotF + (size_t)n * L.gp_max;
     sa.status = w + L.status;
+    sa.dbg = env_int("CP_SOLVE_DBG", 0);
+    sa.linv = linv;
     grid_of[n] = (int)ceil_div(s->dims[n], rpc);
     if (n == N - 1) {
       // the sweep's last solve also evaluates f, f~ (finalize_body in its last block)
@@ -637,6 +642,35 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
   };
   const int RS = R + (R & 1);
   const int rpc_d = 256 / R > 0 ? 256 / R : 1;
+  const int RR = R * R;
+  // Gamma^(n) job (gamma_job.cuh): Upsilon^(k) for k > n from the prep partials (old factors),
+  // k = n-1 from the previous solve's partials, k < n-1 from the totals earlier jobs wrote
+  const bool jobs = L.tree && env_int("CP_GAMMA_JOBS", 1) != 0;
+  auto gamma_job = [&](int n) -> GammaJob {
+    GammaJob g;
+    memset(&g, 0, sizeof(g));
+    g.on = 1;
+    g.N = N;
+    g.R = R;
+    g.mode = n;
+    for (int k = 0; k < N; ++k) {
+      if (k == n) continue;
+      if (k > n) {
+        g.src[k] = w + L.gpre + (size_t)pg.blk_off[k] * RR;
+        g.cnt[k] = pg.nblk[k];
+      } else if (k == n - 1) {
+        g.src[k] = gp[k & 1];
+        g.cnt[k] = grid_of[k];
+      } else {
+        g.src[k] = w + L.Ups + (size_t)k * RR;
+        g.cnt[k] = 0;
+      }
+    }
+    g.ups = w + L.Ups;
+    g.linv = w + L.linv + (size_t)n * RR;
+    g.status = w + L.status;
+    return g;
+  };
   if (L.tree) {
     // ---- dimension-tree sweep: two passes over Z instead of N ----
     StreamPlan p1 = L.yl_plan;
@@ -646,6 +680,9 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     p1.edge = w + L.edge;
     p1.segcnt = yl_inline ? reinterpret_cast<unsigned *>(w + L.segtab) : nullptr;
     p1.part = nullptr;
+    // Gamma^(0) (Grams of the old factors only) rides in the Y_L pass's idle weight warp
+    const bool job0 = jobs && p1.mma && p1.direct_w;
+    if (job0) p1.gj = gamma_job(0);
     if (launch_stream(p1, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     YLGeom yg;
@@ -681,12 +718,16 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
       g0.part = w + L.m0part;
       int rpc0, sp0;
       ymm0_solve_blocking(R, s->dims[1], &rpc0, &sp0);
-      if (!solve_mode(0, g0, rpc0, sp0)) return CP_ECUDA;
+      if (!solve_mode(0, g0, rpc0, sp0, job0 ? w + L.linv : nullptr)) return CP_ECUDA;
     }
-    // mode 1: M1 = sum_{i0} Y_L(i0, :, :) * A^(0)_new(i0, :)
-    if (launch_ymm1(yg, A[0], mb, cs) != cudaSuccess) return CP_ECUDA;
+    // mode 1: M1 = sum_{i0} Y_L(i0, :, :) * A^(0)_new(i0, :); Gamma^(1) in an extra block
+    GammaJob gj1;
+    memset(&gj1, 0, sizeof(gj1));
+    if (jobs) gj1 = gamma_job(1);
+    if (launch_ymm1(yg, A[0], mb, gj1, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
-    if (!solve_mode(1, direct_geom(mb, s->dims[1], R), rpc_d, 1)) return CP_ECUDA;
+    if (!solve_mode(1, direct_geom(mb, s->dims[1], R), rpc_d, 1, jobs ? w + L.linv + (size_t)RR : nullptr))
+      return CP_ECUDA;
     // pass 2: modes >= 2 from Z x I0 x I1 contracted with the new A^(0), A^(1)
     StreamPlan p2 = L.p2_plan;
     p2.Z = Z;
@@ -694,10 +735,14 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     p2.At[1] = w + L.At[1];
     p2.At[2] = nullptr;
     p2.part = w + L.part;
+    // Gamma^(2) rides in the pass's idle weight warp
+    const bool job2 = jobs && p2.mma && p2.direct_w;
+    if (job2) p2.gj = gamma_job(2);
     if (launch_stream(p2, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     if (N == 3) {
-      if (!solve_mode(2, reduce_geom(p2), L.rpc2, L.sp2)) return CP_ECUDA;
+      if (!solve_mode(2, reduce_geom(p2), L.rpc2, L.sp2, job2 ? w + L.linv + (size_t)2 * RR : nullptr))
+        return CP_ECUDA;
     } else {
       if (launch_k(reduce_mttkrp_kernel, dim3(L.nyr), dim3(256), 0, cs, reduce_geom(p2), L.rpc2, L.sp2, w + L.yr) != cudaSuccess)
         return CP_ECUDA;
@@ -715,9 +760,14 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
         }
         ya.YR = w + L.yr;
         ya.M = mb;
+        // Gamma^(2) came with pass 2; Gamma^(m > 2) in an extra yr block when CP_GAMMA_JOBS=2
+        // (measured: the yr kernels are too short to hide it)
+        const bool jm = (m == 2) ? job2 : (jobs && env_int("CP_GAMMA_JOBS", 1) >= 2);
+        if (m > 2 && jm) ya.gj = gamma_job(m);
         if (launch_yr(ya, cs) != cudaSuccess) return CP_ECUDA;
         ++launches;
-        if (!solve_mode(m, direct_geom(mb, s->dims[m], R), rpc_d, 1)) return CP_ECUDA;
+        if (!solve_mode(m, direct_geom(mb, s->dims[m], R), rpc_d, 1, jm ? w + L.linv + (size_t)m * RR : nullptr))
+          return CP_ECUDA;
       }
     }
   } else {

@@ -20,6 +20,16 @@ constexpr int kMaxDigits = CP_MAX_N - 1;          // column multi-index digits (
 // with A^(0)); see stream_kernel.cuh.
 enum StreamOp { OP_MTTKRP = 0, OP_RESID = 1, OP_YL = 2 };
 
+// Gamma^(mode) factorization job (gamma_job.cuh): Upsilon^(k) for k != mode is the sum of cnt[k]
+// R x R partials at src[k] (stride R*R, summed in order, total written to ups[k]) or, cnt[k] = 0,
+// the total at src[k]; out: L^{-1} (R x R row-major) in linv; CP_ENOTSPD + mode in status.
+struct GammaJob {
+  int on, N, R, mode;
+  const double *src[CP_MAX_N];
+  int cnt[CP_MAX_N];
+  double *ups, *linv, *status;
+};
+
 // Plan of one streaming pass over Z (MTTKRP of one mode, or the residual pass of cp_fit).
 // Z is viewed as an I1 x Q column-major matrix (Q = P / I1 "columns" = mode-1 fibers).
 // Column groups: CTA (c, rb) streams virtual columns [v0(c), v1(c)) restricted to row block
@@ -63,6 +73,8 @@ struct StreamPlan {
   int direct_w;     // Khatri-Rao rows are the staged factor rows (no weight warp)
   int ars, wstr;    // shared-memory row strides of the staged factor rows / the weight rows
   int srows;        // the producer also stages the slow digits' factor rows (kMaxDigits per stage)
+  GammaJob gj;      // optional side job for the idle weight warp of CTA 0 (MMA kernel, direct_w)
+  int gjsm;         // shared-memory doubles reserved for it
   int dbg;          // experiments only (env CP_STREAM_DBG): 1 = consumers skip the FMAs, 2 = weight warp skips forming
 };
 

@@ -193,34 +193,43 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool live = (a.status[0] == 0.0);  // an earlier mode already failed: straight to the ticket
   if (live) {
-    // total Gram of the previous mode from its per-CTA partials (fixed order)
-    if (a.gprev != nullptr) {
+    const int64_t In = a.In;
+    const int64_t i0 = (int64_t)blockIdx.x * a.rpc;
+    const int nrows = (int)((In - i0) < a.rpc ? (In - i0) : a.rpc);
+    if (a.linv != nullptr) {
+      // L^{-1} from the Gamma job (gamma_job.cuh); the Gram totals are in Ups already
+      for (int e = tid; e < RR; e += blockDim.x) sLi[(e / R) * LS + (e % R)] = a.linv[e];
+    } else if (a.gprev != nullptr && !(a.dbg & 1)) {
+      // total Gram of the previous mode from its per-CTA partials (fixed order)
       for (int e = tid; e < RR; e += blockDim.x) {
         const double s = sum_strided(a.gprev + e, RR, a.nprev);
         sUp[e] = s;
         if (blockIdx.x == 0) a.Ups[(int64_t)a.prev_mode * RR + e] = s;
       }
     }
-    const int64_t In = a.In;
-    const int64_t i0 = (int64_t)blockIdx.x * a.rpc;
-    const int nrows = (int)((In - i0) < a.rpc ? (In - i0) : a.rpc);
     // phase A (independent of Gamma): M rows from the stream partials
     gather_rows(a.rg, i0, nrows, R, a.sp, sM, scratch);
     __syncthreads();
-    // Gamma^(n) = *_{k != n} Upsilon^(k)   (eq:Gamma).  Upsilon^(k): k > n from the prep
-    // partials (factor not yet updated in this sweep), k = n-1 from the previous solve's
-    // partials, k < n-1 from the totals the earlier solves wrote.
-    for (int e = tid; e < RR; e += blockDim.x) {
-      double gm = 1.0;
-      for (int k = 0; k < a.N; ++k) {
-        if (k == a.mode) continue;
-        double u;
-        if (k > a.mode) u = prep_gram(a.pg, k, e, RR);
-        else if (k == a.prev_mode) u = sUp[e];
-        else u = a.Ups[(int64_t)k * RR + e];
-        gm *= u;
+    if (a.linv == nullptr) {
+      // Gamma^(n) = *_{k != n} Upsilon^(k)   (eq:Gamma).  Upsilon^(k): k > n from the prep
+      // partials (factor not yet updated in this sweep), k = n-1 from the previous solve's
+      // partials, k < n-1 from the totals the earlier solves wrote.
+      for (int e = tid; e < RR; e += blockDim.x) {
+        double gm = 1.0;
+        if (a.dbg & 1) {
+          sL[(e % R) * LS + (e / R)] = ((e % R) == (e / R)) ? 1.0 : 0.0;
+          continue;
+        }
+        for (int k = 0; k < a.N; ++k) {
+          if (k == a.mode) continue;
+          double u;
+          if (k > a.mode) u = prep_gram(a.pg, k, e, RR);
+          else if (k == a.prev_mode) u = sUp[e];
+          else u = a.Ups[(int64_t)k * RR + e];
+          gm *= u;
+        }
+        sL[(e % R) * LS + (e / R)] = gm;
       }
-      sL[(e % R) * LS + (e / R)] = gm;
     }
     for (int e = tid; e < nrows * R; e += blockDim.x) {
       const int ii = e / R, r = e - (e / R) * R;
@@ -228,7 +237,12 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
     }
     if (tid == 0) sfail = 0;
     __syncthreads();
-    if (warp == 0) {
+    if (a.linv != nullptr) {
+      // (factored by the Gamma job)
+    } else if (warp == 0 && (a.dbg & 1)) {
+      for (int k = 0; k < R; ++k)
+        if (lane < R) sLi[lane * LS + k] = (k == lane) ? 1.0 : 0.0;
+    } else if (warp == 0) {
       // Cholesky, right-looking, lane i = row i (no pivoting; fail on a pivot <= 0 or NaN).
       // 1/L(j,j) = rsqrt(pivot) and L(j,j) = pivot * rsqrt(pivot): no divisions on the chain.
       double g[R];
@@ -506,8 +520,14 @@ __global__ void __launch_bounds__(256) ymm0_kernel(const YLGeom y, const double 
 // M1(i1, r) = sum_{i0} Y_L(i0, i1, r) A^(0)(i0, r): warp per (r, 4 consecutive i1), lanes stride
 // over i0 (contiguous in Y_L and in the column-major A0; each A0 value feeds 4 rows), 4
 // independent partial sums per row, fixed shuffle tree
-__global__ void __launch_bounds__(256) ymm1_kernel(const YLGeom y, const double *A0, double *M1) {
+__global__ void __launch_bounds__(256) ymm1_kernel(const YLGeom y, const double *A0, double *M1,
+                                                   const GammaJob gj) {
   griddep();
+  if (gj.on && blockIdx.x == gridDim.x - 1) {  // extra block: Gamma^(1) for the next solve
+    __shared__ double gsm[gamma_job_smem_doubles(32)];
+    gamma_job_run(gj, gsm, threadIdx.x, blockDim.x, true);
+    return;
+  }
   const int64_t wg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nq = (y.I1 + 3) / 4;
@@ -548,6 +568,11 @@ __global__ void __launch_bounds__(256) ymm1_kernel(const YLGeom y, const double 
 // warp per (i_m, r): lanes stride over the other indices j of modes 2..N-1
 __global__ void __launch_bounds__(256) yr_kernel(const YRArgs a) {
   griddep();
+  if (a.gj.on && blockIdx.x == gridDim.x - 1) {  // extra block: Gamma^(mode) for the next solve
+    __shared__ double gsm[gamma_job_smem_doubles(32)];
+    gamma_job_run(a.gj, gsm, threadIdx.x, blockDim.x, true);
+    return;
+  }
   const int64_t Im = a.dims[a.mode];
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -596,12 +621,11 @@ int ymm0_ranges(int R, int64_t I1) {
 }
 
 void ymm0_solve_blocking(int R, int64_t I1, int *rpc, int *sp) {
-  int s = ymm0_ranges(R, I1) / 4;
-  if (s < 1) s = 1;
-  if (s > 8) s = 8;
-  while (s > 1 && R * s > 256) --s;
-  int r = 256 / (R * s);
-  *sp = s;
+  // one thread per M0 entry (sums the <= 32 range partials, 8 loads in flight): keeps the solve
+  // grid -- and so the number of Gram partials the next solve sums -- small
+  (void)I1;
+  const int r = 256 / R;
+  *sp = 1;
   *rpc = r < 1 ? 1 : r;
 }
 
@@ -610,14 +634,15 @@ cudaError_t launch_ymm0(const YLGeom &y, const double *A1, double *part, cudaStr
   return launch_k(ymm0_kernel, dim3((unsigned)S, (unsigned)y.R), dim3(256), 0, st, y, A1, S, part);
 }
 
-cudaError_t launch_ymm1(const YLGeom &y, const double *A0, double *M1, cudaStream_t st) {
+cudaError_t launch_ymm1(const YLGeom &y, const double *A0, double *M1, const GammaJob &gj, cudaStream_t st) {
   const int64_t threads = ((y.I1 + 3) / 4) * y.R * 32;
-  return launch_k(ymm1_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, y, A0, M1);
+  const unsigned grid = (unsigned)((threads + 255) / 256) + (gj.on ? 1u : 0u);
+  return launch_k(ymm1_kernel, dim3(grid), dim3(256), 0, st, y, A0, M1, gj);
 }
 
 cudaError_t launch_yr(const YRArgs &a, cudaStream_t st) {
   const int64_t threads = a.dims[a.mode] * a.R * 32;
-  return launch_k(yr_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, st, a);
+  return launch_k(yr_kernel, dim3((unsigned)((threads + 255) / 256) + (a.gj.on ? 1u : 0u)), dim3(256), 0, st, a);
 }
 
 // ---------------------------------------------------------------- host-side launchers

@@ -3,6 +3,7 @@
 #include <cstring>
 
 #include "cp_internal.cuh"
+#include "gamma_job.cuh"
 
 namespace cpk {
 
@@ -111,6 +112,9 @@ struct SolveArgs {
   double *dotM, *dotF;  // per-CTA <M,A>, <F,A>
   double *status;       // [0] status, [1] failed mode
   int fin_on;           // last solve of the sweep: the last block to finish runs the finalize
+  int dbg;              // experiments only (CP_SOLVE_DBG): 1 = skip Gamma / Cholesky (L = I)
+  const double *linv;   // L^{-1} of Gamma^(mode) from a Gamma job (gamma_job.cuh), or null:
+                        // the solve forms Gamma and factors it itself
   unsigned *ticket;
   FinalizeArgs fin;
 };
@@ -164,10 +168,11 @@ int ymm0_ranges(int R, int64_t I1);
 void ymm0_solve_blocking(int R, int64_t I1, int *rpc, int *sp);
 cudaError_t launch_ymm0(const YLGeom &y, const double *A1, double *part, cudaStream_t st);
 // M1(i1, r) = sum_{i0} Y_L(i0, i1, r) A^(0)(i0, r)   (A0: column-major I0 x R)
-cudaError_t launch_ymm1(const YLGeom &y, const double *A0, double *M1, cudaStream_t st);
+cudaError_t launch_ymm1(const YLGeom &y, const double *A0, double *M1, const GammaJob &gj, cudaStream_t st);
 // M_m(i_m, r) = sum_{j: i_m(j)} Y_R(j, r) prod_{k >= 2, k != m} A^(k)(i_k(j), r), j over modes 2..N-1
 struct YRArgs {
   int N, R, RS, mode;
+  GammaJob gj;  // optional: run by one extra block
   int64_t dims[CP_MAX_N];
   const double *At[CP_MAX_N];
   const double *YR;  // J x R column-major, J = prod_{k >= 2} I_k (mode 2 fastest)

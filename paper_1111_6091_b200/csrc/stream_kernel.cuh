@@ -35,7 +35,7 @@ constexpr int kHdrInts = 16;  // per-stage header: ncols, flags, slot, -, digits
 
 // Shared-memory carve-up of one CTA (all offsets in doubles except the tail).
 struct StreamSmem {
-  double *zbuf, *abuf, *wbuf, *sbuf, *red, *sS;
+  double *zbuf, *abuf, *wbuf, *sbuf, *red, *gjbuf, *sS;
   uint64_t *full, *wready, *empty;
   int *hdr;
 };
@@ -50,7 +50,8 @@ __device__ __forceinline__ StreamSmem carve(unsigned char *raw, const StreamPlan
   s.sbuf = s.wbuf + (size_t)p.nstages * p.cps * p.wstr;
   s.red = s.sbuf + (p.srows ? (size_t)p.nstages * kMaxDigits * p.RS : 0);
   (void)WSTR;
-  s.sS = s.red + p.red_doubles;
+  s.gjbuf = s.red + p.red_doubles;
+  s.sS = s.gjbuf + p.gjsm;
   s.full = reinterpret_cast<uint64_t *>(s.sS + 32);
   s.wready = s.full + p.nstages;
   s.empty = s.wready + p.nstages;

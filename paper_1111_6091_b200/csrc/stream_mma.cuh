@@ -19,6 +19,7 @@
 //    mode >= 1 -- C contracted with the A^(1) rows, reduced over lanes and warps in a fixed
 //    order into one R-vector per (CTA, segment); mode 0 -- the CTA's I1 x R partial.
 #pragma once
+#include "gamma_job.cuh"
 #include "stream_kernel.cuh"
 
 namespace cpk {
@@ -134,7 +135,8 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     sm.wbuf = sm.abuf + (size_t)p.nstages * p.cps * p.ars;
     sm.sbuf = sm.wbuf + (size_t)p.nstages * p.cps * p.wstr;
     sm.red = sm.sbuf + (p.srows ? (size_t)p.nstages * kMaxDigits * p.RS : 0);
-    sm.sS = sm.red + p.red_doubles;
+    sm.gjbuf = sm.red + p.red_doubles;
+    sm.sS = sm.gjbuf + p.gjsm;
     sm.full = reinterpret_cast<uint64_t *>(sm.sS + 32);
     sm.wready = sm.full + p.nstages;
     sm.empty = sm.wready + p.nstages;
@@ -166,7 +168,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     return;
   }
   if (warp == kConsumerWarps + 1) {
-    form_weights(p, lane, sm);  // (returns at once when direct_w)
+    // weight rows (returns at once when direct_w), then the optional Gamma job of CTA 0
+    form_weights(p, lane, sm);
+    if (p.gj.on && blockIdx.x == 0) gamma_job_run(p.gj, sm.gjbuf, lane, 32, false);
     return;
   }
 
