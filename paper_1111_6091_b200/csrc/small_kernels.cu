@@ -141,23 +141,23 @@ __device__ void finalize_body(const FinalizeArgs &a, double *sred) {
     }
     return;
   }
-  // Upsilon^(N) from the last solve's partials; ||[[A]]||^2 = 1^T (*_k Upsilon^(k)) 1
+  // Upsilon^(N) from the last solve's partials; ||[[A]]||^2 = 1^T (*_k Upsilon^(k)) 1.  All
+  // loads are issued before the one combined block reduction.
   double m2 = 0.0;
   for (int e = tid; e < RR; e += blockDim.x) {
+    double p = 1.0;
+    for (int k = 0; k < a.N - 1; ++k) p *= a.Ups[(int64_t)k * RR + e];
     const double u = sum_strided(a.glast + e, RR, a.nlast);
     a.Ups[(int64_t)(a.N - 1) * RR + e] = u;
-    double p = u;
-    for (int k = 0; k < a.N - 1; ++k) p *= a.Ups[(int64_t)k * RR + e];
-    m2 += p;
+    m2 = fma(u, p, m2);
   }
-  const double model2 = block_sum_256(m2, sred);
   double in = 0.0;
   for (int c = tid; c < a.nlast; c += blockDim.x) in += a.dotM_last[c];
-  const double inner = block_sum_256(in, sred);
   double fl = 0.0;
   for (int n = 0; n < a.N; ++n)
     for (int c = tid; c < a.nsolve[n]; c += blockDim.x) fl += a.dotF[(int64_t)n * a.dot_stride + c];
-  const double fa = block_sum_256(fl, sred);
+  block_sum3_256(m2, in, fl, sred);
+  const double model2 = m2, inner = in, fa = fl;
   if (tid == 0) {
     const double f = 0.5 * a.normZ2[0] - inner + 0.5 * model2;
     a.out[0] = f;
@@ -315,8 +315,8 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
         if (a.F != nullptr) df = fma(a.F[i + In * r], x, df);
       }
       // partial Gram of the new rows, and the CTA's <M,A>, <F,A> (fixed order)
-      const double dms = block_sum_256(dm, scratch);
-      const double dfs = block_sum_256(df, scratch);
+      double dms = dm, dfs = df, unused = 0.0;
+      block_sum3_256(dms, dfs, unused, scratch);
       for (int e = tid; e < RR; e += blockDim.x) {
         const int r = e % R, s = e / R;
         double gg = 0.0;

@@ -8,19 +8,36 @@
 namespace cpk {
 
 // ---------------------------------------------------------------- block reduction (fixed tree)
-// blockDim.x == 256; returns the sum to every thread.
+// blockDim.x == 256; returns the sum to every thread (warp xor trees, then the 8 warp sums in a
+// fixed order; two barriers).
 __device__ __forceinline__ double block_sum_256(double v, double *sred) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  __syncthreads();  // (sred may still be read by a previous call)
+  if (lane == 0) sred[w] = v;
   __syncthreads();
-  sred[tid] = v;
-  __syncthreads();
-  for (int off = 128; off > 0; off >>= 1) {
-    if (tid < off) sred[tid] += sred[tid + off];
-    __syncthreads();
+  return ((sred[0] + sred[1]) + (sred[2] + sred[3])) + ((sred[4] + sred[5]) + (sred[6] + sred[7]));
+}
+// three sums at once (sred: 24 doubles)
+__device__ __forceinline__ void block_sum3_256(double &a, double &b, double &c, double *sred) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, off);
+    b += __shfl_xor_sync(0xffffffffu, b, off);
+    c += __shfl_xor_sync(0xffffffffu, c, off);
   }
-  const double r = sred[0];
   __syncthreads();
-  return r;
+  if (lane == 0) {
+    sred[w] = a;
+    sred[8 + w] = b;
+    sred[16 + w] = c;
+  }
+  __syncthreads();
+  a = ((sred[0] + sred[1]) + (sred[2] + sred[3])) + ((sred[4] + sred[5]) + (sred[6] + sred[7]));
+  b = ((sred[8] + sred[9]) + (sred[10] + sred[11])) + ((sred[12] + sred[13]) + (sred[14] + sred[15]));
+  c = ((sred[16] + sred[17]) + (sred[18] + sred[19])) + ((sred[20] + sred[21]) + (sred[22] + sred[23]));
 }
 
 // Where the stream kernel left its partials, and how to sum them (fixed order).
