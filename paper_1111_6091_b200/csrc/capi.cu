@@ -424,6 +424,7 @@ static bool make_layout(Layout &L, const cp_shape &s) {
       }
       const int n2 = (int)ceil_div(s.dims[2], L.rpc2);
       if (n2 > L.gp_max) L.gp_max = n2;
+      if (L.gp_max > L.grad_max) L.grad_max = L.gp_max;  // cp_fit's gradient grids (same blocking)
     }
     L.nyr = (int)ceil_div(L.s3.dims[2], L.rpc2);
   }
@@ -828,6 +829,11 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
   PrepArgs pa;
   PrepGrams pg;
   fill_prep(*s, L, w, A, -1, true, nullptr, pa, pg);
+  const bool yl_inline = L.tree && L.yl_plan.mma && env_int("CP_YL_INLINE_FIX", 1);
+  if (yl_inline) {  // Y_L segment tickets (stream_mma.cuh yl_complete_segment)
+    pa.zero = reinterpret_cast<unsigned *>(w + L.segtab);
+    pa.nzero = (int)(s->dims[1] * L.yl_plan.RB);
+  }
   if (launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
   int launches = 1;
   // residual pass 1/2 ||Z - [[A]]||^2 (eq:CPfunctional): one partial per CTA
@@ -837,36 +843,129 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
   rp.part = w + L.residp;
   if (launch_stream(rp, cs) != cudaSuccess) return CP_ECUDA;
   ++launches;
-  for (int n = 0; n < N; ++n) {
-    StreamPlan p = L.plans[n];
-    p.Z = Z;
-    for (int k = 0; k < N; ++k) p.At[k] = w + L.At[k];
-    p.part = w + L.part;
-    if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
+  int ngrad[CP_MAX_N] = {0};
+  // G^(n) = -M^(n) + A^(n) Gamma^(n) - F^(n) and its squared norm (eq:gradEqn, eq:gradConv)
+  auto grad_mode = [&](int n, const ReduceGeom &rg, int rpc, int sp) -> bool {
     GradArgs ga;
     memset(&ga, 0, sizeof(ga));
     ga.N = N;
     ga.R = R;
     ga.mode = n;
-    ga.rpc = L.rpc[n];
-    ga.sp = L.sp[n];
+    ga.rpc = rpc;
+    ga.sp = sp;
     ga.In = s->dims[n];
-    ga.rg = reduce_geom(p);
+    ga.rg = rg;
     ga.pg = pg;
     ga.A = A[n];
     ga.F = (F != nullptr) ? F[n] : nullptr;
     ga.Ups = w + L.Ups;
     ga.G = (G != nullptr) ? G[n] : nullptr;
     ga.gpart = w + L.gradp + (size_t)n * L.grad_max;
-    if (launch_k(gradient_kernel, dim3(L.ngrad[n]), dim3(256), 0, cs, ga) != cudaSuccess) return CP_ECUDA;
-    launches += 2;
+    ngrad[n] = (int)ceil_div(s->dims[n], rpc);
+    ++launches;
+    return launch_k(gradient_kernel, dim3(ngrad[n]), dim3(256), 0, cs, ga) == cudaSuccess;
+  };
+  if (L.tree) {
+    // all N MTTKRPs with the same factors through the dimension tree: 2 more passes over Z
+    // (the Y_L pass and the mode-2 pass of Z viewed as I0 x I1 x J), as in cp_als_sweep
+    const int rpc_d = 256 / R > 0 ? 256 / R : 1;
+    StreamPlan p1 = L.yl_plan;
+    p1.Z = Z;
+    for (int k = 0; k < N; ++k) p1.At[k] = w + L.At[k];
+    p1.yl = w + L.yl;
+    p1.edge = w + L.edge;
+    p1.segcnt = yl_inline ? reinterpret_cast<unsigned *>(w + L.segtab) : nullptr;
+    p1.part = nullptr;
+    if (launch_stream(p1, cs) != cudaSuccess) return CP_ECUDA;
+    ++launches;
+    YLGeom yg;
+    yg.R = R;
+    yg.Gc = p1.Gc;
+    yg.RB = p1.RB;
+    yg.Wmax = p1.Wmax;
+    yg.I0 = s->dims[0];
+    yg.I1 = s->dims[1];
+    yg.Q = p1.Q;
+    yg.Qn = p1.Qn;
+    yg.yl = w + L.yl;
+    yg.edge = w + L.edge;
+    double *mb = w + L.mbuf;
+    if (!yl_inline) {
+      if (launch_yl_fixup(yg, cs) != cudaSuccess) return CP_ECUDA;
+      ++launches;
+    }
+    if (launch_ymm0(yg, A[1], w + L.m0part, cs) != cudaSuccess) return CP_ECUDA;
+    ++launches;
+    {
+      ReduceGeom g0;
+      memset(&g0, 0, sizeof(g0));
+      g0.R = R;
+      g0.Gc = ymm0_ranges(R, s->dims[1]);
+      g0.RB = 1;
+      g0.slots = 1;
+      g0.mode0 = 1;
+      g0.I1 = s->dims[0];
+      g0.In_rows = s->dims[0];
+      g0.part = w + L.m0part;
+      int rpc0, sp0;
+      ymm0_solve_blocking(R, s->dims[1], &rpc0, &sp0);
+      if (!grad_mode(0, g0, rpc0, sp0)) return CP_ECUDA;
+    }
+    GammaJob nojob;
+    memset(&nojob, 0, sizeof(nojob));
+    if (launch_ymm1(yg, A[0], mb, nojob, cs) != cudaSuccess) return CP_ECUDA;
+    ++launches;
+    if (!grad_mode(1, direct_geom(mb, s->dims[1], R), rpc_d, 1)) return CP_ECUDA;
+    StreamPlan p2 = L.p2_plan;
+    p2.Z = Z;
+    p2.At[0] = w + L.At[0];
+    p2.At[1] = w + L.At[1];
+    p2.At[2] = nullptr;
+    p2.part = w + L.part;
+    if (launch_stream(p2, cs) != cudaSuccess) return CP_ECUDA;
+    ++launches;
+    if (N == 3) {
+      if (!grad_mode(2, reduce_geom(p2), L.rpc2, L.sp2)) return CP_ECUDA;
+    } else {
+      if (launch_k(reduce_mttkrp_kernel, dim3(L.nyr), dim3(256), 0, cs, reduce_geom(p2), L.rpc2, L.sp2,
+                   w + L.yr) != cudaSuccess)
+        return CP_ECUDA;
+      ++launches;
+      for (int m = 2; m < N; ++m) {
+        YRArgs ya;
+        memset(&ya, 0, sizeof(ya));
+        ya.N = N;
+        ya.R = R;
+        ya.RS = R + (R & 1);
+        ya.mode = m;
+        for (int k = 0; k < N; ++k) {
+          ya.dims[k] = s->dims[k];
+          ya.At[k] = w + L.At[k];
+        }
+        ya.YR = w + L.yr;
+        ya.M = mb;
+        if (launch_yr(ya, cs) != cudaSuccess) return CP_ECUDA;
+        ++launches;
+        if (!grad_mode(m, direct_geom(mb, s->dims[m], R), rpc_d, 1)) return CP_ECUDA;
+      }
+    }
+  } else {
+    for (int n = 0; n < N; ++n) {
+      StreamPlan p = L.plans[n];
+      p.Z = Z;
+      for (int k = 0; k < N; ++k) p.At[k] = w + L.At[k];
+      p.part = w + L.part;
+      if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
+      ++launches;
+      if (!grad_mode(n, reduce_geom(p), L.rpc[n], L.sp[n])) return CP_ECUDA;
+    }
   }
   FitFinalArgs fa;
   memset(&fa, 0, sizeof(fa));
   fa.N = N;
   fa.nresid = rp.Gc * rp.RB;
   fa.gstride = L.grad_max;
-  for (int n = 0; n < N; ++n) fa.ngrad[n] = L.ngrad[n];
+  for (int n = 0; n < N; ++n) fa.ngrad[n] = ngrad[n];
   fa.resid = rp.part;
   fa.gpart = w + L.gradp;
   fa.normZ2 = normZ2;
