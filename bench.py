@@ -351,6 +351,21 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
     rows["restriction_mode0"] = {"ms": t, "TFLOPs": flops / t / 1e9, "J": J,
                                  "alg_GBps": 8.0 * (P + P * J / dims[0]) / t / 1e6}
     del X
+    # the same sweep with the DFMA streaming consumers (CP_STREAM_MMA=0: FP64 tensor cores only in
+    # the mode products, as BASELINE.json's north star first proposed)
+    os.environ["CP_STREAM_MMA"] = "0"
+    try:
+        ws2 = cp.Workspace(dims, R)
+        A2 = [torch.empty((R, a.shape[0]), dtype=torch.float64, device=dev).t().copy_(a) for a in A]
+        out2 = torch.empty(4, dtype=torch.float64, device=dev)
+        t = timed(lambda: cp.als_sweep(Zd, dims, A2, nz, out=out2, ws=ws2))
+        rows["sweep_dfma_consumers"] = {"ms": t}
+        t = timed(lambda: cp.mttkrp(Zd, dims, A, len(dims) - 1, M=M[-1], ws=ws2))
+        alg = 8.0 * (P + sum(dims[k] * R for k in range(len(dims) - 1)) + dims[-1] * R)
+        rows[f"mttkrp_mode{len(dims) - 1}_dfma_consumers"] = {"ms": t, "alg_GBps": alg / t / 1e6}
+        del ws2
+    finally:
+        del os.environ["CP_STREAM_MMA"]
     return rows
 
 
