@@ -106,9 +106,13 @@ class Workspace:
         self.R = int(R)
         self.nbytes = max(256, workspace_bytes(self.dims, self.R))
         self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+        self._fits = {(self.dims, self.R): True}
 
     def fits(self, dims, R):
-        return workspace_bytes(dims, R) <= self.nbytes
+        key = (tuple(int(d) for d in dims), int(R))
+        if key not in self._fits:
+            self._fits[key] = workspace_bytes(*key) <= self.nbytes
+        return self._fits[key]
 
 
 def _ws(ws, dims, R, device):

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "gamma_job.cuh"
 #include "mg_kernels.cuh"
@@ -42,10 +43,13 @@ const StreamEntry &stream_mma_entry(int nt, int mt, int op) {
 }
 
 static int device_sms() {
+  static int cached[64] = {0};
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev >= 0 && dev < 64 && cached[dev] > 0) return cached[dev];
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
     return 148;
+  if (dev >= 0 && dev < 64) cached[dev] = sms;
   return sms;
 }
 
@@ -59,34 +63,29 @@ bool pdl_enabled() {
   return on;
 }
 
-static int stream_occupancy(int R, int V, int op, int smem) {
-  const StreamEntry &e = stream_entry(R, V, op);
+// resident CTAs / SM of a streaming kernel at a dynamic smem size; cached per (kernel, smem)
+// (the CUDA queries cost microseconds, and every call plans its launches)
+static int kernel_occupancy(const void *kernel, int smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void *, int>, int>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto &c : cache)
+    if (c.first.first == kernel && c.first.second == smem) return c.second;
   int n = 0;
-  if (cudaFuncSetAttribute(e.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
-      cudaSuccess) {
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kStreamThreads, smem) != cudaSuccess) {
     cudaGetLastError();
     return 1;
   }
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, e.kernel, kStreamThreads, smem) != cudaSuccess) {
-    cudaGetLastError();
-    return 1;
-  }
-  return n > 0 ? n : 1;
+  n = n > 0 ? n : 1;
+  cache.push_back({{kernel, smem}, n});
+  return n;
 }
-
+static int stream_occupancy(int R, int V, int op, int smem) {
+  return kernel_occupancy(stream_entry(R, V, op).kernel, smem);
+}
 static int stream_mma_occupancy(int nt, int mt, int op, int smem) {
-  const StreamEntry &e = stream_mma_entry(nt, mt, op);
-  int n = 0;
-  if (cudaFuncSetAttribute(e.kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
-      cudaSuccess) {
-    cudaGetLastError();
-    return 1;
-  }
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, e.kernel, kStreamThreads, smem) != cudaSuccess) {
-    cudaGetLastError();
-    return 1;
-  }
-  return n > 0 ? n : 1;
+  return kernel_occupancy(stream_mma_entry(nt, mt, op).kernel, smem);
 }
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -293,6 +292,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   }
   p.nstages = nst;
   p.dbg = env_int("CP_STREAM_DBG", 0);
+  p.keep_q = 0;
   p.smem_bytes = (nst * stage_doubles + p.red_doubles + p.gjsm + 32) * 8 + nst * 88 + 64;
   if (p.smem_bytes > 200 * 1024) return false;
   const int occ = p.mma ? stream_mma_occupancy(p.nt, p.mt, op, p.smem_bytes)
@@ -339,7 +339,17 @@ static double stream_alg_bytes(const StreamPlan &p) {
   return 8.0 * (P + fac + out);
 }
 
-cudaError_t launch_stream(const StreamPlan &p, cudaStream_t st) {
+cudaError_t launch_stream(const StreamPlan &p0, cudaStream_t st) {
+  StreamPlan p = p0;
+  {
+    // L2 residency across passes (DESIGN 6.8): for a tensor well beyond L2, the first
+    // CP_L2KEEP_MB MiB of Z (default 40) are fetched evict_last and the rest evict_first, so
+    // consecutive passes over the same Z re-read that slice from L2
+    static const int64_t keep_mb = env_int("CP_L2KEEP_MB", 40);
+    double P = 1.0;
+    for (int k = 0; k < p.N; ++k) P *= (double)p.dims[k];
+    if (keep_mb > 0 && p.V >= 2 && 8.0 * P >= 96.0 * (1 << 20)) p.keep_q = (keep_mb << 20) / (8 * p.I1);
+  }
   const StreamEntry &e = p.mma ? stream_mma_entry(p.nt, p.mt, p.op) : stream_entry(p.R, p.V, p.op);
   ++g_launches;
   const bool prof = g_prof_on && g_prof_n < kProfMax;
@@ -590,7 +600,9 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     pa.zero = reinterpret_cast<unsigned *>(w + L.segtab);
     pa.nzero = (int)(s->dims[1] * L.yl_plan.RB);
   }
-  if (launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
+  // experiments only: CP_SWEEP_SKIP bitmask drops launches (timing of the rest; results wrong)
+  const int skip = env_int("CP_SWEEP_SKIP", 0);
+  if (!(skip & 1) && launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
   int launches = 1;
   double *gp[2] = {w + L.gpart0, w + L.gpart1};
   int grid_of[CP_MAX_N] = {0};
@@ -639,6 +651,7 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
       fa.out = out;
     }
     ++launches;
+    if (skip & (4 << n)) return true;
     return launch_solve(sa, grid_of[n], cs) == cudaSuccess;
   };
   const int RS = R + (R & 1);
@@ -684,7 +697,7 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     // Gamma^(0) (Grams of the old factors only) rides in the Y_L pass's idle weight warp
     const bool job0 = jobs && p1.mma && p1.direct_w;
     if (job0) p1.gj = gamma_job(0);
-    if (launch_stream(p1, cs) != cudaSuccess) return CP_ECUDA;
+    if (!(skip & 128) && launch_stream(p1, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     YLGeom yg;
     yg.R = R;
@@ -703,7 +716,7 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
       ++launches;
     }
     // mode 0: M0 = sum_{i1} Y_L(:, i1, :) * A^(1)(i1, :)   (A^(2..) old: Gauss-Seidel order)
-    if (launch_ymm0(yg, A[1], w + L.m0part, cs) != cudaSuccess) return CP_ECUDA;
+    if (!(skip & 2) && launch_ymm0(yg, A[1], w + L.m0part, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     {
       // the mode-0 solve sums the ymm0 range partials (mode-0 partial layout, fixed order)
@@ -725,7 +738,7 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     GammaJob gj1;
     memset(&gj1, 0, sizeof(gj1));
     if (jobs) gj1 = gamma_job(1);
-    if (launch_ymm1(yg, A[0], mb, gj1, cs) != cudaSuccess) return CP_ECUDA;
+    if (!(skip & 64) && launch_ymm1(yg, A[0], mb, gj1, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     if (!solve_mode(1, direct_geom(mb, s->dims[1], R), rpc_d, 1, jobs ? w + L.linv + (size_t)RR : nullptr))
       return CP_ECUDA;
@@ -739,7 +752,7 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     // Gamma^(2) rides in the pass's idle weight warp
     const bool job2 = jobs && p2.mma && p2.direct_w;
     if (job2) p2.gj = gamma_job(2);
-    if (launch_stream(p2, cs) != cudaSuccess) return CP_ECUDA;
+    if (!(skip & 256) && launch_stream(p2, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     if (N == 3) {
       if (!solve_mode(2, reduce_geom(p2), L.rpc2, L.sp2, job2 ? w + L.linv + (size_t)2 * RR : nullptr))
@@ -834,7 +847,9 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
     pa.zero = reinterpret_cast<unsigned *>(w + L.segtab);
     pa.nzero = (int)(s->dims[1] * L.yl_plan.RB);
   }
-  if (launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
+  // experiments only: CP_SWEEP_SKIP bitmask drops launches (timing of the rest; results wrong)
+  const int skip = env_int("CP_SWEEP_SKIP", 0);
+  if (!(skip & 1) && launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
   int launches = 1;
   // residual pass 1/2 ||Z - [[A]]||^2 (eq:CPfunctional): one partial per CTA
   StreamPlan rp = L.resid;
@@ -876,7 +891,7 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
     p1.edge = w + L.edge;
     p1.segcnt = yl_inline ? reinterpret_cast<unsigned *>(w + L.segtab) : nullptr;
     p1.part = nullptr;
-    if (launch_stream(p1, cs) != cudaSuccess) return CP_ECUDA;
+    if (!(skip & 128) && launch_stream(p1, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     YLGeom yg;
     yg.R = R;
@@ -894,7 +909,7 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
       if (launch_yl_fixup(yg, cs) != cudaSuccess) return CP_ECUDA;
       ++launches;
     }
-    if (launch_ymm0(yg, A[1], w + L.m0part, cs) != cudaSuccess) return CP_ECUDA;
+    if (!(skip & 2) && launch_ymm0(yg, A[1], w + L.m0part, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     {
       ReduceGeom g0;

@@ -75,6 +75,8 @@ struct StreamPlan {
   int srows;        // the producer also stages the slow digits' factor rows (kMaxDigits per stage)
   GammaJob gj;      // optional side job for the idle weight warp of CTA 0 (MMA kernel, direct_w)
   int gjsm;         // shared-memory doubles reserved for it
+  int64_t keep_q;   // L2 residency across passes: Z columns q < keep_q are fetched with an
+                    // evict_last policy, the rest evict_first (0: no hints).  See DESIGN 6.8.
   int dbg;          // experiments only (env CP_STREAM_DBG): 1 = consumers skip the FMAs, 2 = weight warp skips forming
 };
 
@@ -183,6 +185,25 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
           smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// The same copy with an L2 eviction-priority policy (createpolicy; evict_last / evict_first).
+__device__ __forceinline__ void bulk_g2s_hint(void *dst_smem, const void *src_gmem, uint32_t bytes,
+                                              uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 // Opaque copy of a value: address arithmetic derived from it inside a rarely taken branch
 // (the per-segment flushes of stream_kernel) cannot be hoisted out of the streaming loop,

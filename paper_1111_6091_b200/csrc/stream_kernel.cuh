@@ -117,6 +117,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
 #ifdef CP_STREAM_TIMING
   long long tm_wait = 0, tm_n = 0, tm0 = clock64();
 #endif
+  const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
   int stage = 0;
   uint32_t eph = 1;
   int64_t v = v0;
@@ -162,12 +163,23 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       // Z columns: q advances by qsd[0] per column within a stage (digit 0 only).  Strided
       // columns are issued by all 32 lanes (one bulk copy per column).
       if (p.RB == 1 && p.qsd[0] == 1 && p.zcs == 0) {
-        if (lane == 0) bulk_g2s(zs, p.Z + q0 * p.I1, (uint32_t)(ncols * Wb * 8), &sm.full[stage]);
+        if (lane == 0) {
+          if (p.keep_q > 0)
+            bulk_g2s_hint(zs, p.Z + q0 * p.I1, (uint32_t)(ncols * Wb * 8), &sm.full[stage],
+                          q0 < p.keep_q ? pol_keep : pol_stream);
+          else
+            bulk_g2s(zs, p.Z + q0 * p.I1, (uint32_t)(ncols * Wb * 8), &sm.full[stage]);
+        }
       } else {
         const int zstride = p.zcs ? p.zcs : Wb;
-        for (int col = lane; col < ncols; col += 32)
-          bulk_g2s(zs + (size_t)col * zstride, p.Z + (q0 + col * p.qsd[0]) * p.I1 + row0,
-                   (uint32_t)(Wb * 8), &sm.full[stage]);
+        for (int col = lane; col < ncols; col += 32) {
+          const int64_t q = q0 + col * p.qsd[0];
+          if (p.keep_q > 0)
+            bulk_g2s_hint(zs + (size_t)col * zstride, p.Z + q * p.I1 + row0, (uint32_t)(Wb * 8), &sm.full[stage],
+                          q < p.keep_q ? pol_keep : pol_stream);
+          else
+            bulk_g2s(zs + (size_t)col * zstride, p.Z + q * p.I1 + row0, (uint32_t)(Wb * 8), &sm.full[stage]);
+        }
       }
       if (has_f0) {
         if (p.ars == p.RS) {
