@@ -715,7 +715,46 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
       if (launch_yl_fixup(yg, cs) != cudaSuccess) return CP_ECUDA;
       ++launches;
     }
+    const bool ylsolve = env_int("CP_YLSOLVE", 1) != 0;
+    if (ylsolve) {
+      // modes 0 and 1: M rows from Y_L, Gamma, Cholesky and the solves in one kernel each
+      // (ylsolve.cu); Gamma^(0) from the Y_L pass's job when it ran, else factored in-block
+      YLSolveArgs ya;
+      memset(&ya, 0, sizeof(ya));
+      ya.N = N;
+      ya.R = R;
+      ya.RSo = RS;
+      ya.I0 = s->dims[0];
+      ya.I1 = s->dims[1];
+      ya.yl = w + L.yl;
+      ya.pg = pg;
+      ya.Ups = w + L.Ups;
+      ya.status = w + L.status;
+      for (int n = 0; n < 2; ++n) {
+        ya.mode = n;
+        ya.In = s->dims[n];
+        ya.RS = RS;
+        ya.Bfac = (n == 0) ? w + L.At[1] : A[0];
+        ya.gin = gp[0];
+        ya.nin = grid_of[0];
+        ya.linv = (n == 0 && job0) ? w + L.linv : nullptr;
+        // mode 1 sums the Gram of A^(0)_new from mode 0's cluster partials (gin) and reads
+        // Upsilon^(k >= 2) as totals (written by job 0 or by the mode-0 kernel)
+        ya.total = nullptr;
+        ya.ticket = reinterpret_cast<unsigned *>(w + L.status + kTicketSlot2);
+        ya.ups_total = (n == 0) ? 0 : (((1 << N) - 1) & ~2);
+        ya.F = (F != nullptr) ? F[n] : nullptr;
+        ya.A = A[n];
+        ya.At = w + L.At[n];
+        ya.gcur = gp[n & 1];
+        ya.dotF = w + L.dotF + (size_t)n * L.gp_max;
+        grid_of[n] = ylsolve_clusters(s->dims[n]);
+        if (launch_ylsolve(ya, cs) != cudaSuccess) return CP_ECUDA;
+        launches += 1;
+      }
+    }
     // mode 0: M0 = sum_{i1} Y_L(:, i1, :) * A^(1)(i1, :)   (A^(2..) old: Gauss-Seidel order)
+    if (!ylsolve) {
     if (!(skip & 2) && launch_ymm0(yg, A[1], w + L.m0part, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     {
@@ -742,6 +781,7 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
     ++launches;
     if (!solve_mode(1, direct_geom(mb, s->dims[1], R), rpc_d, 1, jobs ? w + L.linv + (size_t)RR : nullptr))
       return CP_ECUDA;
+    }  // !ylsolve
     // pass 2: modes >= 2 from Z x I0 x I1 contracted with the new A^(0), A^(1)
     StreamPlan p2 = L.p2_plan;
     p2.Z = Z;

@@ -25,7 +25,9 @@ __device__ __forceinline__ double gj_sum(const double *p, int64_t stride, int n)
 #pragma unroll
     for (int j = 0; j < 8; ++j) s[j] += p[(int64_t)(c + j) * stride];
   }
-  for (int j = 0; c + j < n; ++j) s[j] += p[(int64_t)(c + j) * stride];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (c + j < n) s[j] += p[(int64_t)(c + j) * stride];
   return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 

@@ -5,6 +5,9 @@
 // global read is issued in independent batches, and the R x R algebra runs in registers of
 // one warp (R is a template parameter).
 #include "small_kernels.cuh"
+#ifdef CP_SOLVE_TIMING
+#include <cstdio>
+#endif
 
 namespace cpk {
 
@@ -16,7 +19,9 @@ __device__ __forceinline__ double sum_strided(const double *p, int64_t stride, i
 #pragma unroll
     for (int j = 0; j < 8; ++j) s[j] += p[(int64_t)(c + j) * stride];
   }
-  for (int j = 0; c + j < n; ++j) s[j] += p[(int64_t)(c + j) * stride];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (c + j < n) s[j] += p[(int64_t)(c + j) * stride];
   return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
@@ -95,6 +100,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
     a.status[0] = 0.0;
     a.status[1] = -1.0;
     *reinterpret_cast<unsigned *>(a.status + kTicketSlot) = 0u;  // solve completion ticket
+    *reinterpret_cast<unsigned *>(a.status + kTicketSlot2) = 0u;  // ylsolve ticket
   }
   if (blockIdx.x == 0 && a.zero != nullptr)
     for (int i = tid; i < a.nzero; i += blockDim.x) a.zero[i] = 0u;
@@ -178,9 +184,24 @@ __global__ void __launch_bounds__(256) finalize_sweep_kernel(const FinalizeArgs 
 // row of A^(n) is then x = L^{-T} (L^{-1} (m + f)) as two small triangular mat-vecs.  With
 // a.fin_on (the sweep's last solve) the last block to finish also runs finalize_body
 // (completion ticket; every sum keeps its fixed order, so results stay bitwise reproducible).
+#ifdef CP_SOLVE_TIMING
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SOLVE_T(k) if (threadIdx.x == 0) tstamp[k] = gtimer();
+#else
+#define SOLVE_T(k)
+#endif
 template <int R>
 __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
+#ifdef CP_SOLVE_TIMING
+  unsigned long long tstamp[10] = {0};
+#endif
+  SOLVE_T(0);
   griddep();
+  SOLVE_T(1);
   constexpr int RR = R * R;
   constexpr int LS = R + 1;  // smem row stride of the R x R matrices
   __shared__ double sL[R * LS];    // Gamma, then L (lower)
@@ -207,9 +228,11 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
         if (blockIdx.x == 0) a.Ups[(int64_t)a.prev_mode * RR + e] = s;
       }
     }
+    SOLVE_T(2);
     // phase A (independent of Gamma): M rows from the stream partials
     gather_rows(a.rg, i0, nrows, R, a.sp, sM, scratch);
     __syncthreads();
+    SOLVE_T(3);
     if (a.linv == nullptr) {
       // Gamma^(n) = *_{k != n} Upsilon^(k)   (eq:Gamma).  Upsilon^(k): k > n from the prep
       // partials (factor not yet updated in this sweep), k = n-1 from the previous solve's
@@ -237,6 +260,7 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
     }
     if (tid == 0) sfail = 0;
     __syncthreads();
+    SOLVE_T(4);
     if (a.linv != nullptr) {
       // (factored by the Gamma job)
     } else if (warp == 0 && (a.dbg & 1)) {
@@ -288,6 +312,7 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
       }
     }
     __syncthreads();
+    SOLVE_T(5);
     if (sfail) {
       if (blockIdx.x == 0 && tid == 0) {
         a.status[0] = (double)CP_ENOTSPD;
@@ -314,9 +339,11 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
         dm = fma(sM[e], x, dm);
         if (a.F != nullptr) df = fma(a.F[i + In * r], x, df);
       }
+      SOLVE_T(6);
       // partial Gram of the new rows, and the CTA's <M,A>, <F,A> (fixed order)
       double dms = dm, dfs = df, unused = 0.0;
       block_sum3_256(dms, dfs, unused, scratch);
+      SOLVE_T(7);
       for (int e = tid; e < RR; e += blockDim.x) {
         const int r = e % R, s = e / R;
         double gg = 0.0;
@@ -340,6 +367,13 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
       if (tid == 0) *a.ticket = 0u;
     }
   }
+  SOLVE_T(8);
+#ifdef CP_SOLVE_TIMING
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    printf("solve mode %d blk %d: griddep %llu | pre %llu gather %llu gamma %llu chol %llu apply %llu gram/dot %llu tail %llu\n",
+           a.mode, blockIdx.x, tstamp[1] - tstamp[0], tstamp[2] - tstamp[1], tstamp[3] - tstamp[2], tstamp[4] - tstamp[3],
+           tstamp[5] - tstamp[4], tstamp[6] - tstamp[5], tstamp[7] - tstamp[6], tstamp[8] - tstamp[7]);
+#endif
 }
 
 // ---------------------------------------------------------------- gradient (cp_fit)

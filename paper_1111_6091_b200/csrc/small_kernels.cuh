@@ -114,6 +114,7 @@ struct FinalizeArgs {
 
 // status area (8 doubles): [0] status, [1] failed mode, [kTicketSlot] completion ticket (u32)
 constexpr int kTicketSlot = 4;
+constexpr int kTicketSlot2 = 5;  // ylsolve: last-cluster ticket (zeroed by prep)
 
 struct SolveArgs {
   int N, R, mode, prev_mode, nprev, rpc, sp;
@@ -196,6 +197,32 @@ struct YRArgs {
   double *M;
 };
 cudaError_t launch_yr(const YRArgs &a, cudaStream_t st);
+
+// ylsolve.cu: mode 0 / mode 1 of the dimension-tree sweep -- M rows from Y_L, Gamma, Cholesky
+// and the row solves in one kernel (blocks of 4 rows, 8-CTA clusters).
+struct YLSolveArgs {
+  int N, R, mode;          // mode 0 or 1
+  int RS;                  // mode 0: row stride of Bfac (At^(1)); unused for mode 1
+  int RSo;                 // row stride of the At output
+  int64_t I0, I1, In;      // Y_L dims; rows of this mode
+  const double *yl;        // Y_L [i1][r][i0]
+  const double *Bfac;      // mode 0: At^(1) (row-major, previous sweep); mode 1: A^(0)_new (column-major)
+  PrepGrams pg;            // Grams of the factors not updated yet (prep partials)
+  const double *gin;       // mode 1: per-cluster partial Grams of A^(0)_new
+  int nin;
+  const double *linv;      // optional L^{-1} of Gamma^(mode) from a Gamma job (else factored in-block)
+  int ups_total;           // bit k: Upsilon^(k) is read as the total Ups[k] (else summed from partials)
+  double *total;           // optional: the last cluster writes the Gram total of the new factor here
+  unsigned *ticket;        // (zero; reset by the last cluster)
+  const double *F;         // F^(mode) or null
+  double *A, *At;          // outputs: column-major factor, row-major copy
+  double *Ups;             // Gram totals (block 0 writes the ones it sums)
+  double *gcur;            // per-cluster partial Grams of the new rows
+  double *dotF;            // per-cluster <F, A>
+  double *status;
+};
+int ylsolve_clusters(int64_t In);  // grid = 8 x this
+cudaError_t launch_ylsolve(const YLSolveArgs &a, cudaStream_t st);
 cudaError_t launch_prep(const PrepArgs &a, cudaStream_t st);
 
 // Fill the prep block offsets for a shape (blocks of kPrepRows rows per mode).
