@@ -351,6 +351,20 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
     rows["restriction_mode0"] = {"ms": t, "TFLOPs": flops / t / 1e9, "J": J,
                                  "alg_GBps": 8.0 * (P + P * J / dims[0]) / t / 1e6}
     del X
+    # NEXT-3: the same restriction with the structured BAMG operator (cp_restrict_structured:
+    # 3-tap gather + bidiagonal substitution per fiber; HBM-bound), every mode
+    for n in range(len(dims)):
+        wl, wr = cpsynth.transfer_weights(dims[n], seed=512 + n)
+        wld, wrd = torch.from_numpy(wl).to(dev), torch.from_numpy(wr).to(dev)
+        nd = list(dims)
+        nd[n] = (dims[n] + 1) // 2
+        X = torch.empty(tuple(reversed(nd)), dtype=torch.float64, device=dev)
+        rws = torch.empty(32 * dims[n] + 64, dtype=torch.uint8, device=dev)
+        t = timed(lambda: cp.restrict_structured(Zd, dims, n, wld, wrd, X=X, ws=rws), n=10)
+        alg = 8.0 * (P + P * nd[n] / dims[n])
+        rows[f"restriction_structured_mode{n}"] = {"ms": t, "alg_GBps": alg / t / 1e6,
+                                                   "frac_hbm": alg / t / 1e6 / (json.load(open(PEAKS_PATH)).get("hbm_gbs", FALLBACK_HBM) if os.path.exists(PEAKS_PATH) else FALLBACK_HBM)}
+        del X
     # the same sweep with the DFMA streaming consumers (CP_STREAM_MMA=0: FP64 tensor cores only in
     # the mode products, as BASELINE.json's north star first proposed)
     os.environ["CP_STREAM_MMA"] = "0"

@@ -108,6 +108,14 @@ def random_problem(dims, R, seed, scale_A=1.0):
     return Z, A
 
 
+def transfer_weights(I, seed):
+    """F-row interpolation weights (wl, wr) in [0.2, 0.8] -- the range of the least-squares
+    weights of the paper's smooth problems (linear vectors give exactly 1/2) -- for
+    the structured restriction (cp_restrict_structured / oracle.mg.restrict_structured)."""
+    rng = np.random.default_rng(np.random.SeedSequence([SEED_BASE, 3000, seed]))
+    return rng.uniform(0.2, 0.8, I), rng.uniform(0.2, 0.8, I)
+
+
 def random_matrix(rows, cols, seed):
     rng = np.random.default_rng(np.random.SeedSequence([SEED_BASE, 2000, seed]))
     return np.asfortranarray(rng.standard_normal((rows, cols)))

@@ -8,6 +8,8 @@
  *                    FAS right-hand side F) and the functional f  eq:CPfunctional P:38-42
  *   cp_mode_product  X = Z x_n U (restriction U = Phat^T,      P:74-78, eq:ctensor_transformed
  *                    interpolation on a 2-way factor matrix)
+ *   cp_restrict_structured  X = Z x_n Phat^T for the BAMG
+ *                    transfer operator (bidiagonal factor, O(P))
  *   cp_fit           f (direct), g and ||G^(n)||^2              eq:gradConv P:454-456
  *   cp_norm2         ||Z||^2
  *
@@ -117,6 +119,31 @@ size_t cp_mode_product_workspace_bytes(int32_t N, const int64_t *dims, int32_t m
 int cp_mode_product(int32_t N, const int64_t *dims, const double *Z, int32_t mode,
                     const double *U, int64_t J, double *X, void *ws, size_t ws_bytes,
                     cp_stream_t stream);
+
+/* Restriction by the structured transfer operator of the geometric C/F splitting (SURVEY
+ * 8(f) NEXT-3):  X = Z x_mode Phat^T,  Phat = P L^{-T},  B = P^T P = L L^T   (P:164-189,
+ * eq:ctensor_transformed P:176-180; Phat^T Phat = I).
+ *   P (I x Ic, I = dims[mode], Ic = ceil(I/2)) is the interpolation of P:222-247: the C points
+ *   are the even 0-based fine indices (the paper's odd points), P(2j, j) = 1 (injection); the
+ *   F point i = 2j+1 interpolates from its coarse neighbours,
+ *       P(i, j) = wl[i],   P(i, j+1) = wr[i]   (wr is ignored when i = I-1: one-sided right end)
+ *   -- the weights of Algorithm 1's weighted least-squares fit (eq:LSQinterp).  Entries of wl,
+ *   wr at C points are ignored.
+ *   Because P has at most two nonzeros per row, B is tridiagonal and L bidiagonal: the library
+ *   factors B on the device and applies Phat^T = L^{-1} P^T along mode `mode` as a 3-point
+ *   gather and a bidiagonal forward substitution per fiber -- O(P) flops and one pass over Z
+ *   (HBM-bound), instead of the 2 * Ic * P flops of cp_mode_product with a dense Phat^T.  The
+ *   result equals cp_mode_product(N, dims, Z, mode, Phat^T, Ic, ...) up to rounding.
+ *   wl, wr  device, I doubles each
+ *   X       device, the tensor with dims[mode] replaced by Ic (same layout as Z)
+ *   ws      device workspace of cp_restrict_workspace_bytes() bytes (the factor of B)
+ *   Errors: CP_EINVAL (null pointer, N out of [1, CP_MAX_N], mode out of range), CP_EDIM,
+ *   CP_EWORKSPACE, CP_ECUDA.  B is SPD for any finite weights (every coarse point has its
+ *   injected C row), so there is no numeric failure mode. */
+size_t cp_restrict_workspace_bytes(int32_t N, const int64_t *dims, int32_t mode);
+int cp_restrict_structured(int32_t N, const int64_t *dims, const double *Z, int32_t mode,
+                           const double *wl, const double *wr, double *X, void *ws, size_t ws_bytes,
+                           cp_stream_t stream);
 
 /* Fit and stopping quantity at one iterate (eq:gradConv P:454-456):
  *   out  device, 2 + N doubles: f (direct, one residual pass over Z), g, ||G^(n)||^2 (n < N)

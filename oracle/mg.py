@@ -49,6 +49,29 @@ def interpolation_matrix(U_list, weights):
     return P
 
 
+def interpolation_from_weights(I, wl, wr):
+    """P (I x ceil(I/2)) of the geometric C/F splitting with given F-row weights:
+    P[2j, j] = 1; F point i = 2j+1: P[i, j] = wl[i], P[i, j+1] = wr[i] (one-sided at an even
+    right end, reading R17) -- the sparsity pattern interpolation_matrix() fills by LS."""
+    Ic = (I + 1) // 2
+    P = np.zeros((I, Ic))
+    for i in range(I):
+        if i % 2 == 0:
+            P[i, i // 2] = 1.0
+        else:
+            P[i, (i - 1) // 2] = wl[i]
+            if i + 1 < I:
+                P[i, (i + 1) // 2] = wr[i]
+    return P
+
+
+def restrict_structured(Z, dims, mode, wl, wr):
+    """X = Z x_mode Phat^T with Phat from P (interpolation_from_weights) by transfer(): the
+    definition of eq:ctensor_transformed, dense.  Returns (X, new dims)."""
+    Ph = transfer(interpolation_from_weights(int(dims[mode]), wl, wr))
+    return oracle.mode_product(Z, dims, mode, np.asfortranarray(Ph.T))
+
+
 def transfer(P):
     """B = P^T P = L L^T, Phat = P L^{-T}, R = Phat^T."""
     B = P.T @ P

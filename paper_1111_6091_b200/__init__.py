@@ -23,7 +23,7 @@ from ._lib import (CP_ECUDA, CP_EDIM, CP_EINVAL, CP_ENOTSPD, CP_EWORKSPACE, CP_M
                    CP_OK, CPError, lib, lib_path)
 
 __all__ = ["colmajor", "empty_factor", "Workspace", "norm2", "mttkrp", "als_sweep",
-           "mode_product", "fit", "workspace_bytes", "lib", "lib_path", "last_launch_count",
+           "mode_product", "restrict_structured", "fit", "workspace_bytes", "lib", "lib_path", "last_launch_count",
            "CPError", "CP_OK", "CP_EINVAL", "CP_EDIM", "CP_ENOTSPD", "CP_ECUDA", "CP_EWORKSPACE"]
 
 
@@ -202,6 +202,31 @@ def mode_product(Z, dims, mode, U, X=None, stream=None):
     _check(lib().cp_mode_product(ctypes.c_int32(len(dims)), d, _ptr(Z), ctypes.c_int32(mode),
                                  _ptr(U), ctypes.c_int64(J), _ptr(X), ctypes.c_void_p(),
                                  ctypes.c_size_t(0), _stream(stream)), "cp_mode_product")
+    return X, nd
+
+
+def restrict_structured(Z, dims, mode, wl, wr, X=None, ws=None, stream=None):
+    """X = Z x_mode Phat^T for the BAMG transfer operator of the geometric C/F splitting
+    (cp_restrict_structured): C points 2j injected, F point 2j+1
+    interpolated with weights wl[2j+1] (coarse j) and wr[2j+1] (coarse j+1); Phat = P L^{-T},
+    P^T P = L L^T.  wl, wr: float64 CUDA vectors of length dims[mode].  Returns (X, new dims)."""
+    _check_Z(Z, dims)
+    I = int(dims[mode])
+    for name, w in (("wl", wl), ("wr", wr)):
+        if w.dtype != torch.float64 or not w.is_cuda or w.numel() != I or not w.is_contiguous():
+            raise ValueError(f"{name}: expected a contiguous float64 CUDA vector of length {I}")
+    nd = list(dims)
+    nd[mode] = (I + 1) // 2
+    if X is None:
+        X = torch.empty(tuple(reversed(nd)), dtype=torch.float64, device=Z.device)
+    _check_Z(X, nd)
+    d = (ctypes.c_int64 * len(dims))(*[int(x) for x in dims])
+    need = int(lib().cp_restrict_workspace_bytes(ctypes.c_int32(len(dims)), d, ctypes.c_int32(mode)))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 32), dtype=torch.uint8, device=Z.device)
+    _check(lib().cp_restrict_structured(ctypes.c_int32(len(dims)), d, _ptr(Z), ctypes.c_int32(mode),
+                                        _ptr(wl), _ptr(wr), _ptr(X), _ptr(ws), ctypes.c_size_t(ws.numel()),
+                                        _stream(stream)), "cp_restrict_structured")
     return X, nd
 
 

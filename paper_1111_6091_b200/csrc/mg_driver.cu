@@ -17,6 +17,7 @@
 // the transfer operators (O(I * I_c) per mode) and reads g once per cycle.
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -28,6 +29,11 @@ namespace {
 
 constexpr int kMaxTest = 8;
 constexpr int kMaxLevels = 40;
+
+static bool structured_restriction() {
+  const char *e = getenv("CP_MG_STRUCTURED");
+  return !(e && *e && atoi(e) == 0);
+}
 
 struct Arena {
   char *base = nullptr;
@@ -54,6 +60,7 @@ struct Level {
          *tmp[CP_MAX_N] = {}, *prev[CP_MAX_N] = {};
   double *T[kMaxTest][CP_MAX_N] = {};
   double *Ph[CP_MAX_N] = {}, *Rt[CP_MAX_N] = {};
+  double *wl[CP_MAX_N] = {}, *wr[CP_MAX_N] = {};  // F-row weights of P (cp_restrict_structured)
 };
 
 struct MG {
@@ -119,6 +126,10 @@ struct MG {
         if (v.has_next && v.coarsen[n]) {
           v.Ph[n] = a.take((size_t)v.s.dims[n] * v.Ic[n]);
           v.Rt[n] = a.take((size_t)v.s.dims[n] * v.Ic[n]);
+          v.wl[n] = a.take((size_t)v.s.dims[n]);
+          v.wr[n] = a.take((size_t)v.s.dims[n]);
+          const size_t rw = cp_restrict_workspace_bytes(N, v.s.dims, n);
+          if (rw > wsb) wsb = rw;
         }
       }
       const size_t w = cp_workspace_bytes(&v.s);
@@ -305,6 +316,8 @@ struct MG {
       }
       if (cudaMemcpyAsync(v.Ph[n], Ph.data(), Ph.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
           cudaMemcpyAsync(v.Rt[n], Rt.data(), Rt.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+          cudaMemcpyAsync(v.wl[n], w0.data(), (size_t)I * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+          cudaMemcpyAsync(v.wr[n], w1.data(), (size_t)I * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
           cudaStreamSynchronize(st) != cudaSuccess) {
         err = CP_ECUDA;
         return;
@@ -322,7 +335,12 @@ struct MG {
       if (!v.coarsen[n]) continue;
       --remaining;
       double *dst = (remaining == 0) ? nx.zbuf : scratch[ping];
-      ok(cp_mode_product(N, cur, src, n, v.Rt[n], v.Ic[n], dst, nullptr, 0, cst));
+      // Galerkin tensor by the structured operator (3-tap gather + bidiagonal
+      // substitution, HBM-bound); CP_MG_STRUCTURED=0: the dense product with Phat^T
+      if (structured_restriction())
+        ok(cp_restrict_structured(N, cur, src, n, v.wl[n], v.wr[n], dst, ws, ws_bytes, cst));
+      else
+        ok(cp_mode_product(N, cur, src, n, v.Rt[n], v.Ic[n], dst, nullptr, 0, cst));
       cur[n] = v.Ic[n];
       src = dst;
       ping ^= 1;
