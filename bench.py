@@ -55,6 +55,24 @@ def dist_env():
     return rank, world, local
 
 
+def max_over_ranks(ms, world, device):
+    """Max of a per-rank duration over all ranks (the timing rule: device time, max over ranks);
+    device = the process group's tensor device (cuda for nccl, cpu for gloo)."""
+    if world <= 1:
+        return float(ms)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_value(world, steps, t_max_ms):
+    """Whole-job throughput: units all ranks processed / the slowest rank's time (weak scaling:
+    every rank runs its own replica of the workload)."""
+    return world * steps / (t_max_ms / 1000.0)
+
+
 def metric_name(workload):
     _, dims, R, *_ = cpsynth.CONFIGS[workload]
     shape = "x".join(str(d) for d in dims)
@@ -250,12 +268,8 @@ def main():
     res = out.cpu().numpy()
     if res[2] != 0 or not math.isfinite(res[0]):
         raise SystemExit(f"sweep failed: status {res[2]} mode {res[3]} f {res[0]}")
-    t_max = ms
-    if world > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
-    value = world * args.steps / (t_max / 1000.0)
+    t_max = max_over_ranks(ms, world, dev)
+    value = job_value(world, args.steps, t_max)
 
     # ---- roofline of the dominant kernel (the Z-streaming MTTKRP kernel)
     peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
@@ -365,6 +379,21 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
         rows[f"restriction_structured_mode{n}"] = {"ms": t, "alg_GBps": alg / t / 1e6,
                                                    "frac_hbm": alg / t / 1e6 / (json.load(open(PEAKS_PATH)).get("hbm_gbs", FALLBACK_HBM) if os.path.exists(PEAKS_PATH) else FALLBACK_HBM)}
         del X
+    # 8(d): full multigrid solve time to a stated g tolerance -- BASELINE.json config c1
+    # (50^3, R = 3, C = 0.9: BAMG setup + FAS V-cycles to ||grad f|| <= 1e-9), ML and ML+FMG,
+    # beside the plain ALS solve to the same tolerance; seconds include the stopping tests
+    # (cp_mg_solve reports the fit time separately: the paper excludes it)
+    try:
+        import importlib.util
+        spec = importlib.util.spec_from_file_location("mg_bench", os.path.join(ROOT, "tools", "mg_bench.py"))
+        mgb = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mgb)
+        mgb.run("c1", tol=1e-9)  # warm-up
+        rows["mg_solve_c1"] = mgb.run("c1", tol=1e-9)
+        # and the paper's own dense problem (Table 4 context: s = 50, R = 2)
+        rows["mg_solve_dense50_R2"] = mgb.run("dense50", R=2, tol=1e-9)
+    except Exception as e:  # the row is informative; the sweep metric stands without it
+        rows["mg_solve_c1"] = {"error": repr(e)}
     # the same sweep with the DFMA streaming consumers (CP_STREAM_MMA=0: FP64 tensor cores only in
     # the mode products, as BASELINE.json's north star first proposed)
     os.environ["CP_STREAM_MMA"] = "0"

@@ -577,7 +577,24 @@ int cp_als_solve(const cp_shape *s, const double *Z, double *const *A, double to
   const size_t w = cp_workspace_bytes(s);
   if (w == 0) return CP_EINVAL;
   if (ws_bytes < w + 4096) return CP_EWORKSPACE;
+  // the legacy default stream cannot be captured: run the solve on a private blocking stream
+  // (implicitly ordered with the legacy stream) and graph-capture there
+  struct Own {
+    cudaStream_t s = nullptr;
+    cudaGraphExec_t g = nullptr;
+    ~Own() {
+      if (g) cudaGraphExecDestroy(g);
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    }
+  } own;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (st == nullptr && cudaStreamCreate(&own.s) == cudaSuccess) {
+    st = own.s;
+    stream = reinterpret_cast<cp_stream_t>(st);
+  }
   double *small = reinterpret_cast<double *>(static_cast<char *>(ws) + w);
   double *nz2 = small, *out = small + 8, *fitout = small + 16;
   const auto t0 = std::chrono::steady_clock::now();
@@ -589,9 +606,38 @@ int cp_als_solve(const cp_shape *s, const double *Z, double *const *A, double to
   std::vector<double> h(2 + s->N);
   double g = NAN;
   int it = 0, status = 1;
+  // The check_every sweeps (+ normalization) between two stopping tests are captured once into
+  // a CUDA graph and replayed: for small tensors the loop is launch-bound (~10 launches per
+  // sweep).  Same kernels in the same order -- results are bitwise those of the plain loop.
+  // Needs a capturable stream (not the legacy default stream); CP_ALS_GRAPH=0 disables.
+  cudaGraphExec_t &gexec = own.g;
+  {
+    const char *e = getenv("CP_ALS_GRAPH");
+    const bool want = !(e && *e && atoi(e) == 0) && st != nullptr && check_every > 1;
+    if (want) {
+      cudaGraph_t graph = nullptr;
+      bool okc = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      for (int k = 0; okc && k < check_every; ++k) {
+        okc = cp_als_sweep(s, Z, nz2, A, nullptr, out, ws, w, stream) == CP_OK &&
+              cp_normalize_sort(s, A, 0, nullptr, ws, w, stream) == CP_OK;
+      }
+      const cudaError_t ec = cudaStreamEndCapture(st, &graph);
+      if (okc && ec == cudaSuccess && graph != nullptr &&
+          cudaGraphInstantiate(&gexec, graph, 0) != cudaSuccess)
+        gexec = nullptr;
+      if (graph != nullptr) cudaGraphDestroy(graph);
+      cudaGetLastError();  // a failed capture falls back to the plain loop
+      if (!okc) gexec = nullptr;
+    }
+  }
   for (it = 1; it <= max_iters; ++it) {
-    if ((rc = cp_als_sweep(s, Z, nz2, A, nullptr, out, ws, w, stream))) return rc;
-    if ((rc = cp_normalize_sort(s, A, 0, nullptr, ws, w, stream))) return rc;
+    if (gexec != nullptr && it % check_every == 1 && it + check_every - 1 <= max_iters) {
+      if (cudaGraphLaunch(gexec, st) != cudaSuccess) return CP_ECUDA;
+      it += check_every - 1;  // the graph ran sweeps it .. it + check_every - 1
+    } else {
+      if ((rc = cp_als_sweep(s, Z, nz2, A, nullptr, out, ws, w, stream))) return rc;
+      if ((rc = cp_normalize_sort(s, A, 0, nullptr, ws, w, stream))) return rc;
+    }
     if (it % check_every == 0 || it == max_iters) {
       const auto tf = std::chrono::steady_clock::now();
       if ((rc = cp_fit(s, Z, nz2, A, nullptr, fitout, nullptr, ws, w, stream))) return rc;

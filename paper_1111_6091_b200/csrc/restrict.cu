@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) restrict_inner_kernel(const double *__res
                                                              int64_t S, int64_t nfib, const double *__restrict__ coef,
                                                              double *__restrict__ X) {
   using VT = typename vec_t<V>::T;
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  griddep();  // (every read of Z after the wait: Z may be the output of an earlier kernel)
   const int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;  // first fiber of the thread
   const int64_t o = f / S, s = f - (f / S) * S;
   const VT *z = reinterpret_cast<const VT *>(Z + o * I * S + s);
@@ -102,15 +102,9 @@ __global__ void __launch_bounds__(256) restrict_inner_kernel(const double *__res
     vec_t<V>::set(xprev, u, 0.0);
     vec_t<V>::set(z1, u, 0.0);
   }
-  // Z is an input of the call (not written by the coefficient kernel): the first two fine
-  // points are fetched before waiting for the coefficient table (PDL overlap)
-  z0 = z1;
-  if (f < nfib) {
-    z0 = __ldcs(z);
-    if (I > 1) z1 = __ldcs(z + Sv);
-  }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (f >= nfib) return;
+  z0 = __ldcs(z);
+  if (I > 1) z1 = __ldcs(z + Sv);
   auto step = [&](const double4 &c, const VT &zc, const VT &zf, int64_t j) {
     VT xv;
 #pragma unroll
@@ -153,7 +147,7 @@ constexpr int kR0Rows = 128, kR0Chunk = 32;
 __global__ void __launch_bounds__(kR0Rows) restrict_mode0_kernel(const double *__restrict__ Z, int64_t I, int64_t Ic,
                                                                  int64_t nfib, const double *__restrict__ coef,
                                                                  double *__restrict__ X) {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  griddep();  // (every read of Z after the wait: Z may be the output of an earlier kernel)
   __shared__ double tz[kR0Rows][kR0Chunk + 1];  // the chunk; outputs overwrite it in place
                                                  // (x_jj lands in column jj <= 2 jj, already read)
   const int t = threadIdx.x;
@@ -172,8 +166,6 @@ __global__ void __launch_bounds__(kR0Rows) restrict_mode0_kernel(const double *_
     }
   };
   load_chunk(0);
-  // (PDL) the first chunk of Z is in flight before waiting for the coefficient table
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   double zprev = 0.0, xprev = 0.0;
   for (int64_t c0 = 0; c0 < I; c0 += kR0Chunk) {
 #pragma unroll

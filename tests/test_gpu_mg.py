@@ -111,3 +111,21 @@ def test_normalize_sort_parity():
         Ao, _ = oracle.normalize_sort(dims, A, sort=sort)
         for a, b in zip(Ad, Ao):
             assert relerr(host_factor(a), b) <= 1e-14
+
+
+def test_als_solve_graph_replay_is_bitwise_the_plain_loop(monkeypatch):
+    """cp_als_solve replays the check_every sweeps between stopping tests as one CUDA graph;
+    the result must be bitwise that of the plain launch loop (same kernels, same order)."""
+    dims, R = (20, 18, 16), 3
+    Z, A0 = cpsynth.random_problem(dims, R, seed=21)
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("CP_ALS_GRAPH", mode)
+        Ad = [dev_factor(a) for a in A0]
+        rep = cp.als_solve(dev_tensor(Z), dims, Ad, tol=1e-8, max_iters=203, check_every=10)
+        res[mode] = (rep, [host_factor(a) for a in Ad])
+    (r1, A1), (r0, A0g) = res["1"], res["0"]
+    assert r1["iterations"] == r0["iterations"] and r1["status"] == r0["status"]
+    assert r1["g"] == r0["g"]
+    for a, b in zip(A1, A0g):
+        assert np.array_equal(a, b)

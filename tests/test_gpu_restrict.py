@@ -91,3 +91,20 @@ def test_restrict_rejects_bad_arguments():
     assert L.cp_restrict_structured(2, d, ctypes.c_void_p(Zd.data_ptr()), 2, ctypes.c_void_p(w.data_ptr()),
                                     ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(Zd.data_ptr()),
                                     ctypes.c_void_p(w.data_ptr()), 32, None) == cp.CP_EINVAL
+
+
+def test_restrict_chained_galerkin_all_modes():
+    """The multigrid driver's Galerkin tensor: restrictions of every mode chained on the stream
+    with no host synchronization in between (each call reads the previous call's output)."""
+    dims = (66, 40, 34)
+    Z, _ = cpsynth.random_problem(dims, 1, seed=13)
+    W = [cpsynth.transfer_weights(I, seed=70 + n) for n, I in enumerate(dims)]
+    Xd = torch.from_numpy(Z).cuda()
+    cur = list(dims)
+    for n in range(3):
+        Xd, cur = cp.restrict_structured(Xd, cur, n, torch.from_numpy(W[n][0]).cuda(), torch.from_numpy(W[n][1]).cuda())
+    Xo, curo = Z, list(dims)
+    for n in range(3):
+        Xo, curo = mg.restrict_structured(Xo, curo, n, *W[n])
+    assert list(cur) == list(curo)
+    assert relerr(Xd.cpu().numpy().reshape(-1), Xo.reshape(-1)) <= 1e-12

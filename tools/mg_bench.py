@@ -44,6 +44,10 @@ def run(name, R=None, tol=1e-10, max_als=10000):
                                                               "status", "seconds", "fit_seconds")}
     Ad = [dev(a) for a in A0]
     out["als"] = cp.als_solve(Zd, dims, Ad, tol=tol, max_iters=max_als, check_every=1)
+    # the same ALS with the stopping test every 10 sweeps: the 10 sweeps between tests replay as
+    # one CUDA graph (the loop is launch-bound at these sizes)
+    Ad = [dev(a) for a in A0]
+    out["als_check10_graph"] = cp.als_solve(Zd, dims, Ad, tol=tol, max_iters=max_als, check_every=10)
     return out
 
 
