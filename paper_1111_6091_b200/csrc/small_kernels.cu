@@ -121,9 +121,17 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
     for (int e = tid; e < RR; e += blockDim.x) {
       const int r = e % R, s = e / R;
       const double *ar = sA + r * kPrepRows, *as = sA + s * kPrepRows;
-      double g = 0.0;
-      for (int ii = 0; ii < n; ++ii) g = fma(ar[ii], as[ii], g);
-      a.gpre[(int64_t)blockIdx.x * RR + e] = g;
+      // 4 independent chains (the single 64-long fma chain dominated this kernel)
+      double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+      int ii = 0;
+      for (; ii + 3 < n; ii += 4) {
+        g0 = fma(ar[ii], as[ii], g0);
+        g1 = fma(ar[ii + 1], as[ii + 1], g1);
+        g2 = fma(ar[ii + 2], as[ii + 2], g2);
+        g3 = fma(ar[ii + 3], as[ii + 3], g3);
+      }
+      for (; ii < n; ++ii) g0 = fma(ar[ii], as[ii], g0);
+      a.gpre[(int64_t)blockIdx.x * RR + e] = (g0 + g1) + (g2 + g3);
     }
   }
 }
@@ -323,6 +331,7 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
       for (int e = tid; e < nrows * R; e += blockDim.x) {
         const int ii = e / R, r = e - (e / R) * R;
         double y = 0.0;
+#pragma unroll 4
         for (int k = 0; k <= r; ++k) y = fma(sLi[r * LS + k], sB[ii * R + k], y);
         scratch[e] = y;
       }
@@ -331,6 +340,7 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
       for (int e = tid; e < nrows * R; e += blockDim.x) {
         const int ii = e / R, r = e - (e / R) * R;
         double x = 0.0;
+#pragma unroll 4
         for (int k = r; k < R; ++k) x = fma(sLi[k * LS + r], scratch[ii * R + k], x);
         const int64_t i = i0 + ii;
         a.A[i + In * r] = x;
@@ -346,9 +356,14 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
       SOLVE_T(7);
       for (int e = tid; e < RR; e += blockDim.x) {
         const int r = e % R, s = e / R;
-        double gg = 0.0;
-        for (int ii = 0; ii < nrows; ++ii) gg = fma(sX[ii * R + r], sX[ii * R + s], gg);
-        a.gcur[(int64_t)blockIdx.x * RR + e] = gg;
+        double g0 = 0.0, g1 = 0.0;
+        int ii = 0;
+        for (; ii + 1 < nrows; ii += 2) {
+          g0 = fma(sX[ii * R + r], sX[ii * R + s], g0);
+          g1 = fma(sX[(ii + 1) * R + r], sX[(ii + 1) * R + s], g1);
+        }
+        if (ii < nrows) g0 = fma(sX[ii * R + r], sX[ii * R + s], g0);
+        a.gcur[(int64_t)blockIdx.x * RR + e] = g0 + g1;
       }
       if (tid == 0) {
         a.dotM[blockIdx.x] = dms;
