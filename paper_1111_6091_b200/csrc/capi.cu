@@ -58,9 +58,13 @@ static int env_int(const char *name, int dflt) {
   return (v && *v) ? atoi(v) : dflt;
 }
 
-bool pdl_enabled() {
-  static const bool on = env_int("CP_PDL", 1) != 0;
-  return on;
+// measured (tools/time_sweep.py, no profiling events): PDL on the 8-CTA-cluster ylsolve launches cost
+// c4a ~15 us per sweep (its CTAs, launched early, wait where the pass could run); default: stream +
+// small kernels
+constexpr int kPdlDefaultMask = (1 << kPdlStream) | (1 << kPdlSmall);
+bool pdl_enabled(int cls) {
+  static const int mask = env_int("CP_PDL", 1) != 0 ? env_int("CP_PDL_MASK", kPdlDefaultMask) : 0;
+  return (mask >> cls) & 1;
 }
 
 // resident CTAs / SM of a streaming kernel at a dynamic smem size; cached per (kernel, smem)

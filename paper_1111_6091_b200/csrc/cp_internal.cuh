@@ -123,7 +123,25 @@ __device__ __forceinline__ void griddep() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
-bool pdl_enabled();  // env CP_PDL (default 1)
+// PDL per launch class (env CP_PDL_MASK, bit c = class c; CP_PDL=0 clears all):
+//   kPdlStream: the Z-streaming kernels, kPdlCluster: ylsolve (8-CTA clusters), kPdlSmall: the rest
+enum { kPdlStream = 0, kPdlCluster = 1, kPdlSmall = 2 };
+bool pdl_enabled(int cls = kPdlSmall);
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kc(int cls, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled(cls) ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                      Args &&...args) {

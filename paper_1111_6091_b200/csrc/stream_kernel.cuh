@@ -634,7 +634,7 @@ cudaError_t launch_stream_t(const StreamPlan &p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  return launch_k(kern, dim3(p.Gc * p.RB), dim3(kStreamThreads), (size_t)p.smem_bytes, st, p);
+  return launch_kc(kPdlStream, kern, dim3(p.Gc * p.RB), dim3(kStreamThreads), (size_t)p.smem_bytes, st, p);
 }
 
 }  // namespace cpk

@@ -409,7 +409,7 @@ static cudaError_t launch_ylsolve_t(const YLSolveArgs &a, cudaStream_t st) {
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled(kPdlCluster) ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, ylsolve_kernel_t<R>, a);

@@ -23,7 +23,7 @@ out = torch.empty(4, dtype=torch.float64, device="cuda")
 for _ in range(10):
     cp.als_sweep(Zd, dims, A, nz, out=out, ws=ws)
 torch.cuda.synchronize()
-cp.profile_enable(True)
+cp.profile_enable(os.environ.get("NOPROF", "0") != "1")
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 import time
 e0.record()
@@ -37,8 +37,9 @@ n, pms, pb = cp.profile_read()
 cp.profile_enable(False)
 ms = e0.elapsed_time(e1) / reps
 tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("CP_"))
+gbs = pb / max(1, n) / (pms / max(1, n)) / 1e6 if pms > 0 else float("nan")
 print(f"{name} {tag}: {ms:.4f} ms/sweep; stream kernels {pms / max(1, n):.4f} ms avg, "
-      f"{pb / max(1, n) / (pms / max(1, n)) / 1e6:.0f} GB/s alg, share {pms / reps / ms:.3f}; "
+      f"{gbs:.0f} GB/s alg, share {pms / reps / ms:.3f}; "
       f"status {out[2].item()}; host {th:.4f} ms/call", flush=True)
 if os.environ.get("GRAPH", "0") == "1":
     cp.profile_enable(False)
