@@ -114,7 +114,8 @@ static bool plan_digits(StreamPlan &p, const cp_shape &s) {
 
 // FP64 tensor-core consumer geometry (stream_mma.cuh): row block, k-split and m-tiles per warp
 static bool plan_mma_ok(const StreamPlan &p, const cp_shape &s, int op) {
-  return !(env_int("CP_STREAM_MMA", 1) == 0 || op == OP_RESID || s.R > 32 || (p.I1 & 1));
+  return !(env_int("CP_STREAM_MMA", 1) == 0 || (op == OP_RESID && env_int("CP_RESID_MMA", 1) == 0) || s.R > 32 ||
+           (p.I1 & 1));
 }
 static bool plan_mma(StreamPlan &p, const cp_shape &s, int op) {
   if (!plan_mma_ok(p, s, op)) return false;
@@ -145,6 +146,9 @@ static bool plan_mma(StreamPlan &p, const cp_shape &s, int op) {
   p.mma = 1;
   p.V = 2;
   p.zcs = (int)(ceil_div(W, 16) * 16 + 8);  // = 8 (mod 16) doubles: conflict-free A fragments
+  // residual pass: Z is read at the C-fragment positions (row gq, columns 2 tq, 2 tq + 1);
+  // a column stride = 2 (mod 8) doubles makes each half-warp hit 16 distinct bank pairs
+  if (op == OP_RESID) p.zcs = (int)(ceil_div(W, 8) * 8 + 2);
   return true;
 }
 
@@ -177,7 +181,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   const int WSTR = (s.R % 2 == 0) ? s.R + 2 : s.R + 1;
   p.RS = s.R + (s.R & 1);
   // stage size: tools/sweep*.sh (DFMA consumers), tools/plan_sweep.py (MMA: 2 stages of ~52 KB)
-  const int stage_target = env_int("CP_STAGE_BYTES", (op != OP_RESID && plan_mma_ok(p, s, op)) ? 53248 : 40960);
+  const int stage_target = env_int("CP_STAGE_BYTES", plan_mma_ok(p, s, op) ? 53248 : 40960);
   int cps, cpt = 1;
   if (plan_mma(p, s, op)) {
     // stage: a multiple of 4 KS columns (k-steps of every k-group)
@@ -268,6 +272,13 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     int st = p.RS;
     while (st % 16 != 8) ++st;
     p.ars = env_int("CP_MMA_PAD_A", 0) ? st : p.RS;
+    if (op == OP_RESID && p.direct_w && env_int("CP_RESID_PAD_A", 1)) {
+      // residual pass: B fragments read factor row gq, rank 4 kk + tq -- a row stride of 4
+      // (mod 16) doubles spreads a half-warp over 16 bank pairs (one bulk copy per row)
+      int sa = p.RS;
+      while (sa % 16 != 4) ++sa;
+      p.ars = sa;
+    }
     p.wstr = env_int("CP_MMA_PAD_W", 0) ? st : WSTR;
     if (p.direct_w && env_int("CP_MMA_WSTR0", 1)) p.wstr = 0;  // no weight rows
   } else {

@@ -103,9 +103,11 @@ void register_stream_part1(StreamEntry *t);
 void register_stream_part2(StreamEntry *t);
 void register_stream_part3(StreamEntry *t);
 const StreamEntry &stream_entry(int R, int V, int op);
-// FP64 tensor-core variants stream_mma_kernel<NT, MT, OP> (OP_MTTKRP, OP_YL)
-constexpr int mma_index(int nt, int mt, int op) { return ((nt - 1) * 8 + (mt - 1)) * 2 + (op == 2 ? 1 : 0); }
-constexpr int kMmaTableSize = mma_index(4, 8, 2) + 1;
+// FP64 tensor-core variants stream_mma_kernel<NT, MT, OP> (OP_MTTKRP, OP_YL, OP_RESID)
+constexpr int mma_index(int nt, int mt, int op) {
+  return ((nt - 1) * 8 + (mt - 1)) * 3 + (op == OP_YL ? 1 : (op == OP_RESID ? 2 : 0));
+}
+constexpr int kMmaTableSize = mma_index(4, 8, OP_RESID) + 1;
 void register_stream_mma(StreamEntry *t);
 const StreamEntry &stream_mma_entry(int nt, int mt, int op);
 

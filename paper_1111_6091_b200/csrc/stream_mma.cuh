@@ -14,6 +14,8 @@
 //    bulk copy per column.  B fragments come from the staged factor rows (direct_w: the
 //    Khatri-Rao rows are the factor rows) or from the weight warp's rows.
 //  * ragged stages (fewer than 4 columns in a k-step): A and B masked to zero in registers.
+//  * residual pass (OP_RESID, cp_fit): the same stages, x = A^(0) W^T on the tensor cores and
+//    (z - x)^2 accumulated per thread, one sum per CTA.
 //  * epilogues: Y_L pass -- the k-groups' C blocks are summed in group order in shared memory
 //    and written as the I0 x R block of the segment (yl, or the CTA's edge block); MTTKRP
 //    mode >= 1 -- C contracted with the A^(1) rows, reduced over lanes and warps in a fixed
@@ -195,6 +197,22 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #pragma unroll
   for (int n = 0; n < NT; ++n) nok[n] = (n * 8 + gq) < R;
 
+  // residual pass (OP_RESID, the mode-0 plan): x(rows, cols) = A^(0)(rows, :) W(cols, :)^T on the
+  // tensor cores -- M = rows, N = 8 columns, K = 4 ranks per DMMA; the A fragments (A^(0) rows,
+  // constant over the pass) stay in registers; each thread accumulates (z - x)^2
+  constexpr int KR = (OP == OP_RESID) ? 2 * NT : 1;  // k-steps of 4 ranks
+  double aR[OP == OP_RESID ? MT : 1][KR];
+  double racc = 0.0;
+  if (OP == OP_RESID) {
+#pragma unroll
+    for (int j = 0; j < MT; ++j)
+#pragma unroll
+      for (int kk = 0; kk < KR; ++kk) {
+        const int m = arow0 + 8 * j, rk = 4 * kk + tq;
+        aR[j][kk] = (m < Wb && rk < R) ? __ldg(p.At[0] + (row0 + m) * p.RS + rk) : 0.0;
+      }
+  }
+
   int stage = 0;
   uint32_t fph = 0;
   for (;;) {
@@ -219,6 +237,58 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
           for (int n = 0; n < NT; ++n) sl[n] *= sr[8 * n];
         }
       }
+    }
+    if (OP == OP_RESID) {
+      // k-group kg takes the 8-column tiles nc = kg (mod KS) of the stage
+      double slr[KR];
+#pragma unroll
+      for (int kk = 0; kk < KR; ++kk) slr[kk] = (4 * kk + tq < R) ? 1.0 : 0.0;
+      if (p.srows) {
+#pragma unroll
+        for (int j = 1; j < kMaxDigits; ++j) {
+          if (j < p.nd && p.ord[j] != p.mode) {
+            const double *sr = sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.RS;
+#pragma unroll
+            for (int kk = 0; kk < KR; ++kk)
+              if (4 * kk + tq < R) slr[kk] *= sr[4 * kk + tq];
+          }
+        }
+      }
+      const double *zb = sm.zbuf + (size_t)stage * p.zst;
+      const double *wbase = (p.direct_w ? sm.abuf : sm.wbuf) + (size_t)stage * p.cps * wstride;
+      for (int nc = kg; nc * 8 < ncols; nc += KS) {
+        const int col = nc * 8 + gq;
+        const double *wb = wbase + (col < ncols ? col : 0) * wstride;
+        double b[KR];
+#pragma unroll
+        for (int kk = 0; kk < KR; ++kk) b[kk] = (col < ncols) ? wb[4 * kk + tq] * slr[kk] : 0.0;
+        const int c = nc * 8 + 2 * tq;
+#pragma unroll
+        for (int j = 0; j < MT; ++j) {
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < KR; ++kk) dmma_8x8x4(c0, c1, aR[j][kk], b[kk]);
+          const int m = arow0 + 8 * j;
+          if (m < Wb) {
+            if (c < ncols) {
+              const double d = zb[(size_t)c * zcs + m] - c0;
+              racc = fma(d, d, racc);
+            }
+            if (c + 1 < ncols) {
+              const double d = zb[(size_t)(c + 1) * zcs + m] - c1;
+              racc = fma(d, d, racc);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[stage]);
+      if (++stage == p.nstages) {
+        stage = 0;
+        fph ^= 1u;
+      }
+      if (flags & 2) break;
+      continue;
     }
     // full k-steps (4 landed columns): only the rank mask applies
     int k0 = 4 * kg;
@@ -346,6 +416,18 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     if (flags & 2) break;
   }
 
+  if (OP == OP_RESID) {
+    // ---- this CTA's sum of (z - x)^2: lanes, then warps in order ----
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) racc += __shfl_xor_sync(0xffffffffu, racc, off);
+    if (lane == 0) sm.red[warp] = racc;
+    named_bar_sync(1, kConsumers);
+    if (tid == 0) {
+      double sum = 0.0;
+      for (int w8 = 0; w8 < kConsumerWarps; ++w8) sum += sm.red[w8];
+      p.part[blockIdx.x] = sum;
+    }
+  }
   if (OP == OP_MTTKRP && p.mode == 0) {
     // ---- mode 0: this CTA's I1 x R partial for its row block (k-groups summed in order
     // through the Z ring, which every consumer is done with) ----

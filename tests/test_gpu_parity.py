@@ -255,7 +255,7 @@ def test_mode_product_ragged(dims, J):
         assert relerr(host_tensor(X), Xo) <= 1e-12, (dims, J, n)
 
 
-@pytest.mark.parametrize("name", ["c1", "c3"])
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c3"])
 def test_restriction_configs(name):
     """Restriction Z x_n Phat^T with a dense orthonormal Phat (c3: 256 x 128), every mode."""
     d = config(name)
@@ -266,6 +266,28 @@ def test_restriction_configs(name):
         X, nd = cp.mode_product(Zd, dims, n, dev_factor(U))
         Xo, _ = oracle.mode_product(Z, dims, n, U)
         assert relerr(host_tensor(X), Xo) <= 1e-12, (name, n)
+
+
+@pytest.mark.parametrize("name", ["c4a", "c4b"])
+def test_restriction_full_size_sampled_fibers(name):
+    """Restriction at full size (c4a 512^3 -> 256 along the mode; c4b 96^4 -> 48): the whole
+    output on the GPU, 32 sampled output fibers per mode against Phat^T applied on the host."""
+    d = config(name)
+    dims, Z = d["dims"], d["Z"]
+    N = len(dims)
+    Zt = Z.reshape(tuple(reversed(dims)))
+    Zd = dev_tensor(Z)
+    rng = np.random.default_rng(17)
+    for n in range(N):
+        U = np.asfortranarray(d["Phat"][n].T)
+        X, nd = cp.mode_product(Zd, dims, n, dev_factor(U))
+        Xt = host_tensor(X).reshape(tuple(reversed(nd)))
+        ax = N - 1 - n
+        for _ in range(32):
+            idx = [int(rng.integers(0, m)) for m in reversed(dims)]
+            sl = tuple(slice(None) if a == ax else idx[a] for a in range(N))
+            assert relerr(Xt[sl], U @ Zt[sl]) <= 1e-12, (name, n)
+        del X
 
 
 def test_interpolation_factor_matrix():
