@@ -14,10 +14,13 @@
 // NEXT-3), not in the paper, which costs the Galerkin tensor as O(PS).
 //
 // Kernels: restrict_factor_kernel (one warp: B and its bidiagonal factor, a coefficient table
-// coef[j] = {cA_j = wr[2j-1], cB_j = wl[2j+1], le_j, 1/ld_j}); restrict_inner_kernel (mode
-// n >= 1: thread per fiber, consecutive threads on consecutive inner indices -> coalesced);
+// coef[j] = {cA_j = wr[2j-1], cB_j = wl[2j+1], le_j, 1/ld_j}); restrict_tma_kernel (mode n >= 1,
+// default: 1-KB row slabs of 128 fibers streamed by bulk copies through an mbarrier ring);
+// restrict_inner_kernel (mode n >= 1 fallback: thread per fiber, coalesced loads);
 // restrict_mode0_kernel (mode 0: fibers are contiguous rows; 128-fiber tiles are staged
 // through shared memory so both the loads and the stores are coalesced).
+#include <cstdlib>
+
 #include "cp_internal.cuh"
 
 namespace cpk {
@@ -140,6 +143,63 @@ __global__ void __launch_bounds__(256) restrict_inner_kernel(const double *__res
   }
 }
 
+// mode n >= 1, TMA version: a block owns a slab of kRtW consecutive inner indices s (one fiber
+// per thread) of one outer index o and streams its I rows (kRtW doubles = 1 KB each, contiguous)
+// through a ring of kRtNS shared-memory stages of kRtRows rows, one bulk copy per row
+// (cp.async.bulk + mbarrier transaction counts).  Big contiguous requests, deep pipelining;
+// the recurrence reads the stage from shared memory.  Needs S even (16-byte rows).
+constexpr int kRtW = 128, kRtRows = 8, kRtNS = 5;  // 40 KB of stages: ~5 blocks per SM
+__global__ void __launch_bounds__(kRtW) restrict_tma_kernel(const double *__restrict__ Z, int64_t I, int64_t Ic,
+                                                           int64_t S, int64_t nslab,
+                                                           const double *__restrict__ coef, double *__restrict__ X) {
+  griddep();
+  __shared__ __align__(128) double tz[kRtNS][kRtRows][kRtW];
+  __shared__ __align__(8) uint64_t full[kRtNS];
+  const int t = threadIdx.x;
+  const int64_t o = blockIdx.x / nslab, sb = (blockIdx.x % nslab) * kRtW;
+  const int w = (int)((S - sb) < kRtW ? (S - sb) : kRtW);  // slab width (even)
+  const double *zb = Z + o * I * S + sb;
+  double *xb = X + o * Ic * S + sb;
+  const int nst = (int)((I + kRtRows - 1) / kRtRows);
+  if (t == 0) {
+    for (int q = 0; q < kRtNS; ++q) mbar_init(&full[q], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int st) {  // thread 0: rows st * kRtRows .. of the slab into slot st % kRtNS
+    const int slot = st % kRtNS;
+    const int64_t r0 = (int64_t)st * kRtRows;
+    const int nr = (int)((I - r0) < kRtRows ? (I - r0) : kRtRows);
+    mbar_expect_tx(&full[slot], (uint32_t)(nr * w * 8));
+    for (int r = 0; r < nr; ++r) bulk_g2s(&tz[slot][r][0], zb + (r0 + r) * S, (uint32_t)(w * 8), &full[slot]);
+    mbar_arrive(&full[slot]);  // the phase completes with this arrival and the landed bytes
+  };
+  if (t == 0)
+    for (int st = 0; st < kRtNS && st < nst; ++st) issue(st);
+  double zprev = 0.0, xprev = 0.0;
+  for (int st = 0; st < nst; ++st) {
+    const int slot = st % kRtNS;
+    mbar_wait(&full[slot], (uint32_t)((st / kRtNS) & 1));
+    const int64_t r0 = (int64_t)st * kRtRows;  // even: the stage starts at a C point
+    const int nr = (int)((I - r0) < kRtRows ? (I - r0) : kRtRows);
+    if (t < w) {
+      for (int q = 0; q < nr; q += 2) {
+        const int64_t j = (r0 + q) / 2;
+        const double4 c = coef_at(coef, j);
+        const double zc = tz[slot][q][t];
+        const double zf = (q + 1 < nr) ? tz[slot][q + 1][t] : 0.0;
+        const double y = fma(c.y, zf, fma(c.x, zprev, zc));
+        const double xv = fma(-c.z, xprev, y) * c.w;
+        __stcs(xb + j * S + t, xv);
+        zprev = zf;
+        xprev = xv;
+      }
+    }
+    __syncthreads();  // every thread is done with the slot
+    if (t == 0 && st + kRtNS < nst) issue(st + kRtNS);
+  }
+}
+
 // mode 0: fibers are the contiguous rows of Z (length I); a block stages 128 rows x 32 fine
 // columns (one chunk) in shared memory, each thread runs its row's recurrence over the chunk's
 // 16 coarse points, and the 128 x 16 outputs leave through the same tile
@@ -238,11 +298,19 @@ extern "C" int cp_restrict_structured(int32_t N, const int64_t *dims, const doub
     const int64_t nfib = S * O;
     const bool v2 = (S % 2 == 0) && ((uintptr_t)Z % 16 == 0) && ((uintptr_t)X % 16 == 0);
     const int64_t nthr = v2 ? nfib / 2 : nfib;
-    if (v2)
-      e = launch_k(restrict_inner_kernel<2>, dim3((unsigned)((nthr + 255) / 256)), dim3(256), 0, st, Z, I, Ic, S, nfib,
+    const char *eb = getenv("CP_RESTRICT_BLOCK");
+    const int bs = (eb && *eb) ? atoi(eb) : 128;  // 128: ~7 blocks per SM, small tail
+    const char *et = getenv("CP_RESTRICT_TMA");
+    const bool tma = !(et && *et && atoi(et) == 0) && (S % 2 == 0) && ((uintptr_t)Z % 16 == 0);
+    if (tma) {
+      const int64_t nslab = (S + kRtW - 1) / kRtW;
+      e = launch_k(restrict_tma_kernel, dim3((unsigned)(O * nslab)), dim3(kRtW), 0, st, Z, I, Ic, S, nslab,
+                   (const double *)coef, X);
+    } else if (v2)
+      e = launch_k(restrict_inner_kernel<2>, dim3((unsigned)((nthr + bs - 1) / bs)), dim3(bs), 0, st, Z, I, Ic, S, nfib,
                    (const double *)coef, X);
     else
-      e = launch_k(restrict_inner_kernel<1>, dim3((unsigned)((nthr + 255) / 256)), dim3(256), 0, st, Z, I, Ic, S, nfib,
+      e = launch_k(restrict_inner_kernel<1>, dim3((unsigned)((nthr + bs - 1) / bs)), dim3(bs), 0, st, Z, I, Ic, S, nfib,
                    (const double *)coef, X);
   }
   return e == cudaSuccess ? CP_OK : CP_ECUDA;
