@@ -133,8 +133,11 @@ __device__ __forceinline__ void dmma_m8n8k4(double &d0, double &d1, double a, do
 
 template <bool A_MC, bool B_NC>
 __global__ void __launch_bounds__(256) gemm_dmma_kernel(const GemmArgs g) {
-  __shared__ double As[1][A_MC ? TBK * AMS : TBM * AKS];  // single buffer + register prefetch
-  __shared__ double Bs[1][B_NC ? TBK * BNS : TBN * BKS];
+  // double buffer + register prefetch (dynamic shared memory: > 48 KB)
+  constexpr int ASZ = A_MC ? TBK * AMS : TBM * AKS, BSZ = B_NC ? TBK * BNS : TBN * BKS;
+  extern __shared__ __align__(16) double gsm[];
+  double(*As)[ASZ] = reinterpret_cast<double(*)[ASZ]>(gsm);
+  double(*Bs)[BSZ] = reinterpret_cast<double(*)[BSZ]>(gsm + 2 * ASZ);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps
   const int gq = lane >> 2, tq = lane & 3;  // fragment coordinates
@@ -209,9 +212,11 @@ __global__ void __launch_bounds__(256) gemm_dmma_kernel(const GemmArgs g) {
         for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
     if (more) {
-      __syncthreads();  // every warp is done reading the tile
-      store(buf);
+      // the other buffer was last read in the previous iteration, before that iteration's
+      // barrier: store the prefetched tile there, one barrier per k-tile
+      store(buf ^ 1);
       __syncthreads();
+      buf ^= 1;
     }
   }
 #pragma unroll
@@ -226,6 +231,21 @@ __global__ void __launch_bounds__(256) gemm_dmma_kernel(const GemmArgs g) {
       }
 }
 
+static size_t dmma_smem(bool a_mc, bool b_nc) {
+  return 2 * sizeof(double) * (size_t)((a_mc ? TBK * AMS : TBM * AKS) + (b_nc ? TBK * BNS : TBN * BKS));
+}
+static cudaError_t dmma_attrs() {
+  static cudaError_t done = [] {
+    cudaError_t e = cudaFuncSetAttribute(gemm_dmma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)dmma_smem(true, true));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_dmma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)dmma_smem(true, false));
+    return e;
+  }();
+  return done;
+}
+
 static int env_flag(const char *name, int dflt) {
   const char *v = getenv(name);
   return (v && *v) ? atoi(v) : dflt;
@@ -234,6 +254,7 @@ static int env_flag(const char *name, int dflt) {
 cudaError_t launch_mode_product(int N, const int64_t *dims, const double *Z, int mode,
                                 const double *U, int64_t J, double *X, cudaStream_t st) {
   if (env_flag("CP_MODEPROD_DMMA", 1)) {
+    if (cudaError_t e = dmma_attrs()) return e;
     int64_t left = 1, right = 1;
     for (int k = 0; k < mode; ++k) left *= dims[k];
     for (int k = mode + 1; k < N; ++k) right *= dims[k];
@@ -264,8 +285,8 @@ cudaError_t launch_mode_product(int N, const int64_t *dims, const double *Z, int
       gb.B = g.B + b0 * g.sbb;
       gb.C = g.C + b0 * g.scb;
       dim3 grid((unsigned)gbig, (unsigned)gsmall, (unsigned)gb.batch);
-      if (a_mc && b_nc) gemm_dmma_kernel<true, true><<<grid, 256, 0, st>>>(gb);
-      else gemm_dmma_kernel<true, false><<<grid, 256, 0, st>>>(gb);
+      if (a_mc && b_nc) gemm_dmma_kernel<true, true><<<grid, 256, dmma_smem(true, true), st>>>(gb);
+      else gemm_dmma_kernel<true, false><<<grid, 256, dmma_smem(true, false), st>>>(gb);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
     }
