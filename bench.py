@@ -34,6 +34,7 @@ import cpsynth  # noqa: E402
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+DMMA_PEAK_TF = 37.0    # fp64 mma.sync (DMMA) TFLOP/s measured on this pool (tools/microbench.cu)
 
 
 def parse():
@@ -323,8 +324,13 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle
         val, steps, t = oracle_sampled_sweeps_per_s(d, min_seconds=10.0)
+        cores = oracle.num_threads()
+        oracle.set_threads(1)
+        val1, steps1, t1 = oracle_sampled_sweeps_per_s(d, min_seconds=5.0)
+        oracle.set_threads(cores)
         line["cpu_baseline"] = {
-            "value": val, "unit": "sweeps/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "value": val, "unit": "sweeps/s", "cores": cores, "kind": "oracle",
+            "value_1_thread": val1, "sample_1_thread": f"{steps1} sample steps in {t1:.1f} s on one host core",
             "sample": (f"oracle MTTKRP of a contiguous 1/16 of the output rows of every mode per "
                        f"sample step, {steps} steps in {t:.1f} s on the host cores, scaled to sweeps/s "
                        f"(R x R solves not timed)")}
@@ -376,6 +382,21 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
     rows["restriction_mode0"] = {"ms": t, "TFLOPs": flops / t / 1e9, "J": J,
                                  "alg_GBps": 8.0 * (P + P * J / dims[0]) / t / 1e6}
     del X
+    # BASELINE.json configs[3]: restriction of a 256^3 tensor by a dense 256 x 128 transfer
+    # operator, every mode (random data of that shape; fp64-compute-bound: DMMA roofline)
+    Z3 = torch.randn(256, 256, 256, dtype=torch.float64, device=dev)
+    for n in range(3):
+        U3 = colmajor(torch.randn(128, 256, dtype=torch.float64, device=dev))
+        nd3 = [256, 256, 256]
+        nd3[n] = 128
+        X3 = torch.empty(tuple(reversed(nd3)), dtype=torch.float64, device=dev)
+        t = timed(lambda: cp.mode_product(Z3, (256, 256, 256), n, U3, X=X3), n=10)
+        tf = 2.0 * 128 * 256**3 / t / 1e9
+        rows[f"restriction_c3_dense_mode{n}"] = {"ms": t, "TFLOPs": tf,
+                                                 "frac_dmma_peak": tf / DMMA_PEAK_TF,
+                                                 "peak_note": "DMMA peak 37.0 TFLOP/s measured by tools/microbench.cu"}
+        del X3
+    del Z3
     # NEXT-3: the same restriction with the structured BAMG operator (cp_restrict_structured:
     # 3-tap gather + bidiagonal substitution per fiber; HBM-bound), every mode
     for n in range(len(dims)):

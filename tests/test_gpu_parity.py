@@ -328,3 +328,31 @@ def test_fit_configs(name):
     oo, _ = oracle.gradient(Z, dims, A, want_G=False)
     assert abs(out[0] - oo[0]) <= 1e-12 * abs(oo[0])
     assert abs(out[1] - oo[1]) <= 1e-10 * abs(oo[1]) + 1e-13
+
+
+def test_chained_calls_without_sync_match_synced():
+    """Every kernel reads its inputs only after its programmatic-dependent-launch wait: a chain of
+    library calls on one stream with no host synchronization (sweep -> restriction -> mode
+    product -> fit -> MTTKRP, each consuming the previous outputs) equals the same chain with a
+    synchronization after every call, bitwise."""
+    dims, R = (40, 36, 30), 6
+    Z, A0 = cpsynth.random_problem(dims, R, seed=77)
+    wl, wr = cpsynth.transfer_weights(dims[1], seed=5)
+    U = np.asfortranarray(cpsynth.random_matrix(12, dims[2], seed=6))
+
+    def chain(sync):
+        Zd = dev_tensor(Z)
+        Ad = [dev_factor(a) for a in A0]
+        ws = cp.Workspace(dims, R)
+        s = (lambda: torch.cuda.synchronize()) if sync else (lambda: None)
+        nz = cp.norm2(Zd, dims, ws=ws); s()
+        out = cp.als_sweep(Zd, dims, Ad, nz, ws=ws); s()
+        X1, d1 = cp.restrict_structured(Zd, dims, 1, torch.from_numpy(wl).cuda(), torch.from_numpy(wr).cuda()); s()
+        X2, d2 = cp.mode_product(X1, d1, 2, dev_factor(U)); s()
+        f, _ = cp.fit(Zd, dims, Ad, nz, ws=ws); s()
+        M = cp.mttkrp(Zd, dims, Ad, 0, ws=ws); s()
+        torch.cuda.synchronize()
+        return [host_tensor(t) for t in (out, X1, X2, f, M)] + [host_factor(a) for a in Ad]
+
+    for a, b in zip(chain(False), chain(True)):
+        assert np.array_equal(a, b)
