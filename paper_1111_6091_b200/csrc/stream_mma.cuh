@@ -261,7 +261,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
         const double *wb = wbase + (col < ncols ? col : 0) * wstride;
         double b[KR];
 #pragma unroll
-        for (int kk = 0; kk < KR; ++kk) b[kk] = (col < ncols) ? wb[4 * kk + tq] * slr[kk] : 0.0;
+        // (a select, not a multiply by the 0/1 mask: the padding ranks >= R of a staged row are
+        // never written and may hold NaN bit patterns)
+        for (int kk = 0; kk < KR; ++kk) b[kk] = (col < ncols && 4 * kk + tq < R) ? wb[4 * kk + tq] * slr[kk] : 0.0;
         const int c = nc * 8 + 2 * tq;
 #pragma unroll
         for (int j = 0; j < MT; ++j) {
