@@ -230,13 +230,20 @@ class MGOracle:
                 break
             g_old = gn
         if not converged and p["use_fmg"]:
+            # reading R29: the FMG approximation replaces the setup iterate only if it lowers g
+            # ("a new approximation"; P:488 discards a worse iterate the same way)
+            kept = [a.copy(order="F") for a in f.A]
             self.fmg(A_fmg)
-            g = self.fit(0, f.A)[0][1]
+            gf = self.fit(0, f.A)[0][1]
             cycles += 1
-            trace.append((1, cycles, g))
-            converged = g < p["tol"]
-            if not converged:
-                self.setup_cycle(0, False, False)
+            trace.append((1, cycles, gf))
+            if gf < g:
+                g = gf
+                converged = g < p["tol"]
+                if not converged:
+                    self.setup_cycle(0, False, False)
+            else:
+                f.A = kept
         rebuilt = False
         g_old = g
         while not converged and cycles < p["max_cycles"]:

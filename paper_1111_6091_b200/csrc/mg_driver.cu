@@ -516,13 +516,21 @@ int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const doub
     g_old = gn;
   }
   // optional FMG cycle, then a down-sweep rebuild of the operators
+  // (reading R29: the FMG approximation replaces the setup iterate only if it lowers g;
+  // otherwise the setup iterate is restored and the operators are kept)
   if (!converged && prm->use_fmg && mg.err == CP_OK) {
+    for (int n = 0; n < N; ++n) mg.copy(f.prev[n], f.A[n], (size_t)s->dims[n] * R);
     mg.fmg(A_fmg);
-    g = mg.fit(0, f.A, nullptr);
+    const double gf = mg.fit(0, f.A, nullptr);
     ++cycles;
-    record(1, cycles, g);
-    converged = g < prm->tol;
-    if (!converged) mg.setup_cycle(0, false, false);
+    record(1, cycles, gf);
+    if (gf < g) {
+      g = gf;
+      converged = g < prm->tol;
+      if (!converged) mg.setup_cycle(0, false, false);
+    } else {
+      for (int n = 0; n < N; ++n) mg.copy(f.A[n], f.prev[n], (size_t)s->dims[n] * R);
+    }
   }
   // solve phase
   bool rebuilt = false;
