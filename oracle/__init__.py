@@ -177,6 +177,23 @@ def f_direct(Z, dims, A):
     return lib().oracle_f_direct(len(dims), _dims(dims), A[0].shape[1], _dp(z), _ptr_array(A))
 
 
+def f_expand(Z, dims, A, normZ2=None):
+    """f at one iterate by the expansion (reading R6; eq:CPfunctional with eq:propMatricized and
+    eq:Gamma P:113-116):  f = 1/2 ||Z||^2 - <Z_(N) Phi^(N), A^(N)> + 1/2 1^T (*_k A^(k)T A^(k)) 1,
+    written from oracle_mttkrp and oracle_gram.  Pinned against f_direct (the plain definition),
+    the exact-model and zero-factor special cases in tests/test_oracle_pins.py."""
+    N = len(dims)
+    z = _zvec(Z, dims)
+    if normZ2 is None:
+        normZ2 = float(np.dot(z, z))
+    M = mttkrp(Z, dims, A, N - 1)
+    inner = float(np.sum(M * _cm(A[N - 1])))
+    H = np.ones((A[0].shape[1],) * 2)
+    for a in A:
+        H = H * gram(a)
+    return 0.5 * normZ2 - inner + 0.5 * float(np.sum(H))
+
+
 def gradient(Z, dims, A, F=None, normZ2=None, want_G=True):
     """Returns (out[2+N] = f, g, ||G^n||^2..., G list or None)."""
     N = len(dims)

@@ -184,6 +184,26 @@ def test_f_direct_special_cases():
     assert oracle.f_direct(Z, dims, A) == pytest.approx(0.5 * np.sum((Z - X) ** 2), rel=1e-13)
 
 
+@pytest.mark.parametrize("dims,R", [((5, 4, 3), 2), ((3, 2, 4, 3), 3), ((7, 6), 2), ((4, 3, 2, 2, 3), 4)])
+def test_f_expand_special_cases_and_direct(dims, R):
+    """oracle.f_expand (reading R6: 1/2||Z||^2 - <M^(N),A^(N)> + 1/2 1^T(*Upsilon)1) against the plain
+    definition f_direct = 1/2 sum (z - x)^2 (eq:CPfunctional P:38-42) on random iterates; an exact
+    model gives f = 0 up to cancellation; zero factors give 1/2||Z||^2 exactly; a dropped Gram,
+    a wrong mode in the inner product or a missing factor 1/2 fails one of them."""
+    Z, A = cpsynth.random_problem(dims, R, seed=41 + R)
+    half = 0.5 * float(np.vdot(Z, Z))
+    assert oracle.f_expand(Z, dims, A) == pytest.approx(oracle.f_direct(Z, dims, A), abs=1e-13 * half)
+    X = cpsynth.kruskal(A)
+    assert abs(oracle.f_expand(X, dims, A)) <= 1e-13 * 0.5 * float(np.vdot(X, X))
+    zero = [np.zeros_like(a, order="F") for a in A]
+    assert oracle.f_expand(Z, dims, zero) == half
+    # a perturbed iterate moves f_direct and f_expand together (not a constant offset)
+    B = [a.copy(order="F") for a in A]
+    B[0][0, 0] += 0.3
+    assert oracle.f_expand(Z, dims, B) == pytest.approx(oracle.f_direct(Z, dims, B), abs=1e-13 * half)
+    assert abs(oracle.f_direct(Z, dims, B) - oracle.f_direct(Z, dims, A)) > 1e-6 * half
+
+
 @pytest.mark.parametrize("dims,R", [((4, 3, 5), 2), ((3, 2, 4, 3), 3), ((6, 5, 4), 1)])
 def test_gradient_vs_finite_differences(dims, R):
     """G^(n) (eq:gradEqn P:104-107) against central differences of f (eq:CPfunctional),
