@@ -368,6 +368,11 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
     # a8: cp_fit (residual pass + N MTTKRPs + gradients)
     t = timed(lambda: cp.fit(Zd, dims, A, nz, ws=ws), n=5)
     rows["fit"] = {"ms": t}
+    # NEXT-2: cp_gradient (all N gradients at one iterate through the dimension tree, no residual
+    # pass; what the multigrid driver's stopping tests and FAS operators call)
+    t = timed(lambda: cp.gradient(Zd, dims, A, nz, ws=ws), n=5)
+    rows["gradient"] = {"ms": t, "z_passes": 2 if len(dims) >= 3 else len(dims),
+                        "alg_GBps": 2 * 8.0 * P / t / 1e6 if len(dims) >= 3 else None}
     # a7: restriction Z x_1 Phat^T (dense orthonormal Phat, I_1 -> ceil(I_1/2))
     Ph = d["Phat"][0]
     U = torch.from_numpy(np.ascontiguousarray(Ph)).to(dev).t()  # (Ic x I1) column-major = Phat^T

@@ -11,6 +11,8 @@
  *   cp_restrict_structured  X = Z x_n Phat^T for the BAMG
  *                    transfer operator (bidiagonal factor, O(P))
  *   cp_fit           f (direct), g and ||G^(n)||^2              eq:gradConv P:454-456
+ *   cp_gradient      g, ||G^(n)||^2, G^(n) and f (expansion)    eq:gradEqn, eq:gradConv; SURVEY NEXT-2
+ *                    at one iterate, without the residual pass
  *   cp_norm2         ||Z||^2
  *
  * ---------------------------------------------------------------------------------------
@@ -154,6 +156,20 @@ int cp_restrict_structured(int32_t N, const int64_t *dims, const double *Z, int3
 int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const double *const *A,
            const double *const *F, double *out, double *const *G, void *ws, size_t ws_bytes,
            cp_stream_t stream);
+
+/* All-modes gradient at one iterate (eq:gradEqn, eq:gradConv P:454-456): every
+ * M^(n) = Z_(n)Phi^(n) with the SAME factors (no Gauss-Seidel dependency), so for N >= 3 the
+ * dimension tree reads Z twice for all N modes (a Y_L pass and a mode-2 pass), and no residual
+ * pass.  This is what the multigrid driver needs for the stopping test g and the FAS operator
+ * H(A) (eq:FASop P:326-328, eq:FASrhs P:398).  Same arguments and G as cp_fit; out differs only
+ * in out[0]:
+ *   out  device, 2 + N doubles: f by the expansion f = 1/2 ||Z||^2 - <M^(N), A^(N)>
+ *        + 1/2 1^T (*_k A^(k)T A^(k)) 1 (reading R6; equals cp_fit's direct f up to cancellation
+ *        of order eps * ||Z||^2), g, ||G^(n)||^2 (n < N).  F enters G only, as in cp_fit.
+ *   Errors: as cp_fit. */
+int cp_gradient(const cp_shape *s, const double *Z, const double *normZ2, const double *const *A,
+                const double *const *F, double *out, double *const *G, void *ws, size_t ws_bytes,
+                cp_stream_t stream);
 
 /* Number of kernel launches the last successful call on this thread enqueued (for the
  * benchmark's gpu_launches count). */

@@ -336,3 +336,26 @@ def fit(Z, dims, A, normZ2, F=None, want_G=False, out=None, ws=None, stream=None
                         _ptr(out), _ptr_array(G) if G else None, _ptr(ws.buf),
                         ctypes.c_size_t(ws.nbytes), _stream(stream)), "cp_fit")
     return out, G
+
+
+def gradient(Z, dims, A, normZ2, F=None, want_G=False, out=None, ws=None, stream=None):
+    """g, ||G^(n)||^2 (and G) at one iterate without the residual pass, f by the expansion
+    (cp_gradient).  Returns (out, G list or None)."""
+    _check_Z(Z, dims)
+    N = len(dims)
+    R = A[0].shape[1]
+    for k, a in enumerate(A):
+        _check_cm(a, dims[k], R, f"A[{k}]")
+    Fp = None
+    if F is not None:
+        for k, f in enumerate(F):
+            if f is not None:
+                _check_cm(f, dims[k], R, f"F[{k}]")
+        Fp = _ptr_array(list(F))
+    G = [empty_factor(dims[k], R, Z.device) for k in range(N)] if want_G else None
+    out = torch.empty(2 + N, dtype=torch.float64, device=Z.device) if out is None else out
+    ws = _ws(ws, dims, R, Z.device)
+    _check(lib().cp_gradient(ctypes.byref(_shape(dims, R)), _ptr(Z), _ptr(normZ2), _ptr_array(A), Fp,
+                             _ptr(out), _ptr_array(G) if G else None, _ptr(ws.buf),
+                             ctypes.c_size_t(ws.nbytes), _stream(stream)), "cp_gradient")
+    return out, G

@@ -12,7 +12,7 @@ _lib = None
 
 # every symbol include/cp.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = ["cp_workspace_bytes", "cp_norm2", "cp_mttkrp", "cp_als_sweep",
-           "cp_mode_product_workspace_bytes", "cp_mode_product", "cp_fit",
+           "cp_mode_product_workspace_bytes", "cp_mode_product", "cp_fit", "cp_gradient",
            "cp_restrict_workspace_bytes", "cp_restrict_structured",
            "cp_last_launch_count", "cp_profile_enable", "cp_profile_read", "cp_normalize_sort",
            "cp_mg_default_params", "cp_mg_workspace_bytes", "cp_mg_solve",
@@ -54,11 +54,12 @@ def lib():
         L.cp_mode_product_workspace_bytes.restype = sz
         L.cp_mode_product.argtypes = [i32, vp, vp, i32, vp, i64, vp, vp, sz, vp]
         L.cp_fit.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.cp_gradient.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
         L.cp_restrict_workspace_bytes.argtypes = [i32, vp, i32]
         L.cp_restrict_workspace_bytes.restype = sz
         L.cp_restrict_structured.argtypes = [i32, vp, vp, i32, vp, vp, vp, vp, sz, vp]
         L.cp_restrict_structured.restype = ctypes.c_int
-        for f in ["cp_norm2", "cp_mttkrp", "cp_als_sweep", "cp_mode_product", "cp_fit",
+        for f in ["cp_norm2", "cp_mttkrp", "cp_als_sweep", "cp_mode_product", "cp_fit", "cp_gradient",
                   "cp_last_launch_count", "cp_version"]:
             getattr(L, f).restype = ctypes.c_int
         L.cp_profile_enable.argtypes = [ctypes.c_int]

@@ -879,9 +879,11 @@ int cp_mode_product(int32_t N, const int64_t *dims, const double *Z, int32_t mod
   return CP_OK;
 }
 
-int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const double *const *A,
-           const double *const *F, double *out, double *const *G, void *ws, size_t ws_bytes,
-           cp_stream_t stream) {
+// cp_fit (resid = true: f by the residual pass) and cp_gradient (resid = false: no residual
+// pass, f by the expansion from the last mode's <M, A> and the Grams)
+static int fit_impl(const cp_shape *s, const double *Z, const double *normZ2, const double *const *A,
+                    const double *const *F, double *out, double *const *G, void *ws, size_t ws_bytes,
+                    cp_stream_t stream, bool resid) {
   g_launches = 0;
   int st = check_shape(s, 2);
   if (st) return st;
@@ -911,8 +913,10 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
   rp.Z = Z;
   for (int k = 0; k < N; ++k) rp.At[k] = w + L.At[k];
   rp.part = w + L.residp;
-  if (launch_stream(rp, cs) != cudaSuccess) return CP_ECUDA;
-  ++launches;
+  if (resid) {
+    if (launch_stream(rp, cs) != cudaSuccess) return CP_ECUDA;
+    ++launches;
+  }
   int ngrad[CP_MAX_N] = {0};
   // G^(n) = -M^(n) + A^(n) Gamma^(n) - F^(n) and its squared norm (eq:gradEqn, eq:gradConv)
   auto grad_mode = [&](int n, const ReduceGeom &rg, int rpc, int sp) -> bool {
@@ -931,6 +935,7 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
     ga.Ups = w + L.Ups;
     ga.G = (G != nullptr) ? G[n] : nullptr;
     ga.gpart = w + L.gradp + (size_t)n * L.grad_max;
+    ga.dpart = (!resid && n == N - 1) ? w + L.dotM : nullptr;  // (dotM holds gp_max >= ngrad)
     ngrad[n] = (int)ceil_div(s->dims[n], rpc);
     ++launches;
     return launch_k(gradient_kernel, dim3(ngrad[n]), dim3(256), 0, cs, ga) == cudaSuccess;
@@ -1040,9 +1045,29 @@ int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const doubl
   fa.gpart = w + L.gradp;
   fa.normZ2 = normZ2;
   fa.out = out;
+  if (!resid) {
+    fa.nresid = 0;
+    fa.expand = 1;
+    fa.R = R;
+    fa.ndot = ngrad[N - 1];
+    fa.dpart = w + L.dotM;
+    fa.pg = pg;
+  }
   if (launch_k(finalize_fit_kernel, dim3(1), dim3(256), 0, cs, fa) != cudaSuccess) return CP_ECUDA;
   g_launches = launches + 1;
   return CP_OK;
+}
+
+int cp_fit(const cp_shape *s, const double *Z, const double *normZ2, const double *const *A,
+           const double *const *F, double *out, double *const *G, void *ws, size_t ws_bytes,
+           cp_stream_t stream) {
+  return fit_impl(s, Z, normZ2, A, F, out, G, ws, ws_bytes, stream, true);
+}
+
+int cp_gradient(const cp_shape *s, const double *Z, const double *normZ2, const double *const *A,
+                const double *const *F, double *out, double *const *G, void *ws, size_t ws_bytes,
+                cp_stream_t stream) {
+  return fit_impl(s, Z, normZ2, A, F, out, G, ws, ws_bytes, stream, false);
 }
 
 int cp_normalize_sort(const cp_shape *s, double *const *A, int32_t sort, double *lambda, void *ws,

@@ -181,7 +181,7 @@ struct MG {
     Level &v = lv[l];
     if (err != CP_OK) return NAN;
     const auto t0 = std::chrono::steady_clock::now();
-    ok(cp_fit(&v.s, v.Z, v.nz2, A, nullptr, out_fit, G, ws, ws_bytes, cst));
+    ok(cp_gradient(&v.s, v.Z, v.nz2, A, nullptr, out_fit, G, ws, ws_bytes, cst));  // NEXT-2: no residual pass
     h_fit.assign(2 + N, NAN);
     if (err == CP_OK &&
         cudaMemcpyAsync(h_fit.data(), out_fit, (2 + N) * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
@@ -648,7 +648,7 @@ int cp_als_solve(const cp_shape *s, const double *Z, double *const *A, double to
     }
     if (it % check_every == 0 || it == max_iters) {
       const auto tf = std::chrono::steady_clock::now();
-      if ((rc = cp_fit(s, Z, nz2, A, nullptr, fitout, nullptr, ws, w, stream))) return rc;
+      if ((rc = cp_gradient(s, Z, nz2, A, nullptr, fitout, nullptr, ws, w, stream))) return rc;
       if (cudaMemcpyAsync(h.data(), fitout, (2 + s->N) * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
           cudaStreamSynchronize(st) != cudaSuccess)
         return CP_ECUDA;

@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(256) gradient_kernel(const GradArgs a) {
   const int nrows = (int)((In - i0) < a.rpc ? (In - i0) : a.rpc);
   gather_rows(a.rg, i0, nrows, R, a.sp, sM, scratch);
   __syncthreads();
-  double g2 = 0.0;
+  double g2 = 0.0, dm = 0.0;
   for (int e = tid; e < nrows * R; e += blockDim.x) {
     const int ii = e / R, r = e - (e / R) * R;
     const int64_t i = i0 + ii;
@@ -418,9 +418,14 @@ __global__ void __launch_bounds__(256) gradient_kernel(const GradArgs a) {
     if (a.F != nullptr) gv -= a.F[i + In * r];
     if (a.G != nullptr) a.G[i + In * r] = gv;
     g2 = fma(gv, gv, g2);
+    if (a.dpart != nullptr) dm = fma(sM[e], a.A[i + In * r], dm);
   }
   const double t = block_sum_256(g2, scratch);
   if (tid == 0) a.gpart[blockIdx.x] = t;
+  if (a.dpart != nullptr) {
+    const double d = block_sum_256(dm, scratch);
+    if (tid == 0) a.dpart[blockIdx.x] = d;
+  }
 }
 
 __global__ void __launch_bounds__(256) finalize_fit_kernel(const FitFinalArgs a) {
@@ -438,8 +443,22 @@ __global__ void __launch_bounds__(256) finalize_fit_kernel(const FitFinalArgs a)
     if (tid == 0) a.out[2 + n] = sn;
     tot += sn;
   }
+  double f = 0.5 * res;
+  if (a.expand) {
+    // f = 1/2 ||Z||^2 - <M^(N), A^(N)> + 1/2 ||[[A]]||^2 (reading R6), fixed summation order
+    const int RR = a.R * a.R;
+    double m2 = 0.0, in = 0.0, unused = 0.0;
+    for (int e = tid; e < RR; e += blockDim.x) {
+      double p = 1.0;
+      for (int k = 0; k < a.N; ++k) p *= prep_gram(a.pg, k, e, RR);
+      m2 += p;
+    }
+    for (int c = tid; c < a.ndot; c += blockDim.x) in += a.dpart[c];
+    block_sum3_256(m2, in, unused, sred);
+    f = 0.5 * a.normZ2[0] - in + 0.5 * m2;
+  }
   if (tid == 0) {
-    a.out[0] = 0.5 * res;
+    a.out[0] = f;
     a.out[1] = sqrt(tot) / sqrt(a.normZ2[0]);
   }
 }

@@ -144,6 +144,7 @@ struct GradArgs {
   PrepGrams pg;
   const double *A, *F, *Ups;
   double *G, *gpart;
+  double *dpart;  // cp_gradient, last mode: per-CTA <M^(n), A^(n)> (f by expansion), or null
 };
 
 struct FitFinalArgs {
@@ -151,6 +152,11 @@ struct FitFinalArgs {
   int ngrad[CP_MAX_N];
   const double *resid, *gpart, *normZ2;
   double *out;
+  // cp_gradient (expand = 1): f = 1/2 ||Z||^2 - <M^(N), A^(N)> + 1/2 1^T (*_k Upsilon^(k)) 1
+  // from the last mode's <M, A> partials and the prep Grams, instead of the residual pass
+  int expand, R, ndot;
+  const double *dpart;
+  PrepGrams pg;
 };
 
 __global__ void reduce_mttkrp_kernel(const ReduceGeom g, int rpc, int sp, double *M);
