@@ -4,7 +4,7 @@
  *
  * The library computes, on one GPU, in IEEE fp64:
  *   cp_mttkrp        M = Z_(n) Phi^(n)                       eq:gradEqn, eq:Phi
- *   cp_als_sweep     one ALS / BNGS iteration (with optional   P:121, eq:relaxinnersolve P:356-358
+ *   cp_als_sweep(s)  one (or nsweeps) ALS / BNGS iteration(s) (with optional   P:121, eq:relaxinnersolve P:356-358
  *                    FAS right-hand side F) and the functional f  eq:CPfunctional P:38-42
  *   cp_mode_product  X = Z x_n U (restriction U = Phat^T,      P:74-78, eq:ctensor_transformed
  *                    interpolation on a 2-way factor matrix)
@@ -111,6 +111,15 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
 int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
                  const double *const *F, double *out, void *ws, size_t ws_bytes,
                  cp_stream_t stream);
+
+/* nsweeps >= 1 consecutive cp_als_sweep calls (the nu relaxations of a multigrid level, Table 1
+ * P:462-478), out = the values after the last sweep; a numeric failure stops at the failing
+ * sweep.  For a tensor small enough to live in one CTA's shared memory (P <= 16384, the coarse
+ * levels) all nsweeps run in ONE launch of a fused kernel; otherwise it loops the general
+ * sweep.  Same arguments and errors as cp_als_sweep (nsweeps < 1: CP_EINVAL). */
+int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
+                  const double *const *F, int32_t nsweeps, double *out, void *ws, size_t ws_bytes,
+                  cp_stream_t stream);
 
 /* n-mode product X = Z x_mode U  (X_(n) = U Z_(n))
  *   dims [host] N sizes of Z;  U: J x dims[mode], column-major;  X: dims with dims[mode] -> J.

@@ -11,7 +11,7 @@ _LIB = os.environ.get("CP_LIB_PATH") or os.path.join(_HERE, "lib", "libcp.so")
 _lib = None
 
 # every symbol include/cp.h declares (checked by tests/test_capi_symbols.py)
-EXPORTS = ["cp_workspace_bytes", "cp_norm2", "cp_mttkrp", "cp_als_sweep",
+EXPORTS = ["cp_workspace_bytes", "cp_norm2", "cp_mttkrp", "cp_als_sweep", "cp_als_sweeps",
            "cp_mode_product_workspace_bytes", "cp_mode_product", "cp_fit", "cp_gradient",
            "cp_restrict_workspace_bytes", "cp_restrict_structured",
            "cp_last_launch_count", "cp_profile_enable", "cp_profile_read", "cp_normalize_sort",
@@ -50,6 +50,7 @@ def lib():
         L.cp_norm2.argtypes = [vp, vp, vp, vp, sz, vp]
         L.cp_mttkrp.argtypes = [vp, vp, vp, i32, vp, vp, sz, vp]
         L.cp_als_sweep.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.cp_als_sweeps.argtypes = [vp, vp, vp, vp, vp, i32, vp, vp, sz, vp]
         L.cp_mode_product_workspace_bytes.argtypes = [i32, vp, i32, i64]
         L.cp_mode_product_workspace_bytes.restype = sz
         L.cp_mode_product.argtypes = [i32, vp, vp, i32, vp, i64, vp, vp, sz, vp]
@@ -59,7 +60,7 @@ def lib():
         L.cp_restrict_workspace_bytes.restype = sz
         L.cp_restrict_structured.argtypes = [i32, vp, vp, i32, vp, vp, vp, vp, sz, vp]
         L.cp_restrict_structured.restype = ctypes.c_int
-        for f in ["cp_norm2", "cp_mttkrp", "cp_als_sweep", "cp_mode_product", "cp_fit", "cp_gradient",
+        for f in ["cp_norm2", "cp_mttkrp", "cp_als_sweep", "cp_als_sweeps", "cp_mode_product", "cp_fit", "cp_gradient",
                   "cp_last_launch_count", "cp_version"]:
             getattr(L, f).restype = ctypes.c_int
         L.cp_profile_enable.argtypes = [ctypes.c_int]

@@ -9,6 +9,7 @@
 
 #include "gamma_job.cuh"
 #include "mg_kernels.cuh"
+#include "small_sweep.cuh"
 #include "small_kernels.cuh"
 #include "stream_kernel.cuh"
 
@@ -591,18 +592,55 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
   return CP_OK;
 }
 
+// small tensors (coarse multigrid levels): the fused shared-memory sweep kernel (small_sweep.cu)
+static bool use_small_sweep(const cp_shape &s) {
+  return env_int("CP_SMALL_SWEEP", 1) != 0 && small_sweep_smem_bytes(s) != 0 &&
+         small_sweep_smem_bytes(s) <= (size_t)env_int("CP_SMALL_SWEEP_SMEM", 200 * 1024);
+}
+
+static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
+                      const double *const *F, double *out, void *ws, size_t ws_bytes, cp_stream_t stream);
+
 int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
                  const double *const *F, double *out, void *ws, size_t ws_bytes,
                  cp_stream_t stream) {
+  return cp_als_sweeps(s, Z, normZ2, A, F, 1, out, ws, ws_bytes, stream);
+}
+
+int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
+                  const double *const *F, int32_t nsweeps, double *out, void *ws, size_t ws_bytes,
+                  cp_stream_t stream) {
   g_launches = 0;
   int st = check_shape(s, 2);
   if (st) return st;
-  if (!Z || !normZ2 || !A || !out || !aligned(Z, 16)) return CP_EINVAL;
+  if (!Z || !normZ2 || !A || !out || !aligned(Z, 16) || nsweeps < 1) return CP_EINVAL;
   for (int k = 0; k < s->N; ++k)
     if (A[k] == nullptr) return CP_EINVAL;
   Layout L;
   if (!make_layout(L, *s)) return CP_EINVAL;
   if ((st = check_ws(L, ws, ws_bytes))) return st;
+  if (use_small_sweep(*s)) {
+    if (launch_small_sweep(*s, Z, normZ2, A, F, nsweeps, out, reinterpret_cast<cudaStream_t>(stream)) !=
+        cudaSuccess)
+      return CP_ECUDA;
+    g_launches = 1;
+    return CP_OK;
+  }
+  int total = 0;
+  for (int k = 0; k < nsweeps; ++k) {
+    if ((st = sweep_impl(s, Z, normZ2, A, F, out, ws, ws_bytes, stream))) return st;
+    total += g_launches;
+  }
+  g_launches = total;
+  return CP_OK;
+}
+
+static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
+                      const double *const *F, double *out, void *ws, size_t ws_bytes, cp_stream_t stream) {
+  g_launches = 0;
+  int st;
+  Layout L;
+  if (!make_layout(L, *s)) return CP_EINVAL;
   double *w = static_cast<double *>(ws);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   const int N = s->N, R = s->R;

@@ -30,6 +30,11 @@ namespace {
 constexpr int kMaxTest = 8;
 constexpr int kMaxLevels = 40;
 
+static bool env_flag(const char *name, bool dflt) {
+  const char *e = getenv(name);
+  return (e && *e) ? atoi(e) != 0 : dflt;
+}
+
 static bool structured_restriction() {
   const char *e = getenv("CP_MG_STRUCTURED");
   return !(e && *e && atoi(e) == 0);
@@ -76,6 +81,14 @@ struct MG {
   int err = CP_OK;
   double fit_seconds = 0.0;
   std::vector<double> h_fit;
+  cudaEvent_t fev[2] = {nullptr, nullptr};  // device time of the stopping-test cp_gradient calls
+  void destroy_events() {
+    for (cudaEvent_t &e : fev)
+      if (e) {
+        cudaEventDestroy(e);
+        e = nullptr;
+      }
+  }
 
   // ------------------------------------------------------------ planning / allocation
   bool plan(const cp_shape &s0, const cp_mg_params &p) {
@@ -171,26 +184,44 @@ struct MG {
   // BNGS with RHS (eq:relaxinnersolve); finest level: normalize + sort
   void relax_fas(int l, double *const *A, const double *const *F, int sweeps) {
     Level &v = lv[l];
+    if (l > 0) {  // coarse levels: no normalization between sweeps -> one call (fused when small)
+      if (sweeps > 0) ok(cp_als_sweeps(&v.s, v.Z, v.nz2, A, F, sweeps, out_sweep, ws, ws_bytes, cst));
+      return;
+    }
     for (int k = 0; k < sweeps && err == CP_OK; ++k) {
       ok(cp_als_sweep(&v.s, v.Z, v.nz2, A, F, out_sweep, ws, ws_bytes, cst));
-      if (l == 0) ok(cp_normalize_sort(&v.s, A, 1, nullptr, ws, ws_bytes, cst));
+      ok(cp_normalize_sort(&v.s, A, 1, nullptr, ws, ws_bytes, cst));
     }
   }
   // g (eq:gradConv) at level l; optional G^(n) = H^(n)(A) into G (F = 0)
+  // (host synchronizing: the value is read on the host).  fit_seconds accumulates the DEVICE time
+  // of the cp_gradient call (CUDA events around it), not the host wait for earlier queued work.
   double fit(int l, double *const *A, double *const *G, double *gradnorm2 = nullptr) {
     Level &v = lv[l];
     if (err != CP_OK) return NAN;
-    const auto t0 = std::chrono::steady_clock::now();
+    if (!fev[0] && (cudaEventCreate(&fev[0]) != cudaSuccess || cudaEventCreate(&fev[1]) != cudaSuccess)) {
+      err = CP_ECUDA;
+      return NAN;
+    }
+    cudaEventRecord(fev[0], st);
     ok(cp_gradient(&v.s, v.Z, v.nz2, A, nullptr, out_fit, G, ws, ws_bytes, cst));  // NEXT-2: no residual pass
+    cudaEventRecord(fev[1], st);
     h_fit.assign(2 + N, NAN);
     if (err == CP_OK &&
         cudaMemcpyAsync(h_fit.data(), out_fit, (2 + N) * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
       err = CP_ECUDA;
     if (err == CP_OK && cudaStreamSynchronize(st) != cudaSuccess) err = CP_ECUDA;
-    fit_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    float ms = 0.f;
+    if (err == CP_OK && cudaEventElapsedTime(&ms, fev[0], fev[1]) == cudaSuccess) fit_seconds += 1e-3 * ms;
     if (gradnorm2)
       for (int n = 0; n < N; ++n) gradnorm2[n] = h_fit[2 + n];
     return h_fit[1];
+  }
+  // G^(n) = H^(n)(A) at level l, enqueued only (no host synchronization; graph-capturable)
+  void grad(int l, double *const *A, double *const *G) {
+    Level &v = lv[l];
+    if (err != CP_OK) return;
+    ok(cp_gradient(&v.s, v.Z, v.nz2, A, nullptr, out_fit, G, ws, ws_bytes, cst));
   }
   // dst (level l+1 sizes) = R^(n) src^(n) for coarsened modes, copy otherwise
   void restrict_(int l, double *const *src, double *const *dst) {
@@ -384,8 +415,8 @@ struct MG {
     relax_fas(l, v.A, F, prm.nu1_solve);
     Level &nx = lv[l + 1];
     restrict_(l, v.A, nx.Atil);     // A~_c
-    fit(l, v.A, v.H);               // H(A)
-    fit(l + 1, nx.Atil, nx.H);      // H_c(A~_c)
+    grad(l, v.A, v.H);              // H(A)
+    grad(l + 1, nx.Atil, nx.H);     // H_c(A~_c)
     for (int n = 0; n < N; ++n)     // tmp = F - H(A)
       lincomb(v.tmp[n], -1.0, v.H[n], 1.0, F ? F[n] : nullptr, v.s.dims[n] * R);
     restrict_(l, v.tmp, nx.tmp);    // R (F - H(A))
@@ -458,6 +489,7 @@ int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const doub
   if (prm->use_fmg && !A_fmg) return CP_EINVAL;
   static MG mgs;
   MG &mg = mgs;
+  mg.destroy_events();
   mg = MG();
   if (!mg.plan(*s, *prm)) return CP_EINVAL;
   {
@@ -471,8 +503,57 @@ int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const doub
   a.cap = ws_bytes;
   a.dry = false;
   mg.layout(a);
+  // the legacy default stream cannot be captured: run the solve on a private blocking stream
+  // (implicitly ordered with the legacy stream), where the solve phase replays each FAS V-cycle
+  // as one CUDA graph (CP_MG_GRAPH=0: plain launches).  Same kernels, same order: bitwise equal.
+  struct Own {
+    cudaStream_t s = nullptr;
+    cudaGraphExec_t g = nullptr;
+    void drop() {
+      if (g) cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+    ~Own() {
+      drop();
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    }
+  } own;
   mg.st = reinterpret_cast<cudaStream_t>(stream);
+  if (mg.st == nullptr && cudaStreamCreate(&own.s) == cudaSuccess) {
+    mg.st = own.s;
+    stream = reinterpret_cast<cp_stream_t>(own.s);
+  }
   mg.cst = stream;
+  const bool want_graph = env_flag("CP_MG_GRAPH", true) && mg.st != nullptr;
+  bool captured = false;
+  // one FAS V-cycle from the finest level (Algorithm 2), replayed from a graph when possible
+  auto v_cycle = [&]() {
+    if (want_graph && !captured && mg.err == CP_OK) {
+      captured = true;
+      cudaGraph_t graph = nullptr;
+      if (cudaStreamBeginCapture(mg.st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+        mg.fas_cycle(0, nullptr);
+        const cudaError_t ec = cudaStreamEndCapture(mg.st, &graph);
+        if (mg.err == CP_OK && ec == cudaSuccess && graph != nullptr &&
+            cudaGraphInstantiate(&own.g, graph, 0) != cudaSuccess)
+          own.g = nullptr;
+        if (graph != nullptr) cudaGraphDestroy(graph);
+        cudaGetLastError();  // a failed capture falls back to plain launches
+        if (mg.err != CP_OK) {
+          mg.err = CP_OK;
+          own.drop();
+        }
+      }
+    }
+    if (own.g != nullptr) {
+      if (cudaGraphLaunch(own.g, mg.st) != cudaSuccess) mg.err = CP_ECUDA;
+    } else {
+      mg.fas_cycle(0, nullptr);
+    }
+  };
   const int N = s->N, R = s->R;
   for (int k = 0; k < 16; ++k) report[k] = 0.0;
   const auto t0 = std::chrono::steady_clock::now();
@@ -537,7 +618,7 @@ int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const doub
   g_old = g;
   while (!converged && cycles < prm->max_cycles && mg.err == CP_OK) {
     for (int n = 0; n < N; ++n) mg.copy(f.prev[n], f.A[n], (size_t)s->dims[n] * R);
-    mg.fas_cycle(0, nullptr);
+    v_cycle();
     double gn = mg.fit(0, f.A, nullptr);
     ++cycles;
     ++solve_cycles;
@@ -551,6 +632,8 @@ int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const doub
     if (solve_cycles > prm->solve_stagnation_after && gn >= g_old && !rebuilt) {
       for (int n = 0; n < N; ++n) mg.copy(f.A[n], f.prev[n], (size_t)s->dims[n] * R);
       mg.setup_cycle(0, false, false);
+      own.drop();  // (re-captured after the rebuild)
+      captured = false;
       rebuilt = true;
       ++rebuilds;
       gn = g_old;

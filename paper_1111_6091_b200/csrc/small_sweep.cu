@@ -1,0 +1,297 @@
+// Fused ALS / BNGS sweeps for a tensor that fits in one CTA's shared memory (the coarse levels of
+// the multigrid hierarchy: c1 50^3 -> 25^3 -> 13^3 -> 7^3 -> 4^3).
+//
+// The coarsest level runs nu_c = 50 relaxation sweeps per V-cycle (Table 1).  On the
+// general path a sweep is ~8 launches whose work is a few hundred flops each at 4^3, so the
+// V-cycle is launch-latency bound.  Here ONE launch runs `nsweeps` complete sweeps (for
+// n = 1..N, M = Z_(n)Phi^(n) (eq:gradEqn), Gamma = *_{k != n} A^(k)T A^(k) (eq:Gamma),
+// A^(n) Gamma = M + F (eq:relaxinnersolve P:356-358) by Cholesky) with Z, every factor and every
+// Gram resident in shared memory, and returns f, f~ after the last sweep exactly as
+// cp_als_sweep does (readings R5, R6).  Every sum has a fixed order: bitwise reproducible.
+#include "cp_internal.cuh"
+#include "small_sweep.cuh"
+
+namespace cpk {
+
+namespace {
+constexpr int kT = kSmallSweepThreads;
+
+// fixed-order block sum of one value per thread (red: kT doubles); result in every thread
+__device__ double block_sum_fixed(double v, double *red) {
+  const int tid = threadIdx.x;
+  __syncthreads();
+  red[tid] = v;
+  __syncthreads();
+  for (int off = kT / 2; off > 0; off >>= 1) {
+    if (tid < off) red[tid] += red[tid + off];
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const SmallSweepArgs a) {
+  griddep();
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x, N = a.N, R = a.R, RR = R * R;
+  const int64_t P = a.P;
+  // shared layout (doubles): Z | A^(0..N-1) | Ups^(0..N-1) | M | part | WL | WR | Gam | L | red
+  double *sZ = sm;
+  // factor offsets and dims in shared memory (dynamically indexed: no local-memory copies)
+  __shared__ int s_aoff[CP_MAX_N], s_dims[CP_MAX_N];
+  int64_t off = P;
+  for (int k = 0; k < N; ++k) {
+    if (tid == 0) {
+      s_aoff[k] = (int)off;
+      s_dims[k] = (int)a.dims[k];
+    }
+    off += a.dims[k] * R;
+  }
+  double *sU = sm + off;
+  off += (int64_t)N * RR;
+  double *sM = sm + off;
+  off += a.imax * R;
+  double *part = sm + off;
+  off += a.npart + a.lr * R;  // part | WL | WR
+  double *sG = sm + off;
+  off += RR;
+  double *sL = sm + off;
+  off += RR;
+  double *red = sm + off;
+  __shared__ int s_status, s_failed;
+
+  __syncthreads();
+  for (int64_t e = tid; e < P; e += kT) sZ[e] = a.Z[e];
+  for (int k = 0; k < N; ++k)
+    for (int64_t e = tid; e < s_dims[k] * R; e += kT) (sm + s_aoff[k])[e] = a.A[k][e];
+  if (tid == 0) {
+    s_status = 0;
+    s_failed = -1;
+  }
+  __syncthreads();
+  // Upsilon^(k) = A^(k)T A^(k), sum over i ascending
+  for (int e = tid; e < N * RR; e += kT) {
+    const int k = e / RR, rs = e - k * RR, r = rs % R, s = rs / R;
+    const double *x = (sm + s_aoff[k]) + s_dims[k] * r, *y = (sm + s_aoff[k]) + s_dims[k] * s;
+    double g = 0.0;
+    for (int64_t i = 0; i < s_dims[k]; ++i) g = fma(x[i], y[i], g);
+    sU[e] = g;
+  }
+  __syncthreads();
+
+  double inner_last = 0.0;
+  for (int sweep = 0; sweep < a.nsweeps && s_status == 0; ++sweep) {
+    for (int n = 0; n < N; ++n) {
+      // Z viewed as left x I_n x right (left = prod_{k<n} I_k); the Khatri-Rao row of column
+      // (a, b) is WL(a, :) * WR(b, :) with WL = the left modes' rows (P:110 order), WR the right
+      const int In = (int)s_dims[n];
+      int left = 1, right = 1;
+      for (int k = 0; k < n; ++k) left *= (int)s_dims[k];
+      for (int k = n + 1; k < N; ++k) right *= (int)s_dims[k];
+      double *sWL = part + a.npart, *sWR = sWL + (int64_t)left * R;
+      for (int e = tid; e < (left + right) * R; e += kT) {
+        const bool isl = e < left * R;
+        const int ee = isl ? e : e - left * R;
+        const int len = isl ? left : right;
+        int c = ee % len;
+        const int r = ee / len;
+        double w = 1.0;
+        for (int k = isl ? 0 : n + 1; k < (isl ? n : N); ++k) {
+          const int Ik = (int)s_dims[k];
+          const int ik = c % Ik;
+          c /= Ik;
+          w *= (sm + s_aoff[k])[ik + Ik * r];
+        }
+        (isl ? sWL : sWR)[ee] = w;  // ee = c + len * r
+      }
+      __syncthreads();
+      // ---- M(i, r) = sum_{a,b} z(a, i, b) WL(a, r) WR(b, r) (eq:gradEqn): unit = (o, segment) ----
+      const int Q = left * right;
+      const int nout = In * R;
+      const int S = nout >= kT ? 1 : kT / nout;  // column segments per output entry
+      const int units = nout * S;
+      for (int u = tid; u < units; u += kT) {
+        const int o = u / S, sg = u - o * S;
+        const int i = o % In, r = o / In;
+        const int q0 = (int)(((int64_t)Q * sg) / S), q1 = (int)(((int64_t)Q * (sg + 1)) / S);
+        int aa = q0 % left, bb = q0 / left;
+        const double *wl = sWL + left * r, *wr = sWR + right * r;
+        const double *zrow = sZ + left * i;
+        const int bstride = left * In;
+        double acc = 0.0;
+        for (int q = q0; q < q1; ++q) {
+          acc = fma(zrow[aa + bstride * bb], wl[aa] * wr[bb], acc);
+          if (++aa == left) {
+            aa = 0;
+            ++bb;
+          }
+        }
+        part[u] = acc;
+      }
+      __syncthreads();
+      for (int o = tid; o < nout; o += kT) {
+        double m = 0.0;
+        for (int sg = 0; sg < S; ++sg) m += part[o * S + sg];
+        sM[o] = m;
+      }
+      // Gamma^(n) = *_{k != n} Upsilon^(k) (eq:Gamma)
+      for (int e = tid; e < RR; e += kT) {
+        double g = 1.0;
+        for (int k = 0; k < N; ++k)
+          if (k != n) g *= sU[k * RR + e];
+        sG[e] = g;
+      }
+      __syncthreads();
+      // ---- Gamma = L L^T, lower, no pivoting; pivot <= 0 -> CP_ENOTSPD ----
+      if (tid == 0) {
+        for (int e = 0; e < RR; ++e) sL[e] = 0.0;
+        for (int j = 0; j < R && s_status == 0; ++j) {
+          double d = sG[j + R * j];
+          for (int k = 0; k < j; ++k) d -= sL[j + R * k] * sL[j + R * k];
+          if (!(d > 0.0)) {
+            s_status = CP_ENOTSPD;
+            s_failed = n;
+            break;
+          }
+          const double ljj = sqrt(d);
+          sL[j + R * j] = ljj;
+          for (int i = j + 1; i < R; ++i) {
+            double s = sG[i + R * j];
+            for (int k = 0; k < j; ++k) s -= sL[i + R * k] * sL[j + R * k];
+            sL[i + R * j] = s / ljj;
+          }
+        }
+      }
+      __syncthreads();
+      if (s_status != 0) break;
+      // ---- each row: L y = (m + f)^T, L^T x^T = y (eq:relaxinnersolve) ----
+      const double *F = a.F[n];
+      __syncthreads();  // (part is reused for y below)
+      for (int i = tid; i < In; i += kT) {
+        double *y = part + (int64_t)i * R;
+        for (int r = 0; r < R; ++r) {
+          double b = sM[i + In * r] + (F != nullptr ? F[i + In * r] : 0.0);
+          for (int k = 0; k < r; ++k) b -= sL[r + R * k] * y[k];
+          y[r] = b / sL[r + R * r];
+        }
+        for (int r = R - 1; r >= 0; --r) {
+          double x = y[r];
+          for (int k = r + 1; k < R; ++k) x -= sL[k + R * r] * y[k];
+          y[r] = x / sL[r + R * r];
+          (sm + s_aoff[n])[i + In * r] = y[r];
+        }
+      }
+      __syncthreads();
+      // Upsilon^(n) of the new factor
+      for (int e = tid; e < RR; e += kT) {
+        const int r = e % R, s = e / R;
+        const double *x = (sm + s_aoff[n]) + In * r, *y = (sm + s_aoff[n]) + In * s;
+        double g = 0.0;
+        for (int i = 0; i < In; ++i) g = fma(x[i], y[i], g);
+        sU[n * RR + e] = g;
+      }
+      if (n == N - 1 && sweep == a.nsweeps - 1) {
+        double d = 0.0;
+        for (int o = tid; o < nout; o += kT) d = fma(sM[o], (sm + s_aoff[n])[o], d);
+        inner_last = block_sum_fixed(d, red);
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- write back, f and f~ (readings R6, R5) ----
+  for (int k = 0; k < N; ++k)
+    for (int64_t e = tid; e < s_dims[k] * R; e += kT) a.A[k][e] = (sm + s_aoff[k])[e];
+  if (s_status != 0) {
+    if (tid == 0) {
+      a.out[0] = nan("");
+      a.out[1] = nan("");
+      a.out[2] = (double)s_status;
+      a.out[3] = (double)s_failed;
+    }
+    return;
+  }
+  double m2 = 0.0;
+  for (int e = tid; e < RR; e += kT) {
+    double p = 1.0;
+    for (int k = 0; k < N; ++k) p *= sU[k * RR + e];
+    m2 += p;
+  }
+  const double model2 = block_sum_fixed(m2, red);
+  double fa = 0.0;
+  for (int k = 0; k < N; ++k)
+    if (a.F[k] != nullptr)
+      for (int64_t e = tid; e < s_dims[k] * R; e += kT) fa = fma(a.F[k][e], (sm + s_aoff[k])[e], fa);
+  const double fas = block_sum_fixed(fa, red);
+  if (tid == 0) {
+    const double f = 0.5 * a.normZ2[0] - inner_last + 0.5 * model2;
+    a.out[0] = f;
+    a.out[1] = f - fas;
+    a.out[2] = 0.0;
+    a.out[3] = -1.0;
+  }
+}
+
+size_t small_sweep_smem_bytes(const cp_shape &s) {
+  if (s.R > kSmallSweepMaxR) return 0;
+  double P = 1.0;
+  int64_t imax = 1, sumI = 0;
+  for (int k = 0; k < s.N; ++k) {
+    P *= (double)s.dims[k];
+    sumI += s.dims[k];
+    if (s.dims[k] > imax) imax = s.dims[k];
+  }
+  if (P > (double)kSmallSweepMaxP) return 0;
+  const int64_t npart = imax * s.R > kT ? imax * s.R : kT;
+  double lr = 0.0;  // Khatri-Rao halves WL, WR of the largest mode geometry
+  for (int n = 0; n < s.N; ++n) {
+    double left = 1.0, right = 1.0;
+    for (int k = 0; k < n; ++k) left *= (double)s.dims[k];
+    for (int k = n + 1; k < s.N; ++k) right *= (double)s.dims[k];
+    if (left + right > lr) lr = left + right;
+  }
+  const double d = P + (double)sumI * s.R + (double)s.N * s.R * s.R + (double)imax * s.R + (double)npart +
+                   lr * s.R + 2.0 * s.R * s.R + kT;
+  return (size_t)(d * 8.0);
+}
+
+cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double *normZ2, double *const *A,
+                               const double *const *F, int nsweeps, double *out, cudaStream_t st) {
+  SmallSweepArgs a;
+  memset(&a, 0, sizeof(a));
+  a.N = s.N;
+  a.R = s.R;
+  a.nsweeps = nsweeps;
+  a.P = 1;
+  a.imax = 1;
+  for (int k = 0; k < s.N; ++k) {
+    a.dims[k] = s.dims[k];
+    a.P *= s.dims[k];
+    if (s.dims[k] > a.imax) a.imax = s.dims[k];
+    a.A[k] = A[k];
+    a.F[k] = (F != nullptr) ? F[k] : nullptr;
+  }
+  a.npart = a.imax * s.R > kT ? a.imax * s.R : kT;
+  a.lr = 0;
+  for (int n = 0; n < s.N; ++n) {
+    int64_t left = 1, right = 1;
+    for (int k = 0; k < n; ++k) left *= s.dims[k];
+    for (int k = n + 1; k < s.N; ++k) right *= s.dims[k];
+    if (left + right > a.lr) a.lr = left + right;
+  }
+  a.Z = Z;
+  a.normZ2 = normZ2;
+  a.out = out;
+  const size_t smem = small_sweep_smem_bytes(s);
+  static size_t attr_set = 0;
+  if (smem > 48 * 1024 && smem > attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(small_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = smem;
+  }
+  return launch_k(small_sweep_kernel, dim3(1), dim3(kT), smem, st, a);
+}
+
+}  // namespace cpk

@@ -1,0 +1,32 @@
+// Fused multi-sweep ALS / BNGS kernel for tensors resident in one CTA's shared memory
+// (small_sweep.cu).  Used by cp_als_sweep / cp_als_sweeps when small_sweep_smem_bytes() != 0.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cstring>
+#include <cuda_runtime.h>
+
+#include "../../include/cp.h"
+
+namespace cpk {
+
+constexpr int kSmallSweepThreads = 512;
+constexpr int kSmallSweepMaxR = 32;
+constexpr int64_t kSmallSweepMaxP = 16384;  // 128 KiB of Z: one CTA streams it faster than ~8 launches
+
+struct SmallSweepArgs {
+  int N, R, nsweeps;
+  int64_t P, imax, npart, lr;  // lr: max over modes of left + right (Khatri-Rao halves)
+  int64_t dims[CP_MAX_N];
+  const double *Z, *normZ2;
+  double *A[CP_MAX_N];
+  const double *F[CP_MAX_N];
+  double *out;
+};
+
+// dynamic shared memory the kernel needs for shape s, or 0 if s is not small enough
+size_t small_sweep_smem_bytes(const cp_shape &s);
+cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double *normZ2, double *const *A,
+                               const double *const *F, int nsweeps, double *out, cudaStream_t st);
+
+}  // namespace cpk

@@ -129,3 +129,33 @@ def test_als_solve_graph_replay_is_bitwise_the_plain_loop(monkeypatch):
     assert r1["g"] == r0["g"]
     for a, b in zip(A1, A0g):
         assert np.array_equal(a, b)
+
+
+def test_mg_graph_replayed_v_cycles_are_bitwise_the_plain_launches(monkeypatch):
+    """The solve phase replays each FAS V-cycle as one captured CUDA graph (no host
+    synchronization inside a cycle: H(A) by cp_gradient, enqueued only).  Same kernels in the same
+    order: factors, cycle count and g trace equal the plain-launch run (CP_MG_GRAPH=0) bitwise,
+    including with FMG and on the paper's dense problem."""
+    for name, R, fmg in (("c1", None, 1), ("dense", 2, 0)):
+        if name == "dense":
+            dims = (24, 24, 24)
+            Z = cpsynth.dense_inverse_norm(24)
+            A0 = cpsynth.uniform_init(dims, R, seed=0)
+        else:
+            d = cpsynth.make_config(name, with_transfer=False)
+            dims, R, Z, A0 = d["dims"], d["R"], d["Z"], d["A0"]
+        T0 = [cpsynth.uniform_init(dims, R, seed=10 + t) for t in range(2)]
+        Af = cpsynth.uniform_init(cp.mg_levels(dims, R)[-1], R, seed=99)
+        res = []
+        for graph in ("1", "0"):
+            monkeypatch.setenv("CP_MG_GRAPH", graph)
+            Ad = [dev_factor(a) for a in A0]
+            prm = cp.MGParams.default(use_fmg=fmg, tol=1e-9, max_cycles=30)
+            rep, tr = cp.mg_solve(dev_tensor(Z), dims, Ad, [[dev_factor(t) for t in b] for b in T0],
+                                  A_fmg=[dev_factor(a) for a in Af], params=prm)
+            res.append(([host_factor(a) for a in Ad], rep, tr))
+        (A1, r1, t1), (A0_, r0, t0) = res
+        assert int(r1["cycles"]) == int(r0["cycles"]) and int(r1["status"]) == int(r0["status"])
+        np.testing.assert_array_equal(t1[:, :3], t0[:, :3])
+        for a, b in zip(A1, A0_):
+            np.testing.assert_array_equal(a, b)
