@@ -8,10 +8,18 @@
 // A^(n) Gamma = M + F (eq:relaxinnersolve P:356-358) by Cholesky) with Z, every factor and every
 // Gram resident in shared memory, and returns f, f~ after the last sweep exactly as
 // cp_als_sweep does (readings R5, R6).  Every sum has a fixed order: bitwise reproducible.
+#include <cstdio>
+
 #include "cp_internal.cuh"
 #include "small_sweep.cuh"
 
 namespace cpk {
+
+#ifdef CP_SMALL_TIMING
+#define ST(k) if (threadIdx.x == 0 && sweep == 1) tst[k] = clock64();
+#else
+#define ST(k)
+#endif
 
 namespace {
 constexpr int kT = kSmallSweepThreads;
@@ -61,6 +69,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
   off += RR;
   double *red = sm + off;
   __shared__ int s_status, s_failed;
+  __shared__ double sDi[kSmallSweepMaxR];  // 1 / L(r, r)
 
   __syncthreads();
   for (int64_t e = tid; e < P; e += kT) sZ[e] = a.Z[e];
@@ -82,10 +91,14 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
   __syncthreads();
 
   double inner_last = 0.0;
+#ifdef CP_SMALL_TIMING
+  long long tst[16] = {0};
+#endif
   for (int sweep = 0; sweep < a.nsweeps && s_status == 0; ++sweep) {
     for (int n = 0; n < N; ++n) {
       // Z viewed as left x I_n x right (left = prod_{k<n} I_k); the Khatri-Rao row of column
       // (a, b) is WL(a, :) * WR(b, :) with WL = the left modes' rows (P:110 order), WR the right
+      if (n == 0) ST(0);
       const int In = (int)s_dims[n];
       int left = 1, right = 1;
       for (int k = 0; k < n; ++k) left *= (int)s_dims[k];
@@ -107,15 +120,19 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
         (isl ? sWL : sWR)[ee] = w;  // ee = c + len * r
       }
       __syncthreads();
+      if (n == 0) ST(1);
       // ---- M(i, r) = sum_{a,b} z(a, i, b) WL(a, r) WR(b, r) (eq:gradEqn): unit = (o, segment) ----
       const int Q = left * right;
       const int nout = In * R;
-      const int S = nout >= kT ? 1 : kT / nout;  // column segments per output entry
+      // column segments per output entry: enough units for the block, but >= 8 columns each
+      // (the segment partials are summed serially below)
+      int S = nout >= kT ? 1 : kT / nout;
+      if (S > (Q + 7) / 8) S = (Q + 7) / 8;
       const int units = nout * S;
       for (int u = tid; u < units; u += kT) {
         const int o = u / S, sg = u - o * S;
         const int i = o % In, r = o / In;
-        const int q0 = (int)(((int64_t)Q * sg) / S), q1 = (int)(((int64_t)Q * (sg + 1)) / S);
+        const int q0 = (Q * sg) / S, q1 = (Q * (sg + 1)) / S;  // (Q * S <= 16384 * 512)
         int aa = q0 % left, bb = q0 / left;
         const double *wl = sWL + left * r, *wr = sWR + right * r;
         const double *zrow = sZ + left * i;
@@ -131,6 +148,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
         part[u] = acc;
       }
       __syncthreads();
+      if (n == 0) ST(2);
       for (int o = tid; o < nout; o += kT) {
         double m = 0.0;
         for (int sg = 0; sg < S; ++sg) m += part[o * S + sg];
@@ -144,6 +162,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
         sG[e] = g;
       }
       __syncthreads();
+      if (n == 0) ST(3);
       // ---- Gamma = L L^T, lower, no pivoting; pivot <= 0 -> CP_ENOTSPD ----
       if (tid == 0) {
         for (int e = 0; e < RR; ++e) sL[e] = 0.0;
@@ -155,16 +174,18 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
             s_failed = n;
             break;
           }
-          const double ljj = sqrt(d);
+          const double ljj = sqrt(d), rj = 1.0 / ljj;
           sL[j + R * j] = ljj;
+          sDi[j] = rj;
           for (int i = j + 1; i < R; ++i) {
             double s = sG[i + R * j];
             for (int k = 0; k < j; ++k) s -= sL[i + R * k] * sL[j + R * k];
-            sL[i + R * j] = s / ljj;
+            sL[i + R * j] = s * rj;
           }
         }
       }
       __syncthreads();
+      if (n == 0) ST(4);
       if (s_status != 0) break;
       // ---- each row: L y = (m + f)^T, L^T x^T = y (eq:relaxinnersolve) ----
       const double *F = a.F[n];
@@ -174,16 +195,17 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
         for (int r = 0; r < R; ++r) {
           double b = sM[i + In * r] + (F != nullptr ? F[i + In * r] : 0.0);
           for (int k = 0; k < r; ++k) b -= sL[r + R * k] * y[k];
-          y[r] = b / sL[r + R * r];
+          y[r] = b * sDi[r];
         }
         for (int r = R - 1; r >= 0; --r) {
           double x = y[r];
           for (int k = r + 1; k < R; ++k) x -= sL[k + R * r] * y[k];
-          y[r] = x / sL[r + R * r];
+          y[r] = x * sDi[r];
           (sm + s_aoff[n])[i + In * r] = y[r];
         }
       }
       __syncthreads();
+      if (n == 0) ST(5);
       // Upsilon^(n) of the new factor
       for (int e = tid; e < RR; e += kT) {
         const int r = e % R, s = e / R;
@@ -201,6 +223,11 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
     }
   }
 
+#ifdef CP_SMALL_TIMING
+  if (threadIdx.x == 0)
+    printf("small sweep phases (clk, mode 0 of sweep 1): wlwr %lld mttkrp %lld msum+gamma %lld chol %lld solve %lld\n",
+           tst[1] - tst[0], tst[2] - tst[1], tst[3] - tst[2], tst[4] - tst[3], tst[5] - tst[4]);
+#endif
   // ---- write back, f and f~ (readings R6, R5) ----
   for (int k = 0; k < N; ++k)
     for (int64_t e = tid; e < s_dims[k] * R; e += kT) a.A[k][e] = (sm + s_aoff[k])[e];
