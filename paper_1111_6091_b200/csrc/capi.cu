@@ -586,8 +586,15 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
   p.part = w + L.part;
   if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
   const ReduceGeom g = reduce_geom(p);
-  if (launch_k(reduce_mttkrp_kernel, dim3(L.nsolve[mode]), dim3(256), 0, cs, g, L.rpc[mode], L.sp[mode], M) != cudaSuccess)
+  if (g.mode0 && !g.direct && env_int("CP_REDUCE0_COALESCED", 1)) {
+    const int64_t S = g.In_rows * g.R;
+    if (launch_k(reduce_mode0_kernel, dim3((unsigned)ceil_div(S, 32)), dim3(256), 0, cs, (const double *)g.part, g.Gc,
+                 S, M) != cudaSuccess)
+      return CP_ECUDA;
+  } else if (launch_k(reduce_mttkrp_kernel, dim3(L.nsolve[mode]), dim3(256), 0, cs, g, L.rpc[mode], L.sp[mode], M) !=
+             cudaSuccess) {
     return CP_ECUDA;
+  }
   g_launches = 3;
   return CP_OK;
 }

@@ -160,6 +160,7 @@ struct FitFinalArgs {
 };
 
 __global__ void reduce_mttkrp_kernel(const ReduceGeom g, int rpc, int sp, double *M);
+__global__ void reduce_mode0_kernel(const double *part, int Gc, int64_t S, double *M);
 __global__ void finalize_sweep_kernel(const FinalizeArgs a);
 __global__ void gradient_kernel(const GradArgs a);
 __global__ void finalize_fit_kernel(const FitFinalArgs a);
