@@ -376,7 +376,7 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
     # a7: restriction Z x_1 Phat^T (dense orthonormal Phat, I_1 -> ceil(I_1/2))
     Ph = d["Phat"][0]
     U = torch.from_numpy(np.ascontiguousarray(Ph)).to(dev).t()  # (Ic x I1) column-major = Phat^T
-    from paper_1111_6091_b200 import colmajor
+    from paper_1111_6091_b200 import colmajor, empty_factor
     U = colmajor(U)
     J = U.shape[0]
     nd = list(dims)
@@ -416,6 +416,26 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
         rows[f"restriction_structured_mode{n}"] = {"ms": t, "alg_GBps": alg / t / 1e6,
                                                    "frac_hbm": alg / t / 1e6 / (json.load(open(PEAKS_PATH)).get("hbm_gbs", FALLBACK_HBM) if os.path.exists(PEAKS_PATH) else FALLBACK_HBM)}
         del X
+    # the 4-way roofline point of BASELINE.json configs[4] (c4b: 96^4, R = 10): the sweep (two
+    # dimension-tree passes) and every MTTKRP, on device-random data (timing does not depend on
+    # the values; the c4b parity tests use the config's own tensor)
+    if tuple(dims) != (96, 96, 96, 96):
+        d4, R4 = (96, 96, 96, 96), 10
+        P4 = 96 ** 4
+        Z4 = torch.randn(d4, dtype=torch.float64, device=dev)
+        A4 = [colmajor(torch.randn(I, R4, dtype=torch.float64, device=dev)) for I in d4]
+        ws4 = cp.Workspace(d4, R4)
+        nz4 = cp.norm2(Z4, d4, ws=ws4)
+        out4 = torch.empty(4, dtype=torch.float64, device=dev)
+        t = timed(lambda: cp.als_sweep(Z4, d4, A4, nz4, out=out4, ws=ws4), n=20)
+        rows["c4b_sweep"] = {"ms": t, "sweeps_per_s": 1e3 / t, "z_passes": 2,
+                             "alg_GBps_2pass": 2 * 8.0 * P4 / t / 1e6}
+        M4 = [empty_factor(I, R4, dev) for I in d4]
+        for n in range(4):
+            t = timed(lambda: cp.mttkrp(Z4, d4, A4, n, M=M4[n], ws=ws4))
+            alg = 8.0 * (P4 + sum(d4[k] * R4 for k in range(4) if k != n) + d4[n] * R4)
+            rows[f"c4b_mttkrp_mode{n}"] = {"ms": t, "alg_GBps": alg / t / 1e6}
+        del Z4, A4, ws4, M4
     # 8(d): full multigrid solve time to a stated g tolerance -- BASELINE.json config c1
     # (50^3, R = 3, C = 0.9: BAMG setup + FAS V-cycles to ||grad f|| <= 1e-9), ML and ML+FMG,
     # beside the plain ALS solve to the same tolerance; seconds include the stopping tests
