@@ -7,6 +7,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "gamma_job.cuh"
 #include "mg_kernels.cuh"
 #include "small_sweep.cuh"
@@ -355,6 +357,42 @@ static double stream_alg_bytes(const StreamPlan &p) {
   return 8.0 * (P + fac + out);
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// The stage tensor map of an MMA plan (StreamPlan::use_tmap), when the plan qualifies: the row
+// block is the whole column (RB = 1) and padded (zcs > Wb: the out-of-bounds box rows fill the
+// padding with zeros), 16-byte row strides, box within the TMA limits (<= 256 per dimension).
+static bool encode_stage_tmap(StreamPlan &p) {
+  if (p.RB != 1 || p.zcs <= p.I1 || p.zcs > 256 || p.cps > 256 || (p.I1 & 1) || p.V < 2) return false;
+  if (p.op == OP_RESID) return false;  // (residual pass: its own column stride; per-column copies)
+  const int64_t qs = p.qsd[0];
+  if (qs < 1 || p.Q % qs != 0 || p.Q / qs > 0xffffffffLL || qs > 0xffffffffLL) return false;
+  if ((p.zst * 8) % 128 != 0) return false;  // stage slots must stay 128-B aligned
+  auto enc = tmap_encoder();
+  if (enc == nullptr) return false;
+  const cuuint64_t gdim[3] = {(cuuint64_t)p.I1, (cuuint64_t)qs, (cuuint64_t)(p.Q / qs)};
+  const cuuint64_t gstride[2] = {(cuuint64_t)p.I1 * 8, (cuuint64_t)(p.I1 * qs * 8)};
+  const cuuint32_t box[3] = {(cuuint32_t)p.zcs, 1u, (cuuint32_t)p.cps};
+  const cuuint32_t estride[3] = {1u, 1u, 1u};
+  const CUresult r = enc(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(p.Z), gdim, gstride, box,
+                         estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 cudaError_t launch_stream(const StreamPlan &p0, cudaStream_t st) {
   StreamPlan p = p0;
   {
@@ -366,6 +404,8 @@ cudaError_t launch_stream(const StreamPlan &p0, cudaStream_t st) {
     for (int k = 0; k < p.N; ++k) P *= (double)p.dims[k];
     if (keep_mb > 0 && p.V >= 2 && 8.0 * P >= 96.0 * (1 << 20)) p.keep_q = (keep_mb << 20) / (8 * p.I1);
   }
+  p.use_tmap = 0;
+  if (p.mma && env_int("CP_STREAM_TMAP", 1)) p.use_tmap = encode_stage_tmap(p) ? 1 : 0;
   const StreamEntry &e = p.mma ? stream_mma_entry(p.nt, p.mt, p.op) : stream_entry(p.R, p.V, p.op);
   ++g_launches;
   const bool prof = g_prof_on && g_prof_n < kProfMax;

@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 #include <utility>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/cp.h"
@@ -78,6 +79,12 @@ struct StreamPlan {
   int64_t keep_q;   // L2 residency across passes: Z columns q < keep_q are fetched with an
                     // evict_last policy, the rest evict_first (0: no hints).  See DESIGN 6.8.
   int dbg;          // experiments only (env CP_STREAM_DBG): 1 = consumers skip the FMAs, 2 = weight warp skips forming
+  // MMA plans whose row block is the whole column (RB = 1): one 3-D tensor-map TMA per full
+  // stage instead of one bulk copy per column.  View {I1, qsd[0], Q / qsd[0]} of Z, box
+  // {zcs, 1, cps}: the stage's columns are consecutive along dim 2, and the box rows past I1
+  // are out of bounds -> zero-filled padding of the zcs column slots (no extra HBM bytes).
+  int use_tmap;
+  alignas(64) CUtensorMap tmap;
 };
 
 // Kernel table: one entry per (R, V, op) instantiation of stream_kernel.
@@ -204,6 +211,23 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// 3-D tensor-map TMA (box -> shared memory, complete_tx on the stage barrier)
+__device__ __forceinline__ void tma_load_3d(void *dst_smem, const CUtensorMap *map, int c0, int c1, int c2,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_hint(void *dst_smem, const CUtensorMap *map, int c0, int c1, int c2,
+                                                 uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 // The same copy with an L2 eviction-priority policy (createpolicy; evict_last / evict_first).

@@ -148,9 +148,10 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
         for (int j = 1; j < kMaxDigits; ++j)
           if (j < nd && p.ord[j] != p.mode) ++nslow;
       }
+      const bool tstage = p.use_tmap && ncols == p.cps;  // full stage: one tensor-map TMA
+      const uint32_t zbytes = tstage ? (uint32_t)(p.zcs * p.cps * 8) : (uint32_t)(ncols * Wb * 8);
       if (lane == 0)
-        mbar_expect_tx(&sm.full[stage],
-                       (uint32_t)(ncols * Wb * 8 + (has_f0 ? ncols * p.RS * 8 : 0) + nslow * p.RS * 8));
+        mbar_expect_tx(&sm.full[stage], zbytes + (has_f0 ? ncols * p.RS * 8 : 0) + nslow * p.RS * 8);
       __syncwarp();
       if (p.srows) {
         // the factor rows of the slow digits (constant over the stage), one copy each
@@ -162,7 +163,16 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       }
       // Z columns: q advances by qsd[0] per column within a stage (digit 0 only).  Strided
       // columns are issued by all 32 lanes (one bulk copy per column).
-      if (p.RB == 1 && p.qsd[0] == 1 && p.zcs == 0) {
+      if (tstage) {
+        if (lane == 0) {
+          const int64_t qs = p.qsd[0];
+          const int c1 = (int)(q0 % qs), c2 = (int)(q0 / qs);
+          if (p.keep_q > 0)
+            tma_load_3d_hint(zs, &p.tmap, 0, c1, c2, &sm.full[stage], q0 < p.keep_q ? pol_keep : pol_stream);
+          else
+            tma_load_3d(zs, &p.tmap, 0, c1, c2, &sm.full[stage]);
+        }
+      } else if (p.RB == 1 && p.qsd[0] == 1 && p.zcs == 0) {
         if (lane == 0) {
           if (p.keep_q > 0)
             bulk_g2s_hint(zs, p.Z + q0 * p.I1, (uint32_t)(ncols * Wb * 8), &sm.full[stage],
