@@ -377,7 +377,6 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 // padding with zeros), 16-byte row strides, box within the TMA limits (<= 256 per dimension).
 static bool encode_stage_tmap(StreamPlan &p) {
   if (p.RB != 1 || p.zcs <= p.I1 || p.zcs > 256 || p.cps > 256 || (p.I1 & 1) || p.V < 2) return false;
-  if (p.op == OP_RESID) return false;  // (residual pass: its own column stride; per-column copies)
   const int64_t qs = p.qsd[0];
   if (qs < 1 || p.Q % qs != 0 || p.Q / qs > 0xffffffffLL || qs > 0xffffffffLL) return false;
   if ((p.zst * 8) % 128 != 0) return false;  // stage slots must stay 128-B aligned
