@@ -120,6 +120,12 @@ static bool plan_mma_ok(const StreamPlan &p, const cp_shape &s, int op) {
   return !(env_int("CP_STREAM_MMA", 1) == 0 || (op == OP_RESID && env_int("CP_RESID_MMA", 1) == 0) || s.R > 32 ||
            (p.I1 & 1));
 }
+// row block = the whole (even) column, padded column slots within the TMA box limit: the stage
+// can be one tensor-map TMA whose out-of-bounds rows fill the padding (launch_stream)
+static bool tmap_geometry_ok(const StreamPlan &p) {
+  return p.mma && p.RB == 1 && p.zcs > p.I1 && p.zcs <= 256 && (p.I1 & 1) == 0 && p.V >= 2;
+}
+
 static bool plan_mma(StreamPlan &p, const cp_shape &s, int op) {
   if (!plan_mma_ok(p, s, op)) return false;
   p.nt = (s.R + 7) / 8;
@@ -184,9 +190,12 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   const int WSTR = (s.R % 2 == 0) ? s.R + 2 : s.R + 1;
   p.RS = s.R + (s.R & 1);
   // stage size: tools/sweep*.sh (DFMA consumers), tools/plan_sweep.py (MMA: 2 stages of ~52 KB)
-  const int stage_target = env_int("CP_STAGE_BYTES", plan_mma_ok(p, s, op) ? 53248 : 40960);
+  int stage_target = env_int("CP_STAGE_BYTES", plan_mma_ok(p, s, op) ? 53248 : 40960);
   int cps, cpt = 1;
   if (plan_mma(p, s, op)) {
+    // whole-column row blocks loaded by one tensor-map TMA per stage (launch_stream): 3 stages
+    // of ~26 KB beat 2 of ~52 KB (c4b MTTKRP 0.153 -> 0.143 ms; tools/sweep_c4b.sh)
+    if (tmap_geometry_ok(p) && env_int("CP_STREAM_TMAP", 1)) stage_target = env_int("CP_STAGE_BYTES", 26624);
     // stage: a multiple of 4 KS columns (k-steps of every k-group)
     const int unit = 4 * p.ks;
     cps = stage_target / (p.zcs * 8);
@@ -376,7 +385,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 // block is the whole column (RB = 1) and padded (zcs > Wb: the out-of-bounds box rows fill the
 // padding with zeros), 16-byte row strides, box within the TMA limits (<= 256 per dimension).
 static bool encode_stage_tmap(StreamPlan &p) {
-  if (p.RB != 1 || p.zcs <= p.I1 || p.zcs > 256 || p.cps > 256 || (p.I1 & 1) || p.V < 2) return false;
+  if (!tmap_geometry_ok(p) || p.cps > 256) return false;
   const int64_t qs = p.qsd[0];
   if (qs < 1 || p.Q % qs != 0 || p.Q / qs > 0xffffffffLL || qs > 0xffffffffLL) return false;
   if ((p.zst * 8) % 128 != 0) return false;  // stage slots must stay 128-B aligned
