@@ -972,6 +972,8 @@ int cp_mode_product(int32_t N, const int64_t *dims, const double *Z, int32_t mod
   return CP_OK;
 }
 
+static bool use_small_sweep(const cp_shape &s);
+
 // cp_fit (resid = true: f by the residual pass) and cp_gradient (resid = false: no residual
 // pass, f by the expansion from the last mode's <M, A> and the Grams)
 static int fit_impl(const cp_shape *s, const double *Z, const double *normZ2, const double *const *A,
@@ -989,6 +991,12 @@ static int fit_impl(const cp_shape *s, const double *Z, const double *normZ2, co
   double *w = static_cast<double *>(ws);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   const int N = s->N, R = s->R;
+  if (!resid && use_small_sweep(*s)) {  // small tensor: the fused shared-memory kernel (gradient mode)
+    if (launch_small_sweep(*s, Z, normZ2, const_cast<double *const *>(A), F, 1, out, cs, G, true) != cudaSuccess)
+      return CP_ECUDA;
+    g_launches = 1;
+    return CP_OK;
+  }
   PrepArgs pa;
   PrepGrams pg;
   fill_prep(*s, L, w, A, -1, true, nullptr, pa, pg);

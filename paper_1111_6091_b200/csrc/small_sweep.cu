@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
   }
   __syncthreads();
 
-  double inner_last = 0.0;
+  double inner_last = 0.0, gsum = 0.0;
 #ifdef CP_SMALL_TIMING
   long long tst[16] = {0};
 #endif
@@ -163,6 +163,27 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
       }
       __syncthreads();
       if (n == 0) ST(3);
+      if (a.grad) {
+        // ---- cp_gradient: G = -M + A Gamma - F at this iterate (eq:gradEqn), ||G||^2 ----
+        const double *Fg = a.F[n];
+        double *G = a.G[n];
+        const double *An = sm + s_aoff[n];
+        double g2 = 0.0, d = 0.0;
+        for (int o = tid; o < nout; o += kT) {
+          const int i = o % In, r = o / In;
+          double gv = -sM[o];
+          for (int t = 0; t < R; ++t) gv = fma(An[i + In * t], sG[t + R * r], gv);
+          if (Fg != nullptr) gv -= Fg[o];
+          if (G != nullptr) G[o] = gv;
+          g2 = fma(gv, gv, g2);
+          if (n == N - 1) d = fma(sM[o], An[o], d);
+        }
+        const double g2s = block_sum_fixed(g2, red);
+        if (tid == 0) a.out[2 + n] = g2s;
+        gsum += g2s;
+        if (n == N - 1) inner_last = block_sum_fixed(d, red);
+        continue;
+      }
       // ---- Gamma = L L^T, lower, no pivoting; pivot <= 0 -> CP_ENOTSPD ----
       if (tid == 0) {
         for (int e = 0; e < RR; ++e) sL[e] = 0.0;
@@ -228,6 +249,21 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
     printf("small sweep phases (clk, mode 0 of sweep 1): wlwr %lld mttkrp %lld msum+gamma %lld chol %lld solve %lld\n",
            tst[1] - tst[0], tst[2] - tst[1], tst[3] - tst[2], tst[4] - tst[3], tst[5] - tst[4]);
 #endif
+  if (a.grad) {
+    // f by the expansion (reading R6), g = (sum_n ||G^(n)||^2)^{1/2} / ||Z|| (eq:gradConv)
+    double m2 = 0.0;
+    for (int e = tid; e < RR; e += kT) {
+      double p = 1.0;
+      for (int k = 0; k < N; ++k) p *= sU[k * RR + e];
+      m2 += p;
+    }
+    const double model2 = block_sum_fixed(m2, red);
+    if (tid == 0) {
+      a.out[0] = 0.5 * a.normZ2[0] - inner_last + 0.5 * model2;
+      a.out[1] = sqrt(gsum) / sqrt(a.normZ2[0]);
+    }
+    return;
+  }
   // ---- write back, f and f~ (readings R6, R5) ----
   for (int k = 0; k < N; ++k)
     for (int64_t e = tid; e < s_dims[k] * R; e += kT) a.A[k][e] = (sm + s_aoff[k])[e];
@@ -285,9 +321,12 @@ size_t small_sweep_smem_bytes(const cp_shape &s) {
 }
 
 cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double *normZ2, double *const *A,
-                               const double *const *F, int nsweeps, double *out, cudaStream_t st) {
+                               const double *const *F, int nsweeps, double *out, cudaStream_t st,
+                               double *const *G, bool grad) {
   SmallSweepArgs a;
   memset(&a, 0, sizeof(a));
+  a.grad = grad ? 1 : 0;
+  for (int k = 0; k < s.N; ++k) a.G[k] = (G != nullptr) ? G[k] : nullptr;
   a.N = s.N;
   a.R = s.R;
   a.nsweeps = nsweeps;
@@ -297,7 +336,7 @@ cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double 
     a.dims[k] = s.dims[k];
     a.P *= s.dims[k];
     if (s.dims[k] > a.imax) a.imax = s.dims[k];
-    a.A[k] = A[k];
+    a.A[k] = const_cast<double *>(A[k]);
     a.F[k] = (F != nullptr) ? F[k] : nullptr;
   }
   a.npart = a.imax * s.R > kT ? a.imax * s.R : kT;

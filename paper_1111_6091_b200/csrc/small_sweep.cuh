@@ -22,11 +22,14 @@ struct SmallSweepArgs {
   double *A[CP_MAX_N];
   const double *F[CP_MAX_N];
   double *out;
+  int grad;               // 1: cp_gradient at this iterate (no updates): out = f, g, ||G^(n)||^2
+  double *G[CP_MAX_N];    // gradient mode: G^(n) outputs (entries may be null)
 };
 
 // dynamic shared memory the kernel needs for shape s, or 0 if s is not small enough
 size_t small_sweep_smem_bytes(const cp_shape &s);
 cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double *normZ2, double *const *A,
-                               const double *const *F, int nsweeps, double *out, cudaStream_t st);
+                               const double *const *F, int nsweeps, double *out, cudaStream_t st,
+                               double *const *G = nullptr, bool grad = false);
 
 }  // namespace cpk

@@ -380,30 +380,35 @@ def test_fit_configs(name):
 
 @pytest.mark.parametrize("dims,R", [((5, 7, 3), 3), ((20, 20, 20), 3), ((2, 3, 2, 3), 2), ((700, 5, 4), 16),
                                     ((33, 29, 31), 16), ((9, 8, 7, 6), 5), ((11, 13), 4), ((6, 5, 4, 3, 2), 3)])
-def test_gradient_ragged(dims, R):
+def test_gradient_ragged(dims, R, monkeypatch):
     """cp_gradient: g, ||G^(n)||^2, G against the oracle's gradient (eq:gradEqn,
-    eq:gradConv) and f against the oracle's expansion (reading R6); g and G are bitwise cp_fit's
-    (same kernels, same order: only the residual pass is dropped)."""
+    eq:gradConv) and f against the oracle's expansion (reading R6), on both paths (small tensors:
+    the fused shared-memory kernel in gradient mode); on the general path (CP_SMALL_SWEEP=0) g and
+    G are bitwise cp_fit's (same kernels, same order: only the residual pass is dropped)."""
     Z, A = cpsynth.random_problem(dims, R, seed=R + 60)
     F = [0.1 * cpsynth.random_matrix(I, R, k) for k, I in enumerate(dims)]
     half = 0.5 * float(np.vdot(Z, Z))
-    for Fuse in (None, F):
-        Zd, Ad = dev_problem(Z, A)
-        Fd = None if Fuse is None else [dev_factor(f) for f in Fuse]
-        nz = cp.norm2(Zd, dims)
-        out, G = cp.gradient(Zd, dims, Ad, nz, F=Fd, want_G=True)
-        outf, Gf = cp.fit(Zd, dims, Ad, nz, F=Fd, want_G=True)
-        out, outf = host_tensor(out), host_tensor(outf)
-        oo, Go = oracle.gradient(Z, dims, A, F=Fuse)
-        fe = oracle.f_expand(Z, dims, A)
-        assert abs(out[0] - fe) <= 1e-10 * abs(fe) + 1e-14 * half
-        assert abs(out[1] - oo[1]) <= 1e-10 * abs(oo[1]) + 1e-13
-        assert np.array_equal(out[1:], outf[1:])
-        for n in range(len(dims)):
-            g = host_factor(G[n])
-            assert relerr(g, Go[n]) <= 1e-11
-            assert np.array_equal(g, host_factor(Gf[n]))
-            assert abs(out[2 + n] - oo[2 + n]) <= 1e-10 * oo[2 + n] + 1e-24
+    for path in ("1", "0"):
+        monkeypatch.setenv("CP_SMALL_SWEEP", path)
+        for Fuse in (None, F):
+            Zd, Ad = dev_problem(Z, A)
+            Fd = None if Fuse is None else [dev_factor(f) for f in Fuse]
+            nz = cp.norm2(Zd, dims)
+            out, G = cp.gradient(Zd, dims, Ad, nz, F=Fd, want_G=True)
+            outf, Gf = cp.fit(Zd, dims, Ad, nz, F=Fd, want_G=True)
+            out, outf = host_tensor(out), host_tensor(outf)
+            oo, Go = oracle.gradient(Z, dims, A, F=Fuse)
+            fe = oracle.f_expand(Z, dims, A)
+            assert abs(out[0] - fe) <= 1e-10 * abs(fe) + 1e-14 * half
+            assert abs(out[1] - oo[1]) <= 1e-10 * abs(oo[1]) + 1e-13
+            if path == "0":
+                assert np.array_equal(out[1:], outf[1:])
+            for n in range(len(dims)):
+                g = host_factor(G[n])
+                assert relerr(g, Go[n]) <= 1e-11
+                if path == "0":
+                    assert np.array_equal(g, host_factor(Gf[n]))
+                assert abs(out[2 + n] - oo[2 + n]) <= 1e-10 * oo[2 + n] + 1e-24
 
 
 @pytest.mark.parametrize("name", ["c0", "c1", "c2", "c3"])
