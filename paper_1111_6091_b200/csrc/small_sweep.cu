@@ -121,39 +121,37 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
       }
       __syncthreads();
       if (n == 0) ST(1);
-      // ---- M(i, r) = sum_{a,b} z(a, i, b) WL(a, r) WR(b, r) (eq:gradEqn): unit = (o, segment) ----
+      // ---- M(i, r) = sum_{a,b} z(a, i, b) WL(a, r) WR(b, r) (eq:gradEqn): a warp per output
+      // entry, its lanes stride over the columns q = a + left b, fixed xor-tree reduction ----
       const int Q = left * right;
       const int nout = In * R;
-      // column segments per output entry: enough units for the block, but >= 8 columns each
-      // (the segment partials are summed serially below)
-      int S = nout >= kT ? 1 : kT / nout;
-      if (S > (Q + 7) / 8) S = (Q + 7) / 8;
-      const int units = nout * S;
-      for (int u = tid; u < units; u += kT) {
-        const int o = u / S, sg = u - o * S;
-        const int i = o % In, r = o / In;
-        const int q0 = (Q * sg) / S, q1 = (Q * (sg + 1)) / S;  // (Q * S <= 16384 * 512)
-        int aa = q0 % left, bb = q0 / left;
-        const double *wl = sWL + left * r, *wr = sWR + right * r;
-        const double *zrow = sZ + left * i;
+      {
+        const int warp = tid >> 5, lane = tid & 31;
         const int bstride = left * In;
-        double acc = 0.0;
-        for (int q = q0; q < q1; ++q) {
-          acc = fma(zrow[aa + bstride * bb], wl[aa] * wr[bb], acc);
-          if (++aa == left) {
-            aa = 0;
-            ++bb;
+        for (int o = warp; o < nout; o += kT / 32) {
+          const int i = o % In, r = o / In;
+          const double *wl = sWL + left * r, *wr = sWR + right * r;
+          const double *zrow = sZ + left * i;
+          double acc = 0.0;
+          if (left == 1) {
+            const double w0 = wl[0];
+            for (int q = lane; q < Q; q += 32) acc = fma(zrow[bstride * q], w0 * wr[q], acc);
+          } else if (right == 1) {
+            const double w0 = wr[0];
+            for (int q = lane; q < Q; q += 32) acc = fma(zrow[q], wl[q] * w0, acc);
+          } else {
+            for (int q = lane; q < Q; q += 32) {
+              const int bb = q / left, aa = q - bb * left;
+              acc = fma(zrow[aa + bstride * bb], wl[aa] * wr[bb], acc);
+            }
           }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+          if (lane == 0) sM[o] = acc;
         }
-        part[u] = acc;
       }
       __syncthreads();
       if (n == 0) ST(2);
-      for (int o = tid; o < nout; o += kT) {
-        double m = 0.0;
-        for (int sg = 0; sg < S; ++sg) m += part[o * S + sg];
-        sM[o] = m;
-      }
       // Gamma^(n) = *_{k != n} Upsilon^(k) (eq:Gamma)
       for (int e = tid; e < RR; e += kT) {
         double g = 1.0;
