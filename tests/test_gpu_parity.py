@@ -250,6 +250,25 @@ def test_fused_small_multi_sweep_vs_oracle(dims, R, F):
     _check_sweep([host_factor(a) for a in Ad], out, Ao, oo, nz2)
 
 
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_multi_sweep_call_general_path_vs_oracle(name):
+    """cp_als_sweeps on tensors above the fused-kernel limit (P > 16384): nu = 3 general-path
+    sweeps in one call equal 3 oracle sweeps (the coarse-level relaxations of large
+    hierarchies), F included."""
+    d = config(name)
+    dims, Z, A = d["dims"], d["Z"], d["A0"]
+    R = A[0].shape[1]
+    nz2 = float(np.vdot(Z, Z))
+    Fh = [0.01 * cpsynth.random_matrix(I, R, 30 + k) for k, I in enumerate(dims)]
+    Zd, Ad = dev_problem(Z, A)
+    out = host_tensor(cp.als_sweep(Zd, dims, Ad, cp.norm2(Zd, dims), F=[dev_factor(f) for f in Fh], nsweeps=3))
+    assert cp.last_launch_count() > 3
+    Ao = [a.copy(order="F") for a in A]
+    for _ in range(3):
+        Ao, oo = oracle.als_sweep(Z, dims, Ao, F=Fh, normZ2=nz2)
+    _check_sweep([host_factor(a) for a in Ad], out, Ao, oo, nz2)
+
+
 def test_fused_small_sweep_reports_enotspd_mid_run():
     """Z = 0: the mode-0 update gives A^(0) = 0, so Gamma^(1) = 0 is singular in the first sweep of
     a multi-sweep call: status CP_ENOTSPD, failed mode 1, f = NaN -- as the oracle reports."""
