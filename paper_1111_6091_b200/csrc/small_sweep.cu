@@ -24,6 +24,17 @@ namespace cpk {
 namespace {
 constexpr int kT = kSmallSweepThreads;
 
+// 1/sqrt(x), x > 0: rsqrt.approx.f64 + two Newton steps (as ys_rsqrt in ylsolve.cu): no
+// square root or division on the serial Cholesky chain
+__device__ __forceinline__ double ss_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx, y * y, 1.5);
+  y = y * fma(-hx, y * y, 1.5);
+  return y;
+}
+
 // fixed-order block sum of one value per thread (red: kT doubles); result in every thread
 __device__ double block_sum_fixed(double v, double *red) {
   const int tid = threadIdx.x;
@@ -193,7 +204,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
             s_failed = n;
             break;
           }
-          const double ljj = sqrt(d), rj = 1.0 / ljj;
+          const double rj = ss_rsqrt(d), ljj = d * rj;
           sL[j + R * j] = ljj;
           sDi[j] = rj;
           for (int i = j + 1; i < R; ++i) {
