@@ -443,6 +443,7 @@ struct Layout {
   cp_shape s3;
   int rpc2, sp2, nyr;
   size_t yl, edge, mbuf, yr, segtab, m0part, linv;
+  size_t med;  // medium fused sweep (medium_sweep.cu): barrier counter + partial M buffers
 };
 
 static size_t align_up(size_t x) { return (x + 31) & ~(size_t)31; }  // 256 B in doubles
@@ -529,6 +530,7 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     L.yr = off; off = align_up(off + (size_t)L.s3.dims[2] * R);
     L.segtab = off; off = align_up(off + (size_t)(s.dims[1] * y.RB + 1) / 2);  // u32 ticket per (segment, row block)
   }
+  L.med = off; off = align_up(off + medium_sweep_ws_doubles(s));
   L.total = off * sizeof(double);
   return true;
 }
@@ -680,6 +682,19 @@ int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, doub
       return CP_ECUDA;
     g_launches = 1;
     return CP_OK;
+  }
+  {
+    // medium tensors: one cooperative launch for all nsweeps (medium_sweep.cu).  Opt-in
+    // (CP_MEDIUM_SWEEP=1): measured slower than the general path so far (c1 50^3: 57 vs 46 us
+    // per sweep, c2 100^3: 98 vs 54) -- DESIGN 6.7
+    const int G = env_int("CP_MEDIUM_SWEEP", 0) ? medium_sweep_ctas(*s, device_sms()) : 0;
+    if (G > 0 && medium_sweep_smem_bytes(*s, G) <= 200 * 1024) {
+      if (launch_medium_sweep(*s, G, Z, normZ2, A, F, nsweeps, out, static_cast<double *>(ws) + L.med,
+                              reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return CP_ECUDA;
+      g_launches = 1;
+      return CP_OK;
+    }
   }
   int total = 0;
   for (int k = 0; k < nsweeps; ++k) {

@@ -165,6 +165,7 @@ def sweep_path(request, monkeypatch):
     """cp_als_sweep runs tensors with P <= 16384 through the fused shared-memory kernel
     (small_sweep.cu); CP_SMALL_SWEEP=0 forces the general multi-kernel path."""
     monkeypatch.setenv("CP_SMALL_SWEEP", "1" if request.param == "fused_small" else "0")
+    monkeypatch.setenv("CP_MEDIUM_SWEEP", "1" if request.param == "fused_small" else "0")  # (opt-in kernel)
     return request.param
 
 
@@ -251,10 +252,13 @@ def test_fused_small_multi_sweep_vs_oracle(dims, R, F):
 
 
 @pytest.mark.parametrize("name", ["c1", "c2"])
-def test_multi_sweep_call_general_path_vs_oracle(name):
-    """cp_als_sweeps on tensors above the fused-kernel limit (P > 16384): nu = 3 general-path
-    sweeps in one call equal 3 oracle sweeps (the coarse-level relaxations of large
-    hierarchies), F included."""
+@pytest.mark.parametrize("medium", ["1", "0"])
+def test_multi_sweep_call_general_path_vs_oracle(name, medium, monkeypatch):
+    """cp_als_sweeps on tensors above the single-CTA fused-kernel limit (P > 16384): nu = 3
+    sweeps in one call -- one cooperative launch of the medium fused kernel (medium_sweep.cu),
+    or with CP_MEDIUM_SWEEP=0 the general multi-kernel path -- equal 3 oracle sweeps, F
+    included."""
+    monkeypatch.setenv("CP_MEDIUM_SWEEP", medium)
     d = config(name)
     dims, Z, A = d["dims"], d["Z"], d["A0"]
     R = A[0].shape[1]
@@ -262,7 +266,7 @@ def test_multi_sweep_call_general_path_vs_oracle(name):
     Fh = [0.01 * cpsynth.random_matrix(I, R, 30 + k) for k, I in enumerate(dims)]
     Zd, Ad = dev_problem(Z, A)
     out = host_tensor(cp.als_sweep(Zd, dims, Ad, cp.norm2(Zd, dims), F=[dev_factor(f) for f in Fh], nsweeps=3))
-    assert cp.last_launch_count() > 3
+    assert (cp.last_launch_count() == 1) if medium == "1" else (cp.last_launch_count() > 3)
     Ao = [a.copy(order="F") for a in A]
     for _ in range(3):
         Ao, oo = oracle.als_sweep(Z, dims, Ao, F=Fh, normZ2=nz2)
