@@ -12,6 +12,8 @@
 //     pivots); every row solved; the new Gram.  All CTAs hold bitwise-identical factor copies in
 //     shared memory, so no broadcast is needed.
 // f, f~ as cp_als_sweep (readings R5, R6), written by CTA 0.
+#include <cstdlib>
+
 #include "cp_internal.cuh"
 #include "small_sweep.cuh"
 
@@ -61,7 +63,7 @@ __device__ bool grid_barrier(unsigned *cnt, unsigned target) {
         ok = 0;
         break;
       }
-      __nanosleep(32);
+      __nanosleep(spins < 8 ? 64 : 256);
     }
     s_ok = ok;
   }
@@ -303,7 +305,11 @@ int medium_sweep_ctas(const cp_shape &s, int sms) {
   double P = 1.0;
   for (int k = 0; k < s.N; ++k) P *= (double)s.dims[k];
   if (P <= (double)kSmallSweepMaxP || P > (double)kMediumSweepMaxP) return 0;
-  int G = (int)((P + 6143.0) / 6144.0);
+  static const double per = [] {
+    const char *e = getenv("CP_MEDIUM_ELEMS");
+    return (e && *e) ? atof(e) : 6144.0;
+  }();
+  int G = (int)((P + per - 1.0) / per);
   if (G > sms) G = sms;
   if (G < 2) G = 2;
   return G;
