@@ -416,6 +416,40 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
         rows[f"restriction_structured_mode{n}"] = {"ms": t, "alg_GBps": alg / t / 1e6,
                                                    "frac_hbm": alg / t / 1e6 / (json.load(open(PEAKS_PATH)).get("hbm_gbs", FALLBACK_HBM) if os.path.exists(PEAKS_PATH) else FALLBACK_HBM)}
         del X
+    # BASELINE.json configs[3] (c3: 256^3, R = 8, 128 MiB ~ L2): the sweep and the MTTKRP of every
+    # mode, L2 flushed (256 MiB write) before each rep and each rep timed by its own event pair
+    if tuple(dims) != (256, 256, 256):
+        d3, R3 = (256, 256, 256), 8
+        P3 = 256 ** 3
+        Z3 = torch.randn(d3, dtype=torch.float64, device=dev)
+        A3 = [colmajor(torch.randn(I, R3, dtype=torch.float64, device=dev)) for I in d3]
+        ws3 = cp.Workspace(d3, R3)
+        nz3 = cp.norm2(Z3, d3, ws=ws3)
+        out3 = torch.empty(4, dtype=torch.float64, device=dev)
+        fl = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
+
+        def flushed(fn, n=20):
+            fn()
+            tot = 0.0
+            for _ in range(n):
+                fl.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+                e1.synchronize()
+                tot += e0.elapsed_time(e1)
+            return tot / n
+
+        t = flushed(lambda: cp.als_sweep(Z3, d3, A3, nz3, out=out3, ws=ws3))
+        rows["c3_sweep"] = {"ms": t, "sweeps_per_s": 1e3 / t, "z_passes": 2,
+                            "alg_GBps_2pass": 2 * 8.0 * P3 / t / 1e6, "l2": "flushed before each rep"}
+        M3 = [empty_factor(I, R3, dev) for I in d3]
+        for n in range(3):
+            t = flushed(lambda: cp.mttkrp(Z3, d3, A3, n, M=M3[n], ws=ws3))
+            alg = 8.0 * (P3 + sum(d3[k] * R3 for k in range(3) if k != n) + d3[n] * R3)
+            rows[f"c3_mttkrp_mode{n}"] = {"ms": t, "alg_GBps": alg / t / 1e6, "l2": "flushed before each rep"}
+        del Z3, A3, ws3, M3, fl
     # the 4-way roofline point of BASELINE.json configs[4] (c4b: 96^4, R = 10): the sweep (two
     # dimension-tree passes) and every MTTKRP, on device-random data (timing does not depend on
     # the values; the c4b parity tests use the config's own tensor)
