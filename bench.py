@@ -304,6 +304,13 @@ def main():
                 "timed_region": "a second K-step loop of the same sweep with CUDA events around every "
                                 "streaming-kernel launch (the headline loop runs without them)",
                 "frac_of_8TBs_nominal": (achieved / 8000.0) if achieved else None}
+    # the whole step against the same peak: the sweep's algorithmic bytes (every streaming launch
+    # of one sweep, as counted for the kernel above) at the copy peak vs the measured step time
+    step_bytes = prof_bytes / max(1, args.steps) if nlaunch_prof < 8192 else float("nan")  # (cp.h: 8192 recorded launches)
+    step_ms = t_max / args.steps
+    roofline["step"] = {"alg_bytes": step_bytes, "bound_ms": step_bytes / (peak * 1e9) * 1e3,
+                        "frac": (step_bytes / (peak * 1e9) * 1e3) / step_ms if step_ms > 0 else None,
+                        "note": "sweeps/s as a fraction of its HBM roofline (all N modes' Z passes at the peak)"}
 
     # ---- extra rows (same run, outside the timed region)
     rows = {}
