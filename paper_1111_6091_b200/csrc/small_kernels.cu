@@ -107,7 +107,10 @@ __global__ void __launch_bounds__(256) reduce_mode0_kernel(const double *part, i
 // RS) and the chunk's partial Gram A_chunk^T A_chunk, summed later in chunk order.
 __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
   griddep();
-  __shared__ double sA[kPrepRows * 33];  // chunk x R, column-major (r * kPrepRows + ii)
+  // chunk x R, column-major (r * kPrepLd + ii); the odd column stride keeps the Gram loop's
+  // 16 different r of a warp in 16 different banks (stride 64 put them all in one bank)
+  constexpr int kPrepLd = kPrepRows + 1;
+  __shared__ double sA[kPrepLd * 32];
   int k = 0;
   while (k + 1 < a.N && (int)blockIdx.x >= a.blk_off[k + 1]) ++k;
   const int b = blockIdx.x - a.blk_off[k];
@@ -129,17 +132,17 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
   const int n = (int)((I - i0) < kPrepRows ? (I - i0) : kPrepRows);
   for (int e = tid; e < n * R; e += blockDim.x) {
     const int r = e / n, ii = e - (e / n) * n;
-    sA[r * kPrepRows + ii] = A[(i0 + ii) + I * r];
+    sA[r * kPrepLd + ii] = A[(i0 + ii) + I * r];
   }
   __syncthreads();
   for (int e = tid; e < n * RS; e += blockDim.x) {
     const int ii = e / RS, r = e - (e / RS) * RS;
-    At[(i0 + ii) * RS + r] = (r < R) ? sA[r * kPrepRows + ii] : 0.0;
+    At[(i0 + ii) * RS + r] = (r < R) ? sA[r * kPrepLd + ii] : 0.0;
   }
   if (a.gpre != nullptr) {
     for (int e = tid; e < RR; e += blockDim.x) {
       const int r = e % R, s = e / R;
-      const double *ar = sA + r * kPrepRows, *as = sA + s * kPrepRows;
+      const double *ar = sA + r * kPrepLd, *as = sA + s * kPrepLd;
       // 4 independent chains (the single 64-long fma chain dominated this kernel)
       double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
       int ii = 0;
