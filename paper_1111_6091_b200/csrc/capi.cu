@@ -530,7 +530,13 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     L.yr = off; off = align_up(off + (size_t)L.s3.dims[2] * R);
     L.segtab = off; off = align_up(off + (size_t)(s.dims[1] * y.RB + 1) / 2);  // u32 ticket per (segment, row block)
   }
-  L.med = off; off = align_up(off + medium_sweep_ws_doubles(s));
+  {
+    // the medium fused sweep's barrier + partial M buffers, only for shapes it can run
+    const int G = medium_sweep_ctas(s, sms);
+    const bool med = G > 0 && medium_sweep_smem_bytes(s, G) <= 200 * 1024;
+    L.med = off;
+    off = align_up(off + (med ? medium_sweep_ws_doubles(s, G) : 0));
+  }
   L.total = off * sizeof(double);
   return true;
 }

@@ -331,11 +331,11 @@ size_t medium_sweep_smem_bytes(const cp_shape &s, int G) {
   return (size_t)(d * 8.0);
 }
 
-size_t medium_sweep_ws_doubles(const cp_shape &s) {
+size_t medium_sweep_ws_doubles(const cp_shape &s, int G) {
   int64_t imax = 1;
   for (int k = 0; k < s.N; ++k)
     if (s.dims[k] > imax) imax = s.dims[k];
-  return (size_t)(2 * 160 * imax * s.R + imax * s.R + 32);  // 2 partial buffers + M
+  return (size_t)(2 * (int64_t)G * imax * s.R + imax * s.R + 32);  // 2 partial buffers + M
 }
 
 cudaError_t launch_medium_sweep(const cp_shape &s, int G, const double *Z, const double *normZ2, double *const *A,

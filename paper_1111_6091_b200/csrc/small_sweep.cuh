@@ -34,7 +34,7 @@ constexpr int64_t kMediumSweepMaxP = 1536 * 1024;  // medium_sweep.cu: ~6 K elem
 // doubles (barrier + partial M buffers) and the cooperative launch
 int medium_sweep_ctas(const cp_shape &s, int sms);
 size_t medium_sweep_smem_bytes(const cp_shape &s, int G);
-size_t medium_sweep_ws_doubles(const cp_shape &s);
+size_t medium_sweep_ws_doubles(const cp_shape &s, int G);
 cudaError_t launch_medium_sweep(const cp_shape &s, int G, const double *Z, const double *normZ2, double *const *A,
                                 const double *const *F, int nsweeps, double *out, double *ws, cudaStream_t st);
 
