@@ -387,7 +387,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 static bool encode_stage_tmap(StreamPlan &p) {
   if (!tmap_geometry_ok(p) || p.cps > 256) return false;
   const int64_t qs = p.qsd[0];
-  if (qs < 1 || p.Q % qs != 0 || p.Q / qs > 0xffffffffLL || qs > 0xffffffffLL) return false;
+  if (qs < 1 || p.Q % qs != 0 || p.Q / qs > 0x7fffffffLL || qs > 0x7fffffffLL) return false;  // (int32 TMA coordinates)
   if ((p.zst * 8) % 128 != 0) return false;  // stage slots must stay 128-B aligned
   auto enc = tmap_encoder();
   if (enc == nullptr) return false;
