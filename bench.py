@@ -490,6 +490,9 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
         rows["mg_solve_c1"] = mgb.run("c1", tol=1e-9)
         # and the paper's own dense problem (Table 4 context: s = 50, R = 2)
         rows["mg_solve_dense50_R2"] = mgb.run("dense50", R=2, tol=1e-9)
+        # s = 100, R = 3 (Table 4 context: ML+FMG 9 cycles): the case where the multigrid beats ALS
+        mgb.run("dense100", R=3, tol=1e-10)  # warm-up (plans, graphs)
+        rows["mg_solve_dense100_R3"] = mgb.run("dense100", R=3, tol=1e-10)
     except Exception as e:  # the row is informative; the sweep metric stands without it
         rows["mg_solve_c1"] = {"error": repr(e)}
     # the same sweep with the DFMA streaming consumers (CP_STREAM_MMA=0: FP64 tensor cores only in
