@@ -113,13 +113,17 @@ int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, doubl
                  cp_stream_t stream);
 
 /* nsweeps >= 1 consecutive cp_als_sweep calls (the nu relaxations of a multigrid level, Table 1
- * P:462-478), out = the values after the last sweep; a numeric failure stops at the failing
- * sweep.  For a tensor small enough to live in one CTA's shared memory (P <= 16384, the coarse
- * levels) all nsweeps run in ONE launch of a fused kernel; otherwise it loops the general
- * sweep.  Same arguments and errors as cp_als_sweep (nsweeps < 1: CP_EINVAL). */
+ * P:462-478), out = the values after the last sweep (f, f~ before any normalization); a numeric
+ * failure stops at the failing sweep.  flags: 0, or CP_SWEEPS_NORMALIZE = each sweep followed
+ * by the eq:ALSnorm normalization without sorting (= cp_normalize_sort(sort = 0)), the
+ * ALS relaxation of the setup phase.  For a tensor small enough to live in one CTA's shared
+ * memory (P <= 16384, the coarse levels) all nsweeps (and normalizations) run in ONE launch of a
+ * fused kernel; otherwise it loops the general sweep (+ cp_normalize_sort).  Same arguments and
+ * errors as cp_als_sweep (nsweeps < 1 or unknown flags: CP_EINVAL). */
+#define CP_SWEEPS_NORMALIZE 1
 int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
-                  const double *const *F, int32_t nsweeps, double *out, void *ws, size_t ws_bytes,
-                  cp_stream_t stream);
+                  const double *const *F, int32_t nsweeps, int32_t flags, double *out, void *ws,
+                  size_t ws_bytes, cp_stream_t stream);
 
 /* n-mode product X = Z x_mode U  (X_(n) = U Z_(n))
  *   dims [host] N sizes of Z;  U: J x dims[mode], column-major;  X: dims with dims[mode] -> J.

@@ -167,9 +167,11 @@ def mttkrp(Z, dims, A, mode, M=None, ws=None, stream=None):
     return M
 
 
-def als_sweep(Z, dims, A, normZ2, F=None, out=None, ws=None, stream=None, nsweeps=1):
-    """nsweeps (default 1) ALS/BNGS sweeps, A updated in place.  Returns the device tensor
-    out = [f, f_tilde, status, failed_mode] after the last one (cp_als_sweep / cp_als_sweeps)."""
+def als_sweep(Z, dims, A, normZ2, F=None, out=None, ws=None, stream=None, nsweeps=1, normalize=False):
+    """nsweeps (default 1) ALS/BNGS sweeps, A updated in place; normalize=True follows every sweep
+    by the eq:ALSnorm normalization without sorting (CP_SWEEPS_NORMALIZE).  Returns the device
+    tensor out = [f, f_tilde, status, failed_mode] after the last sweep (cp_als_sweep /
+    cp_als_sweeps)."""
     _check_Z(Z, dims)
     R = A[0].shape[1]
     for k, a in enumerate(A):
@@ -182,13 +184,14 @@ def als_sweep(Z, dims, A, normZ2, F=None, out=None, ws=None, stream=None, nsweep
         Fp = _ptr_array(list(F))
     out = torch.empty(4, dtype=torch.float64, device=Z.device) if out is None else out
     ws = _ws(ws, dims, R, Z.device)
-    if nsweeps == 1:
+    if nsweeps == 1 and not normalize:
         _check(lib().cp_als_sweep(ctypes.byref(_shape(dims, R)), _ptr(Z), _ptr(normZ2), _ptr_array(A),
                                   Fp, _ptr(out), _ptr(ws.buf), ctypes.c_size_t(ws.nbytes),
                                   _stream(stream)), "cp_als_sweep")
     else:
         _check(lib().cp_als_sweeps(ctypes.byref(_shape(dims, R)), _ptr(Z), _ptr(normZ2), _ptr_array(A),
-                                   Fp, ctypes.c_int32(int(nsweeps)), _ptr(out), _ptr(ws.buf),
+                                   Fp, ctypes.c_int32(int(nsweeps)), ctypes.c_int32(1 if normalize else 0),
+                                   _ptr(out), _ptr(ws.buf),
                                    ctypes.c_size_t(ws.nbytes), _stream(stream)), "cp_als_sweeps")
     return out
 

@@ -50,7 +50,7 @@ def lib():
         L.cp_norm2.argtypes = [vp, vp, vp, vp, sz, vp]
         L.cp_mttkrp.argtypes = [vp, vp, vp, i32, vp, vp, sz, vp]
         L.cp_als_sweep.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, vp]
-        L.cp_als_sweeps.argtypes = [vp, vp, vp, vp, vp, i32, vp, vp, sz, vp]
+        L.cp_als_sweeps.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, vp, sz, vp]
         L.cp_mode_product_workspace_bytes.argtypes = [i32, vp, i32, i64]
         L.cp_mode_product_workspace_bytes.restype = sz
         L.cp_mode_product.argtypes = [i32, vp, vp, i32, vp, i64, vp, vp, sz, vp]

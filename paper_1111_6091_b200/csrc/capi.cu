@@ -443,7 +443,8 @@ struct Layout {
   cp_shape s3;
   int rpc2, sp2, nyr;
   size_t yl, edge, mbuf, yr, segtab, m0part, linv;
-  size_t med;  // medium fused sweep (medium_sweep.cu): barrier counter + partial M buffers
+  size_t med;   // medium fused sweep (medium_sweep.cu): barrier counter + partial M buffers
+  size_t ntmp;  // cp_als_sweeps with CP_SWEEPS_NORMALIZE: normalization scratch (sum_n I_n R)
 };
 
 static size_t align_up(size_t x) { return (x + 31) & ~(size_t)31; }  // 256 B in doubles
@@ -536,6 +537,12 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     const bool med = G > 0 && medium_sweep_smem_bytes(s, G) <= 200 * 1024;
     L.med = off;
     off = align_up(off + (med ? medium_sweep_ws_doubles(s, G) : 0));
+  }
+  {
+    size_t sumIR = 0;
+    for (int k = 0; k < s.N; ++k) sumIR += (size_t)s.dims[k] * R;
+    L.ntmp = off;
+    off = align_up(off + sumIR);
   }
   L.total = off * sizeof(double);
   return true;
@@ -667,24 +674,26 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
 int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
                  const double *const *F, double *out, void *ws, size_t ws_bytes,
                  cp_stream_t stream) {
-  return cp_als_sweeps(s, Z, normZ2, A, F, 1, out, ws, ws_bytes, stream);
+  return cp_als_sweeps(s, Z, normZ2, A, F, 1, 0, out, ws, ws_bytes, stream);
 }
 
 int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
-                  const double *const *F, int32_t nsweeps, double *out, void *ws, size_t ws_bytes,
-                  cp_stream_t stream) {
+                  const double *const *F, int32_t nsweeps, int32_t flags, double *out, void *ws,
+                  size_t ws_bytes, cp_stream_t stream) {
   g_launches = 0;
   int st = check_shape(s, 2);
   if (st) return st;
-  if (!Z || !normZ2 || !A || !out || !aligned(Z, 16) || nsweeps < 1) return CP_EINVAL;
+  if (!Z || !normZ2 || !A || !out || !aligned(Z, 16) || nsweeps < 1 || (flags & ~CP_SWEEPS_NORMALIZE))
+    return CP_EINVAL;
+  const bool norm = (flags & CP_SWEEPS_NORMALIZE) != 0;
   for (int k = 0; k < s->N; ++k)
     if (A[k] == nullptr) return CP_EINVAL;
   Layout L;
   if (!make_layout(L, *s)) return CP_EINVAL;
   if ((st = check_ws(L, ws, ws_bytes))) return st;
   if (use_small_sweep(*s)) {
-    if (launch_small_sweep(*s, Z, normZ2, A, F, nsweeps, out, reinterpret_cast<cudaStream_t>(stream)) !=
-        cudaSuccess)
+    if (launch_small_sweep(*s, Z, normZ2, A, F, nsweeps, out, reinterpret_cast<cudaStream_t>(stream), nullptr,
+                           false, norm) != cudaSuccess)
       return CP_ECUDA;
     g_launches = 1;
     return CP_OK;
@@ -694,7 +703,7 @@ int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, doub
     // (CP_MEDIUM_SWEEP=1): measured slower than the general path so far (c1 50^3: 57 vs 46 us
     // per sweep, c2 100^3: 98 vs 54) -- DESIGN 6.7
     const int G = env_int("CP_MEDIUM_SWEEP", 0) ? medium_sweep_ctas(*s, device_sms()) : 0;
-    if (G > 0 && medium_sweep_smem_bytes(*s, G) <= 200 * 1024) {
+    if (G > 0 && !norm && medium_sweep_smem_bytes(*s, G) <= 200 * 1024) {
       if (launch_medium_sweep(*s, G, Z, normZ2, A, F, nsweeps, out, static_cast<double *>(ws) + L.med,
                               reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
         return CP_ECUDA;
@@ -706,6 +715,22 @@ int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, doub
   for (int k = 0; k < nsweeps; ++k) {
     if ((st = sweep_impl(s, Z, normZ2, A, F, out, ws, ws_bytes, stream))) return st;
     total += g_launches;
+    if (norm) {  // cp_normalize_sort(sort = 0) with the sweep workspace's own scratch region
+      NormArgs na;
+      memset(&na, 0, sizeof(na));
+      na.N = s->N;
+      na.R = s->R;
+      int64_t o = 0;
+      for (int n = 0; n < s->N; ++n) {
+        na.dims[n] = s->dims[n];
+        na.A[n] = A[n];
+        na.off[n] = o;
+        o += s->dims[n] * s->R;
+      }
+      na.tmp = static_cast<double *>(ws) + L.ntmp;
+      if (launch_normalize_sort(na, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess) return CP_ECUDA;
+      ++total;
+    }
   }
   g_launches = total;
   return CP_OK;

@@ -176,16 +176,15 @@ struct MG {
   // ALS relaxation of the setup phase: sweep + normalization, every level
   void relax_setup(int l, double *const *A, int sweeps) {
     Level &v = lv[l];
-    for (int k = 0; k < sweeps && err == CP_OK; ++k) {
-      ok(cp_als_sweep(&v.s, v.Z, v.nz2, A, nullptr, out_sweep, ws, ws_bytes, cst));
-      ok(cp_normalize_sort(&v.s, A, 0, nullptr, ws, ws_bytes, cst));
-    }
+    // sweep + normalization (no sort) nu times: one fused launch on small levels
+    if (sweeps > 0)
+      ok(cp_als_sweeps(&v.s, v.Z, v.nz2, A, nullptr, sweeps, CP_SWEEPS_NORMALIZE, out_sweep, ws, ws_bytes, cst));
   }
   // BNGS with RHS (eq:relaxinnersolve); finest level: normalize + sort
   void relax_fas(int l, double *const *A, const double *const *F, int sweeps) {
     Level &v = lv[l];
     if (l > 0) {  // coarse levels: no normalization between sweeps -> one call (fused when small)
-      if (sweeps > 0) ok(cp_als_sweeps(&v.s, v.Z, v.nz2, A, F, sweeps, out_sweep, ws, ws_bytes, cst));
+      if (sweeps > 0) ok(cp_als_sweeps(&v.s, v.Z, v.nz2, A, F, sweeps, 0, out_sweep, ws, ws_bytes, cst));
       return;
     }
     for (int k = 0; k < sweeps && err == CP_OK; ++k) {

@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
   }
   __syncthreads();
 
-  double inner_last = 0.0, gsum = 0.0;
+  double inner_last = 0.0, gsum = 0.0, model2_last = 0.0, fa_last = 0.0;
 #ifdef CP_SMALL_TIMING
   long long tst[16] = {0};
 #endif
@@ -251,6 +251,64 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
       }
       __syncthreads();
     }
+    if (a.grad || s_status != 0) continue;
+    if (sweep == a.nsweeps - 1) {
+      // f pieces of the last sweep, before any normalization (as cp_als_sweep then
+      // cp_normalize_sort): ||[[A]]||^2 = 1^T (*_k Upsilon^(k)) 1 and sum_n <F^(n), A^(n)>
+      double m2 = 0.0;
+      for (int e = tid; e < RR; e += kT) {
+        double p = 1.0;
+        for (int k = 0; k < N; ++k) p *= sU[k * RR + e];
+        m2 += p;
+      }
+      model2_last = block_sum_fixed(m2, red);
+      double fa = 0.0;
+      for (int k = 0; k < N; ++k)
+        if (a.F[k] != nullptr)
+          for (int64_t e = tid; e < s_dims[k] * R; e += kT) fa = fma(a.F[k][e], (sm + s_aoff[k])[e], fa);
+      fa_last = block_sum_fixed(fa, red);
+    }
+    if (a.normalize) {
+      // eq:ALSnorm after the sweep (cp_normalize_sort with sort = 0): every column
+      // scaled to lambda_r = (prod_n ||a_r^(n)||)^(1/N), unless a column norm is zero
+      __shared__ double sNrm[CP_MAX_N * kSmallSweepMaxR], sLam[kSmallSweepMaxR];
+      __shared__ int sPos[kSmallSweepMaxR];
+      for (int e = tid; e < N * R; e += kT) {
+        const int k = e / R, r = e - k * R;
+        const double *col = (sm + s_aoff[k]) + s_dims[k] * r;
+        double ss = 0.0;
+        for (int i = 0; i < s_dims[k]; ++i) ss = fma(col[i], col[i], ss);
+        sNrm[e] = sqrt(ss);
+      }
+      __syncthreads();
+      for (int r = tid; r < R; r += kT) {
+        double prod = 1.0;
+        int pos = 1;
+        for (int k = 0; k < N; ++k) {
+          prod *= sNrm[k * R + r];
+          pos = pos && (sNrm[k * R + r] > 0.0);
+        }
+        sLam[r] = pow(prod, 1.0 / (double)N);
+        sPos[r] = pos;
+      }
+      __syncthreads();
+      for (int k = 0; k < N; ++k) {
+        double *Ak = sm + s_aoff[k];
+        for (int e = tid; e < s_dims[k] * R; e += kT) {
+          const int r = e / s_dims[k];
+          if (sPos[r]) Ak[e] = sLam[r] * (Ak[e] / sNrm[k * R + r]);
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < N * RR; e += kT) {  // the Grams of the normalized factors
+        const int k = e / RR, rs = e - k * RR, r = rs % R, s2 = rs / R;
+        const double *x = (sm + s_aoff[k]) + s_dims[k] * r, *y = (sm + s_aoff[k]) + s_dims[k] * s2;
+        double g = 0.0;
+        for (int i = 0; i < s_dims[k]; ++i) g = fma(x[i], y[i], g);
+        sU[e] = g;
+      }
+      __syncthreads();
+    }
   }
 
 #ifdef CP_SMALL_TIMING
@@ -285,18 +343,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
     }
     return;
   }
-  double m2 = 0.0;
-  for (int e = tid; e < RR; e += kT) {
-    double p = 1.0;
-    for (int k = 0; k < N; ++k) p *= sU[k * RR + e];
-    m2 += p;
-  }
-  const double model2 = block_sum_fixed(m2, red);
-  double fa = 0.0;
-  for (int k = 0; k < N; ++k)
-    if (a.F[k] != nullptr)
-      for (int64_t e = tid; e < s_dims[k] * R; e += kT) fa = fma(a.F[k][e], (sm + s_aoff[k])[e], fa);
-  const double fas = block_sum_fixed(fa, red);
+  const double model2 = model2_last, fas = fa_last;
   if (tid == 0) {
     const double f = 0.5 * a.normZ2[0] - inner_last + 0.5 * model2;
     a.out[0] = f;
@@ -331,10 +378,11 @@ size_t small_sweep_smem_bytes(const cp_shape &s) {
 
 cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double *normZ2, double *const *A,
                                const double *const *F, int nsweeps, double *out, cudaStream_t st,
-                               double *const *G, bool grad) {
+                               double *const *G, bool grad, bool normalize) {
   SmallSweepArgs a;
   memset(&a, 0, sizeof(a));
   a.grad = grad ? 1 : 0;
+  a.normalize = normalize ? 1 : 0;
   for (int k = 0; k < s.N; ++k) a.G[k] = (G != nullptr) ? G[k] : nullptr;
   a.N = s.N;
   a.R = s.R;

@@ -23,6 +23,7 @@ struct SmallSweepArgs {
   const double *F[CP_MAX_N];
   double *out;
   int grad;               // 1: cp_gradient at this iterate (no updates): out = f, g, ||G^(n)||^2
+  int normalize;          // 1: eq:ALSnorm (no sort) after every sweep (CP_SWEEPS_NORMALIZE)
   double *G[CP_MAX_N];    // gradient mode: G^(n) outputs (entries may be null)
   unsigned *bar;          // medium kernel: grid-barrier counter (zeroed before the launch)
   double *mpart;          // medium kernel: 2 x G x imax x R partial M buffers
@@ -42,6 +43,6 @@ cudaError_t launch_medium_sweep(const cp_shape &s, int G, const double *Z, const
 size_t small_sweep_smem_bytes(const cp_shape &s);
 cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double *normZ2, double *const *A,
                                const double *const *F, int nsweeps, double *out, cudaStream_t st,
-                               double *const *G = nullptr, bool grad = false);
+                               double *const *G = nullptr, bool grad = false, bool normalize = false);
 
 }  // namespace cpk

@@ -273,6 +273,26 @@ def test_multi_sweep_call_general_path_vs_oracle(name, medium, monkeypatch):
     _check_sweep([host_factor(a) for a in Ad], out, Ao, oo, nz2)
 
 
+@pytest.mark.parametrize("dims,R", [((7, 7, 7), 3), ((13, 12, 11), 4), ((50, 50, 50), 3), ((9, 8, 7, 6), 2)])
+@pytest.mark.parametrize("small", ["1", "0"])
+def test_multi_sweep_normalized_vs_oracle(dims, R, small, monkeypatch):
+    """cp_als_sweeps with CP_SWEEPS_NORMALIZE (the setup-phase ALS relaxation: every sweep followed
+    by eq:ALSnorm without sorting) against nu oracle sweeps + oracle normalizations, on
+    the fused path and on the general path (sweep + cp_normalize_sort launches); f, f~ are the last
+    sweep's, before its normalization."""
+    monkeypatch.setenv("CP_SMALL_SWEEP", small)
+    Z, A = cpsynth.random_problem(dims, R, seed=700 + R)
+    nz2 = float(np.vdot(Z, Z))
+    Zd, Ad = dev_problem(Z, A)
+    nu = 4
+    out = host_tensor(cp.als_sweep(Zd, dims, Ad, cp.norm2(Zd, dims), nsweeps=nu, normalize=True))
+    Ao = [a.copy(order="F") for a in A]
+    for _ in range(nu):
+        Ao, oo = oracle.als_sweep(Z, dims, Ao, normZ2=nz2)
+        Ao, _ = oracle.normalize_sort(dims, Ao, sort=False)
+    _check_sweep([host_factor(a) for a in Ad], out, Ao, oo, nz2)
+
+
 def test_fused_small_sweep_reports_enotspd_mid_run():
     """Z = 0: the mode-0 update gives A^(0) = 0, so Gamma^(1) = 0 is singular in the first sweep of
     a multi-sweep call: status CP_ENOTSPD, failed mode 1, f = NaN -- as the oracle reports."""
