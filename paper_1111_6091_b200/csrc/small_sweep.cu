@@ -23,6 +23,9 @@ namespace cpk {
 
 namespace {
 constexpr int kT = kSmallSweepThreads;
+// smallest R whose Cholesky runs on warp 0 (tools/chol_ab.py: R = 3 one thread 12.4 us/sweep vs
+// warp 12.9 at 4^3; R = 8 34.5 vs 30.2 at 7^3; R = 32 450 vs 209 at 13^3)
+constexpr int kSmallCholWarpMinR = 5;
 
 // 1/sqrt(x), x > 0: rsqrt.approx.f64 + two Newton steps (as ys_rsqrt in ylsolve.cu): no
 // square root or division on the serial Cholesky chain
@@ -194,24 +197,59 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
         continue;
       }
       // ---- Gamma = L L^T, lower, no pivoting; pivot <= 0 -> CP_ENOTSPD ----
-      if (tid == 0) {
-        for (int e = 0; e < RR; ++e) sL[e] = 0.0;
-        for (int j = 0; j < R && s_status == 0; ++j) {
-          double d = sG[j + R * j];
+      // R <= 4: one thread (the serial chain is short; measured faster).  Otherwise:
+      // Column j by warp 0, lane i = row i (R <= 32): each lane forms its own
+      //   s_i = Gamma(i,j) - sum_{k<j} L(i,k) L(j,k)
+      // in the same order and expression the former one-thread loop used (bitwise identical
+      // L), so the serial chain per column is j multiply-adds instead of (R - j) * j.
+      if (R < kSmallCholWarpMinR) {
+        if (tid == 0) {
+          for (int e = 0; e < RR; ++e) sL[e] = 0.0;
+          for (int j = 0; j < R && s_status == 0; ++j) {
+            double d = sG[j + R * j];
+            for (int k = 0; k < j; ++k) d -= sL[j + R * k] * sL[j + R * k];
+            if (!(d > 0.0)) {
+              s_status = CP_ENOTSPD;
+              s_failed = n;
+              break;
+            }
+            const double rj = ss_rsqrt(d), ljj = d * rj;
+            sL[j + R * j] = ljj;
+            sDi[j] = rj;
+            for (int i = j + 1; i < R; ++i) {
+              double s = sG[i + R * j];
+              for (int k = 0; k < j; ++k) s -= sL[i + R * k] * sL[j + R * k];
+              sL[i + R * j] = s * rj;
+            }
+          }
+        }
+      } else if (tid < 32) {
+        const int lane = tid;
+        for (int e = lane; e < RR; e += 32) sL[e] = 0.0;
+        __syncwarp();
+        for (int j = 0; j < R; ++j) {
+          // every lane also forms the pivot itself (same order: the lane-j value), no shuffle
+          double s = 0.0, d = sG[j + R * j];
           for (int k = 0; k < j; ++k) d -= sL[j + R * k] * sL[j + R * k];
+          if (lane > j && lane < R) {
+            s = sG[lane + R * j];
+            for (int k = 0; k < j; ++k) s -= sL[lane + R * k] * sL[j + R * k];
+          }
           if (!(d > 0.0)) {
-            s_status = CP_ENOTSPD;
-            s_failed = n;
+            if (lane == 0) {
+              s_status = CP_ENOTSPD;
+              s_failed = n;
+            }
             break;
           }
-          const double rj = ss_rsqrt(d), ljj = d * rj;
-          sL[j + R * j] = ljj;
-          sDi[j] = rj;
-          for (int i = j + 1; i < R; ++i) {
-            double s = sG[i + R * j];
-            for (int k = 0; k < j; ++k) s -= sL[i + R * k] * sL[j + R * k];
-            sL[i + R * j] = s * rj;
+          const double rj = ss_rsqrt(d);
+          if (lane == j) {
+            sL[j + R * j] = d * rj;  // lane j's s is d
+            sDi[j] = rj;
+          } else if (lane > j && lane < R) {
+            sL[lane + R * j] = s * rj;
           }
+          __syncwarp();
         }
       }
       __syncthreads();

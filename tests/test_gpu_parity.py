@@ -213,10 +213,13 @@ def test_sweep_with_rhs(sweep_path):
         _check_sweep(Ag, og, Ao, oo, nz2)
 
 
-def test_sweep_singular_gamma_reports_enotspd(sweep_path):
-    dims, R = (6, 5, 4), 2
+@pytest.mark.parametrize("R,col", [(2, 0), (8, 5)])
+def test_sweep_singular_gamma_reports_enotspd(sweep_path, R, col):
+    """A zero factor column makes Gamma^(0) singular (Keller condition P:362); R = 8 runs the
+    fused kernel's warp Cholesky and fails at pivot j = col, mid-factorization."""
+    dims = (6, 5, 4)
     Z, A = cpsynth.random_problem(dims, R, seed=9)
-    A[1][:, 0] = 0.0
+    A[1][:, col] = 0.0
     Zd, Ad = dev_problem(Z, A)
     out = host_tensor(cp.als_sweep(Zd, dims, Ad, cp.norm2(Zd, dims)))
     _, oo = oracle.als_sweep(Z, dims, A)
@@ -293,10 +296,12 @@ def test_multi_sweep_normalized_vs_oracle(dims, R, small, monkeypatch):
     _check_sweep([host_factor(a) for a in Ad], out, Ao, oo, nz2)
 
 
-def test_fused_small_sweep_reports_enotspd_mid_run():
+@pytest.mark.parametrize("R", [2, 8])
+def test_fused_small_sweep_reports_enotspd_mid_run(R):
     """Z = 0: the mode-0 update gives A^(0) = 0, so Gamma^(1) = 0 is singular in the first sweep of
-    a multi-sweep call: status CP_ENOTSPD, failed mode 1, f = NaN -- as the oracle reports."""
-    dims, R = (6, 5, 4), 2
+    a multi-sweep call: status CP_ENOTSPD, failed mode 1, f = NaN -- as the oracle reports
+    (R = 2: one-thread Cholesky; R = 8: warp Cholesky)."""
+    dims = (6, 5, 4)
     _, A = cpsynth.random_problem(dims, R, seed=9)
     Z = np.zeros(tuple(reversed(dims)))
     Zd, Ad = dev_problem(Z, A)
