@@ -258,6 +258,32 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
       // ---- each row: L y = (m + f)^T, L^T x^T = y (eq:relaxinnersolve) ----
       const double *F = a.F[n];
       __syncthreads();  // (part is reused for y below)
+      if (R >= kSmallCholWarpMinR) {
+        // one warp per row, lane r = component r.  Forward: column-oriented (after y_r, lanes
+        // k > r subtract L(k,r) y_r) -- each b_k sees the subtractions in the same order
+        // k' = 0..k-1 as the row-oriented loop below, so y is bitwise the same.  Backward:
+        // lane j subtracts L(r,j) x_r for r = R-1 down to j+1 (the reverse of the row loop's
+        // order; a rounding-level difference).  The serial chain per row is 2R shuffles+FMAs
+        // instead of R^2 dependent shared-memory FMAs (13^3 R = 32: 51 k -> see DESIGN 6.7).
+        const int lane = tid & 31, warp = tid >> 5;
+        double *An = sm + s_aoff[n];
+        const double dl = lane < R ? sDi[lane] : 0.0;
+        for (int i = warp; i < In; i += kT / 32) {
+          double b = 0.0;
+          if (lane < R) b = sM[i + In * lane] + (F != nullptr ? F[i + In * lane] : 0.0);
+          for (int r = 0; r < R; ++r) {
+            const double yr = __shfl_sync(0xffffffffu, b * dl, r);
+            if (lane == r) b = yr;
+            else if (lane > r && lane < R) b -= sL[lane + R * r] * yr;
+          }
+          for (int r = R - 1; r >= 0; --r) {
+            const double xr = __shfl_sync(0xffffffffu, b * dl, r);
+            if (lane == r) b = xr;
+            else if (lane < r) b -= sL[r + R * lane] * xr;
+          }
+          if (lane < R) An[i + In * lane] = b;
+        }
+      } else
       for (int i = tid; i < In; i += kT) {
         double *y = part + (int64_t)i * R;
         for (int r = 0; r < R; ++r) {
