@@ -228,6 +228,12 @@ typedef struct {
     int32_t coarsest;                                 /* I_coarsest; 0 = 2R (reading R16) */
     int32_t solve_stagnation_after;                   /* 5 */
     int32_t max_trace;                                /* rows of the trace buffer */
+    int32_t fmg_guard;                                /* 0 (default): P:492 -- the solve phase always
+                                                         continues from the FMG result, after a
+                                                         down-sweep rebuild of the operators;
+                                                         1: reading R29 -- keep the FMG result only
+                                                         if it lowers g (else restore the setup
+                                                         iterate, no rebuild) */
 } cp_mg_params;
 
 void cp_mg_default_params(cp_mg_params *p);
@@ -237,15 +243,21 @@ size_t cp_mg_workspace_bytes(const cp_shape *s, const cp_mg_params *p);
  * mode n at T[t*N + n]; read only);  A_fmg: [host] N device pointers to the coarsest-level
  * random initial guess of FMG (ignored unless use_fmg);  report [host, 16 doubles]:
  *   0 g, 1 f, 2 cycles (setup + FMG + solve), 3 setup cycles, 4 solve cycles, 5 levels,
- *   6 status (0 converged, 1 cycle limit, CP_ENOTSPD), 7 trace rows, 8 rebuilds, 9 seconds;
- * trace [host, max_trace x 4]: phase (0 setup, 1 FMG, 2 solve), cycle, g, seconds. */
+ *   6 status (0 converged, 1 cycle limit, CP_ENOTSPD: a relaxation on some level hit a
+ *   non-positive Cholesky pivot -- the solve stops at the next stopping test), 7 trace rows,
+ *   8 rebuilds, 9 seconds, 10 device seconds of the stopping tests (excluded from the paper's
+ *   timings), 11 failing mode of a CP_ENOTSPD (else -1);
+ * trace [host, max_trace x 4]: phase (0 setup, 1 FMG, 2 solve), cycle, g, seconds.
+ * Reentrant: all driver state is per call (the workspace and the heap). */
 int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const double *const *T,
                 const double *const *A_fmg, const cp_mg_params *prm, double *report, double *trace,
                 void *ws, size_t ws_bytes, cp_stream_t stream);
 
 /* Standalone ALS (the paper's baseline): sweeps with normalization until g < tol or
- * max_iters; g is evaluated every `check_every` sweeps.  report [host, 8]: 0 g, 1 f,
- * 2 iterations, 3 status (0 converged, 1 iteration limit, CP_ENOTSPD), 4 seconds. */
+ * max_iters; g is evaluated every `check_every` sweeps, together with the status word of every
+ * sweep since the last check.  report [host, 8]: 0 g, 1 f, 2 iterations, 3 status (0 converged,
+ * 1 iteration limit, CP_ENOTSPD: a sweep hit a non-positive Cholesky pivot -- the loop stops at
+ * the next check), 4 seconds, 5 seconds of the stopping tests, 6 failing mode (or -1). */
 size_t cp_als_solve_workspace_bytes(const cp_shape *s);
 int cp_als_solve(const cp_shape *s, const double *Z, double *const *A, double tol, int32_t max_iters,
                  int32_t check_every, double *report, void *ws, size_t ws_bytes, cp_stream_t stream);

@@ -77,15 +77,17 @@ int oracle_mttkrp_rows(int N, const int64_t *dims, int R, const double *Z,
     for (int k = 1; k < N; ++k) stride[k] = stride[k - 1] * dims[k - 1];
     const int64_t J = numel(N, dims) / In; /* number of columns of Z_(n) */
 
-    for (int64_t i = row_lo; i < row_hi; ++i)
-        for (int r = 0; r < R; ++r) CM(M, In, i, r) = 0.0;
-
 #pragma omp parallel
     {
         double *phi = (double *)malloc(sizeof(double) * (size_t)R);
+        /* row i's R sums live in this thread-private array and are stored into M once: M is
+         * column-major, so rows owned by different threads share cache lines (the summation
+         * order -- j ascending per (i, r) -- is the same as accumulating in M) */
+        double *acc = (double *)malloc(sizeof(double) * (size_t)R);
         int64_t idx[OR_MAXN];
 #pragma omp for schedule(static)
         for (int64_t i = row_lo; i < row_hi; ++i) {
+            for (int r = 0; r < R; ++r) acc[r] = 0.0;
             for (int k = 0; k < N; ++k) idx[k] = 0;
             for (int64_t j = 0; j < J; ++j) {
                 /* idx holds the multi-index of column j (mode `mode` excluded) */
@@ -99,7 +101,7 @@ int oracle_mttkrp_rows(int N, const int64_t *dims, int R, const double *Z,
                     phi[r] = p;
                 }
                 const double z = Z[lin];
-                for (int r = 0; r < R; ++r) CM(M, In, i, r) += z * phi[r];
+                for (int r = 0; r < R; ++r) acc[r] += z * phi[r];
                 /* advance the column multi-index, lowest mode fastest */
                 for (int k = 0; k < N; ++k) {
                     if (k == mode) continue;
@@ -107,7 +109,9 @@ int oracle_mttkrp_rows(int N, const int64_t *dims, int R, const double *Z,
                     idx[k] = 0;
                 }
             }
+            for (int r = 0; r < R; ++r) CM(M, In, i, r) = acc[r];
         }
+        free(acc);
         free(phi);
     }
     return OR_OK;

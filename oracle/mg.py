@@ -230,20 +230,23 @@ class MGOracle:
                 break
             g_old = gn
         if not converged and p["use_fmg"]:
-            # reading R29: the FMG approximation replaces the setup iterate only if it lowers g
-            # ("a new approximation"; P:488 discards a worse iterate the same way)
+            # "Multilevel + FMG": one FMG-CP-FAS cycle computes a new approximation to the
+            # boot factors, then the transfer operators are rebuilt by one down-sweep of
+            # CP-AMG-mult (boot factors not updated).  fmg_guard = 1 is reading R29 (not the
+            # paper's default): the FMG result is kept only if it lowers g, else the setup
+            # iterate is restored and the operators are not rebuilt.
             kept = [a.copy(order="F") for a in f.A]
             self.fmg(A_fmg)
             gf = self.fit(0, f.A)[0][1]
             cycles += 1
             trace.append((1, cycles, gf))
-            if gf < g:
+            if p["fmg_guard"] and not gf < g:
+                f.A = kept
+            else:
                 g = gf
                 converged = g < p["tol"]
                 if not converged:
                     self.setup_cycle(0, False, False)
-            else:
-                f.A = kept
         rebuilt = False
         g_old = g
         while not converged and cycles < p["max_cycles"]:
@@ -274,7 +277,7 @@ class MGOracle:
 
 
 DEFAULTS = dict(nu1_setup=5, nu2_setup=5, nuc_setup=100, n_test=2, nu1_solve=1, nu2_solve=1, nuc_solve=50,
-                max_setup_cycles=5, min_setup_cycles=3, stagnation_eps=0.1, use_fmg=0, nu_fmg=50,
+                max_setup_cycles=5, min_setup_cycles=3, stagnation_eps=0.1, use_fmg=0, nu_fmg=50, fmg_guard=0,
                 max_cycles=500, tol=1e-10, coarsest=0, solve_stagnation_after=5)
 
 

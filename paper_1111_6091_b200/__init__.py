@@ -258,7 +258,7 @@ class MGParams(ctypes.Structure):
                 ("min_setup_cycles", ctypes.c_int32), ("stagnation_eps", ctypes.c_double),
                 ("use_fmg", ctypes.c_int32), ("nu_fmg", ctypes.c_int32), ("max_cycles", ctypes.c_int32),
                 ("tol", ctypes.c_double), ("coarsest", ctypes.c_int32), ("solve_stagnation_after", ctypes.c_int32),
-                ("max_trace", ctypes.c_int32)]
+                ("max_trace", ctypes.c_int32), ("fmg_guard", ctypes.c_int32)]
 
     @classmethod
     def default(cls, **kw):
@@ -303,7 +303,7 @@ def mg_solve(Z, dims, A, T, A_fmg=None, params=None, stream=None):
                              _ptr_array(A_fmg) if A_fmg is not None else None, ctypes.byref(params),
                              report, trace, _ptr(buf), ctypes.c_size_t(nbytes), _stream(stream)), "cp_mg_solve")
     keys = ["g", "f", "cycles", "setup_cycles", "solve_cycles", "levels", "status", "trace_rows", "rebuilds",
-            "seconds", "fit_seconds"]
+            "seconds", "fit_seconds", "failed_mode"]
     rep = {k: report[i] for i, k in enumerate(keys)}
     tr = np.array(trace[: 4 * int(rep["trace_rows"])]).reshape(-1, 4)
     return rep, tr
@@ -320,7 +320,7 @@ def als_solve(Z, dims, A, tol=1e-10, max_iters=10000, check_every=1, stream=None
     _check(lib().cp_als_solve(ctypes.byref(s), _ptr(Z), _ptr_array(A), ctypes.c_double(tol), ctypes.c_int32(max_iters),
                               ctypes.c_int32(check_every), report, _ptr(buf), ctypes.c_size_t(nbytes),
                               _stream(stream)), "cp_als_solve")
-    keys = ["g", "f", "iterations", "status", "seconds", "fit_seconds"]
+    keys = ["g", "f", "iterations", "status", "seconds", "fit_seconds", "failed_mode"]
     return {k: report[i] for i, k in enumerate(keys)}
 
 

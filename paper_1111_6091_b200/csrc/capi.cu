@@ -24,7 +24,6 @@ static thread_local int g_launches = 0;
 
 // ---------------------------------------------------------------- kernel table
 static StreamEntry g_table[kStreamTableSize];
-static int g_occ[kStreamTableSize];  // resident CTAs / SM at the configured smem (0 = unknown)
 static std::once_flag g_table_once;
 
 const StreamEntry &stream_entry(int R, int V, int op) {
@@ -45,47 +44,97 @@ const StreamEntry &stream_mma_entry(int nt, int mt, int op) {
   return g_mma_table[mma_index(nt, mt, op)];
 }
 
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  return dev;
+}
+
 static int device_sms() {
+  static std::mutex mu;
   static int cached[64] = {0};
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-  if (dev >= 0 && dev < 64 && cached[dev] > 0) return cached[dev];
-  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
-    return 148;
+  const int dev = current_device();
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev >= 0 && dev < 64 && cached[dev] > 0) return cached[dev];
+  }
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) return 148;
+  std::lock_guard<std::mutex> lk(mu);
   if (dev >= 0 && dev < 64) cached[dev] = sms;
   return sms;
 }
 
-static int env_int(const char *name, int dflt) {
+static int parse_env(const char *name, int dflt) {
   const char *v = getenv(name);
   return (v && *v) ? atoi(v) : dflt;
 }
 
+int path_flag(const char *name, int dflt) {
+  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP",
+                                       "CP_SWEEP_TREE", "CP_YLSOLVE", "CP_MODEPROD_DMMA", "CP_MG_GRAPH",
+                                       "CP_ALS_GRAPH", "CP_MG_STRUCTURED", "CP_PDL"};
+  for (const char *k : kPaths)
+    if (strcmp(k, name) == 0) return parse_env(name, dflt);
+  return dflt;
+}
+
+int knob(const char *name, int dflt) {
+#ifdef CP_EXPERIMENTS
+  return parse_env(name, dflt);
+#else
+  (void)name;
+  return dflt;
+#endif
+}
+
+cudaError_t ensure_smem_attr(const void *kernel, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, const void *>, int>> done;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  for (const auto &d : done)
+    if (d.first.first == dev && d.first.second == kernel && d.second >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  for (auto &d : done)
+    if (d.first.first == dev && d.first.second == kernel) {
+      d.second = bytes;
+      return cudaSuccess;
+    }
+  done.push_back({{dev, kernel}, bytes});
+  return cudaSuccess;
+}
+
 // measured (tools/time_sweep.py, no profiling events): PDL on the 8-CTA-cluster ylsolve launches cost
 // c4a ~15 us per sweep (its CTAs, launched early, wait where the pass could run); default: stream +
-// small kernels
+// small kernels.  CP_PDL=0 (path selector) disables PDL everywhere; the mask is an experiment knob.
 constexpr int kPdlDefaultMask = (1 << kPdlStream) | (1 << kPdlSmall);
 bool pdl_enabled(int cls) {
-  static const int mask = env_int("CP_PDL", 1) != 0 ? env_int("CP_PDL_MASK", kPdlDefaultMask) : 0;
+  const int mask = path_flag("CP_PDL", 1) != 0 ? knob("CP_PDL_MASK", kPdlDefaultMask) : 0;
   return (mask >> cls) & 1;
 }
 
-// resident CTAs / SM of a streaming kernel at a dynamic smem size; cached per (kernel, smem)
-// (the CUDA queries cost microseconds, and every call plans its launches)
+// resident CTAs / SM of a streaming kernel at a dynamic smem size; cached per (device, kernel,
+// smem) (the CUDA queries cost microseconds, and every call plans its launches)
 static int kernel_occupancy(const void *kernel, int smem) {
   static std::mutex mu;
-  static std::vector<std::pair<std::pair<const void *, int>, int>> cache;
-  std::lock_guard<std::mutex> lk(mu);
-  for (const auto &c : cache)
-    if (c.first.first == kernel && c.first.second == smem) return c.second;
+  static std::vector<std::pair<std::pair<const void *, int>, std::pair<int, int>>> cache;
+  const int dev = current_device();
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto &c : cache)
+      if (c.first.first == kernel && c.first.second == smem && c.second.first == dev) return c.second.second;
+  }
   int n = 0;
-  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
+  if (ensure_smem_attr(kernel, 200 * 1024) != cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kStreamThreads, smem) != cudaSuccess) {
     cudaGetLastError();
     return 1;
   }
   n = n > 0 ? n : 1;
-  cache.push_back({{kernel, smem}, n});
+  std::lock_guard<std::mutex> lk(mu);
+  cache.push_back({{kernel, smem}, {dev, n}});
   return n;
 }
 static int stream_occupancy(int R, int V, int op, int smem) {
@@ -117,7 +166,7 @@ static bool plan_digits(StreamPlan &p, const cp_shape &s) {
 
 // FP64 tensor-core consumer geometry (stream_mma.cuh): row block, k-split and m-tiles per warp
 static bool plan_mma_ok(const StreamPlan &p, const cp_shape &s, int op) {
-  return !(env_int("CP_STREAM_MMA", 1) == 0 || (op == OP_RESID && env_int("CP_RESID_MMA", 1) == 0) || s.R > 32 ||
+  return !(path_flag("CP_STREAM_MMA", 1) == 0 || (op == OP_RESID && path_flag("CP_RESID_MMA", 1) == 0) || s.R > 32 ||
            (p.I1 & 1));
 }
 // row block = the whole (even) column, padded column slots within the TMA box limit: the stage
@@ -130,7 +179,7 @@ static bool plan_mma(StreamPlan &p, const cp_shape &s, int op) {
   if (!plan_mma_ok(p, s, op)) return false;
   p.nt = (s.R + 7) / 8;
   int mt_max = (p.nt <= 2) ? 8 : 4;
-  const int mt_env = env_int("CP_MMA_MTMAX", 4);  // measured: MT = 8 (64 accumulators) serializes the A loads
+  const int mt_env = knob("CP_MMA_MTMAX", 4);  // measured: MT = 8 (64 accumulators) serializes the A loads
   if (mt_max > mt_env) mt_max = mt_env;
   int64_t Wt = p.I1;
   if (ceil_div(p.I1, 8) > 8 * mt_max) Wt = 64 * mt_max;
@@ -190,12 +239,12 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   const int WSTR = (s.R % 2 == 0) ? s.R + 2 : s.R + 1;
   p.RS = s.R + (s.R & 1);
   // stage size: tools/sweep*.sh (DFMA consumers), tools/plan_sweep.py (MMA: 2 stages of ~52 KB)
-  int stage_target = env_int("CP_STAGE_BYTES", plan_mma_ok(p, s, op) ? 53248 : 40960);
+  int stage_target = knob("CP_STAGE_BYTES", plan_mma_ok(p, s, op) ? 53248 : 40960);
   int cps, cpt = 1;
   if (plan_mma(p, s, op)) {
     // whole-column row blocks loaded by one tensor-map TMA per stage (launch_stream): 3 stages
     // of ~26 KB beat 2 of ~52 KB (c4b MTTKRP 0.153 -> 0.143 ms; tools/sweep_c4b.sh)
-    if (tmap_geometry_ok(p) && env_int("CP_STREAM_TMAP", 1)) stage_target = env_int("CP_STAGE_BYTES", 26624);
+    if (tmap_geometry_ok(p) && path_flag("CP_STREAM_TMAP", 1)) stage_target = knob("CP_STAGE_BYTES", 26624);
     // stage: a multiple of 4 KS columns (k-steps of every k-group)
     const int unit = 4 * p.ks;
     cps = stage_target / (p.zcs * 8);
@@ -210,7 +259,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     for (int j = 1; j < p.nd; ++j)
       if (p.ord[j] != p.mode) slow = true;
     p.direct_w = has_f0 ? 1 : 0;
-    p.srows = (has_f0 && slow && env_int("CP_MMA_SROWS", 1)) ? 1 : 0;
+    p.srows = (has_f0 && slow && knob("CP_MMA_SROWS", 1)) ? 1 : 0;
     if (has_f0 && slow && !p.srows) p.direct_w = 0;
     const int RP = 8 * p.nt;
     if (op == OP_YL) p.red_doubles = (p.ks - 1) * p.Wmax * RP + 8;
@@ -219,8 +268,8 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   } else {
     // rows per consumer thread: the largest V dividing I1 with V * RT <= 32 accumulators, which
     // keeps the kernel at <= 96 registers and 2 CTAs/SM; residual pass: V <= 4 and V * R <= 64
-    const int vmax_env = env_int("CP_MAX_V", 8);
-    const int vr_max = env_int("CP_MAX_VR", 32);
+    const int vmax_env = knob("CP_MAX_V", 8);
+    const int vr_max = knob("CP_MAX_VR", 32);
     p.V = 1;
     for (int v : {8, 4, 2}) {
       if (v > vmax_env || p.I1 % v != 0) continue;
@@ -235,11 +284,11 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     // partials); every other pass keeps whole columns in one CTA.
     int64_t Wt = p.I1;
     if (op != OP_RESID && p.mode == 0) {
-      const int w0 = env_int("CP_MTTKRP_W0", 512);
+      const int w0 = knob("CP_MTTKRP_W0", 512);
       if (p.I1 >= 2 * w0) Wt = w0;
     }
     if (op == OP_YL) {
-      const int w0 = env_int("CP_YL_W", 512);
+      const int w0 = knob("CP_YL_W", 512);
       if (p.I1 >= 2 * w0) Wt = w0;
     }
     if (Wt > maxW) Wt = maxW;
@@ -283,29 +332,29 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     // conflicts but measured slower (per-row copies; smaller stages): CP_MMA_PAD_A/_W
     int st = p.RS;
     while (st % 16 != 8) ++st;
-    p.ars = env_int("CP_MMA_PAD_A", 0) ? st : p.RS;
-    if (op == OP_RESID && p.direct_w && env_int("CP_RESID_PAD_A", 1)) {
+    p.ars = knob("CP_MMA_PAD_A", 0) ? st : p.RS;
+    if (op == OP_RESID && p.direct_w && knob("CP_RESID_PAD_A", 1)) {
       // residual pass: B fragments read factor row gq, rank 4 kk + tq -- a row stride of 4
       // (mod 16) doubles spreads a half-warp over 16 bank pairs (one bulk copy per row)
       int sa = p.RS;
       while (sa % 16 != 4) ++sa;
       p.ars = sa;
     }
-    p.wstr = env_int("CP_MMA_PAD_W", 0) ? st : WSTR;
-    if (p.direct_w && env_int("CP_MMA_WSTR0", 1)) p.wstr = 0;  // no weight rows
+    p.wstr = knob("CP_MMA_PAD_W", 0) ? st : WSTR;
+    if (p.direct_w && knob("CP_MMA_WSTR0", 1)) p.wstr = 0;  // no weight rows
   } else {
     p.ars = p.RS;
     p.wstr = WSTR;
   }
   // ring: CP_RING_BYTES (default 96 KB) of stages, at least 2; the MMA kernels also keep the whole
   // CTA within the 2-CTAs/SM shared-memory budget (113 KB) by shrinking the stage if needed
-  const int cap = env_int("CP_SMEM_CAP", 113 * 1024);
+  const int cap = knob("CP_SMEM_CAP", 113 * 1024);
   p.gjsm = (p.mma && p.direct_w) ? gamma_job_smem_doubles(s.R) : 0;  // Gamma job (gamma_job.cuh)
   const int unit = p.mma ? 4 * p.ks : 1;
   int stage_doubles = 0, nst = 2;
   for (;;) {
     stage_doubles = p.zst + cps * p.ars + cps * p.wstr + (p.srows ? kMaxDigits * p.RS : 0);
-    nst = env_int("CP_RING_BYTES", 96 * 1024) / (stage_doubles * 8);
+    nst = knob("CP_RING_BYTES", 96 * 1024) / (stage_doubles * 8);
     if (nst < 2) nst = 2;
     if (nst > 8) nst = 8;
     // mode-0 slot / k-group reduction reuses the Z ring: it must hold the reduced blocks
@@ -318,13 +367,13 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     p.zst = cps * p.zcs;
   }
   p.nstages = nst;
-  p.dbg = env_int("CP_STREAM_DBG", 0);
+  p.dbg = knob("CP_STREAM_DBG", 0);
   p.keep_q = 0;
   p.smem_bytes = (nst * stage_doubles + p.red_doubles + p.gjsm + 32) * 8 + nst * 88 + 64;
   if (p.smem_bytes > 200 * 1024) return false;
   const int occ = p.mma ? stream_mma_occupancy(p.nt, p.mt, op, p.smem_bytes)
                         : stream_occupancy(s.R, p.V, op, p.smem_bytes);
-  const int ctas = env_int("CP_CTAS_PER_SM", 0);
+  const int ctas = knob("CP_CTAS_PER_SM", 0);
   const int64_t Gtot = (int64_t)num_sms * (ctas > 0 ? (ctas < occ ? ctas : occ) : occ);
   int64_t Gc = Gtot / p.RB;
   if (Gc < 1) Gc = 1;
@@ -407,13 +456,13 @@ cudaError_t launch_stream(const StreamPlan &p0, cudaStream_t st) {
     // L2 residency across passes (DESIGN 6.8): for a tensor well beyond L2, the first
     // CP_L2KEEP_MB MiB of Z (default 40) are fetched evict_last and the rest evict_first, so
     // consecutive passes over the same Z re-read that slice from L2
-    static const int64_t keep_mb = env_int("CP_L2KEEP_MB", 40);
+    const int64_t keep_mb = knob("CP_L2KEEP_MB", 40);
     double P = 1.0;
     for (int k = 0; k < p.N; ++k) P *= (double)p.dims[k];
     if (keep_mb > 0 && p.V >= 2 && 8.0 * P >= 96.0 * (1 << 20)) p.keep_q = (keep_mb << 20) / (8 * p.I1);
   }
   p.use_tmap = 0;
-  if (p.mma && env_int("CP_STREAM_TMAP", 1)) p.use_tmap = encode_stage_tmap(p) ? 1 : 0;
+  if (p.mma && path_flag("CP_STREAM_TMAP", 1)) p.use_tmap = encode_stage_tmap(p) ? 1 : 0;
   const StreamEntry &e = p.mma ? stream_mma_entry(p.nt, p.mt, p.op) : stream_entry(p.R, p.V, p.op);
   ++g_launches;
   const bool prof = g_prof_on && g_prof_n < kProfMax;
@@ -443,7 +492,6 @@ struct Layout {
   cp_shape s3;
   int rpc2, sp2, nyr;
   size_t yl, edge, mbuf, yr, segtab, m0part, linv;
-  size_t med;   // medium fused sweep (medium_sweep.cu): barrier counter + partial M buffers
   size_t ntmp;  // cp_als_sweeps with CP_SWEEPS_NORMALIZE: normalization scratch (sum_n I_n R)
 };
 
@@ -470,7 +518,7 @@ static bool make_layout(Layout &L, const cp_shape &s) {
   for (int k = 0; k < s.N; ++k) L.prep_blocks += (int)ceil_div(s.dims[k], kPrepRows);
   (void)maxI;
   if (!make_stream_plan(L.resid, s, 0, OP_RESID, sms)) return false;
-  L.tree = (s.N >= 3) && env_int("CP_SWEEP_TREE", 1) != 0;
+  L.tree = (s.N >= 3) && path_flag("CP_SWEEP_TREE", 1) != 0;
   if (L.tree) {
     if (!make_stream_plan(L.yl_plan, s, 1, OP_YL, sms)) return false;
     memset(&L.s3, 0, sizeof(L.s3));
@@ -530,13 +578,6 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     L.linv = off; off = align_up(off + (size_t)s.N * R * R);  // L^{-1} of every Gamma^(n)
     L.yr = off; off = align_up(off + (size_t)L.s3.dims[2] * R);
     L.segtab = off; off = align_up(off + (size_t)(s.dims[1] * y.RB + 1) / 2);  // u32 ticket per (segment, row block)
-  }
-  {
-    // the medium fused sweep's barrier + partial M buffers, only for shapes it can run
-    const int G = medium_sweep_ctas(s, sms);
-    const bool med = G > 0 && medium_sweep_smem_bytes(s, G) <= 200 * 1024;
-    L.med = off;
-    off = align_up(off + (med ? medium_sweep_ws_doubles(s, G) : 0));
   }
   {
     size_t sumIR = 0;
@@ -649,7 +690,7 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
   p.part = w + L.part;
   if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
   const ReduceGeom g = reduce_geom(p);
-  if (g.mode0 && !g.direct && env_int("CP_REDUCE0_COALESCED", 1)) {
+  if (g.mode0 && !g.direct && knob("CP_REDUCE0_COALESCED", 1)) {
     const int64_t S = g.In_rows * g.R;
     if (launch_k(reduce_mode0_kernel, dim3((unsigned)ceil_div(S, 32)), dim3(256), 0, cs, (const double *)g.part, g.Gc,
                  S, M) != cudaSuccess)
@@ -664,12 +705,13 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
 
 // small tensors (coarse multigrid levels): the fused shared-memory sweep kernel (small_sweep.cu)
 static bool use_small_sweep(const cp_shape &s) {
-  return env_int("CP_SMALL_SWEEP", 1) != 0 && small_sweep_smem_bytes(s) != 0 &&
-         small_sweep_smem_bytes(s) <= (size_t)env_int("CP_SMALL_SWEEP_SMEM", 200 * 1024);
+  return path_flag("CP_SMALL_SWEEP", 1) != 0 && small_sweep_smem_bytes(s) != 0 &&
+         small_sweep_smem_bytes(s) <= (size_t)knob("CP_SMALL_SWEEP_SMEM", 200 * 1024);
 }
 
 static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
-                      const double *const *F, double *out, void *ws, size_t ws_bytes, cp_stream_t stream);
+                      const double *const *F, double *out, void *ws, size_t ws_bytes, cp_stream_t stream,
+                      bool first);
 
 int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
                  const double *const *F, double *out, void *ws, size_t ws_bytes,
@@ -698,22 +740,9 @@ int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, doub
     g_launches = 1;
     return CP_OK;
   }
-  {
-    // medium tensors: one cooperative launch for all nsweeps (medium_sweep.cu).  Opt-in
-    // (CP_MEDIUM_SWEEP=1): measured slower than the general path so far (c1 50^3: 57 vs 46 us
-    // per sweep, c2 100^3: 98 vs 54) -- DESIGN 6.7
-    const int G = env_int("CP_MEDIUM_SWEEP", 0) ? medium_sweep_ctas(*s, device_sms()) : 0;
-    if (G > 0 && !norm && medium_sweep_smem_bytes(*s, G) <= 200 * 1024) {
-      if (launch_medium_sweep(*s, G, Z, normZ2, A, F, nsweeps, out, static_cast<double *>(ws) + L.med,
-                              reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
-        return CP_ECUDA;
-      g_launches = 1;
-      return CP_OK;
-    }
-  }
   int total = 0;
   for (int k = 0; k < nsweeps; ++k) {
-    if ((st = sweep_impl(s, Z, normZ2, A, F, out, ws, ws_bytes, stream))) return st;
+    if ((st = sweep_impl(s, Z, normZ2, A, F, out, ws, ws_bytes, stream, k == 0))) return st;
     total += g_launches;
     if (norm) {  // cp_normalize_sort(sort = 0) with the sweep workspace's own scratch region
       NormArgs na;
@@ -736,8 +765,12 @@ int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, doub
   return CP_OK;
 }
 
+// One sweep of the general path.  first = false: a later sweep of the same cp_als_sweeps call --
+// the status word is not reset, so a failure in an earlier sweep stays reported and every later
+// solve skips (the fused small kernel likewise stops at the first failure).
 static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
-                      const double *const *F, double *out, void *ws, size_t ws_bytes, cp_stream_t stream) {
+                      const double *const *F, double *out, void *ws, size_t ws_bytes, cp_stream_t stream,
+                      bool first) {
   g_launches = 0;
   int st;
   Layout L;
@@ -749,13 +782,15 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
   PrepArgs pa;
   PrepGrams pg;
   fill_prep(*s, L, w, (const double *const *)A, -1, true, w + L.status, pa, pg);
-  const bool yl_inline = L.tree && L.yl_plan.mma && env_int("CP_YL_INLINE_FIX", 1);
+  pa.keep_status = first ? 0 : 1;
+  const bool yl_inline = L.tree && L.yl_plan.mma && knob("CP_YL_INLINE_FIX", 1);
   if (yl_inline) {  // Y_L segment tickets (stream_mma.cuh yl_complete_segment)
     pa.zero = reinterpret_cast<unsigned *>(w + L.segtab);
     pa.nzero = (int)(s->dims[1] * L.yl_plan.RB);
   }
-  // experiments only: CP_SWEEP_SKIP bitmask drops launches (timing of the rest; results wrong)
-  const int skip = env_int("CP_SWEEP_SKIP", 0);
+  // experiments only (-DCP_EXPERIMENTS builds): CP_SWEEP_SKIP bitmask drops launches (timing of
+  // the rest; results wrong).  Always 0 in the shipped library.
+  const int skip = knob("CP_SWEEP_SKIP", 0);
   if (!(skip & 1) && launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
   int launches = 1;
   double *gp[2] = {w + L.gpart0, w + L.gpart1};
@@ -783,7 +818,7 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
     sa.dotM = w + L.dotM;
     sa.dotF = w + L.dotF + (size_t)n * L.gp_max;
     sa.status = w + L.status;
-    sa.dbg = env_int("CP_SOLVE_DBG", 0);
+    sa.dbg = knob("CP_SOLVE_DBG", 0);
     sa.linv = linv;
     grid_of[n] = (int)ceil_div(s->dims[n], rpc);
     if (n == N - 1) {
@@ -813,7 +848,7 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
   const int RR = R * R;
   // Gamma^(n) job (gamma_job.cuh): Upsilon^(k) for k > n from the prep partials (old factors),
   // k = n-1 from the previous solve's partials, k < n-1 from the totals earlier jobs wrote
-  const bool jobs = L.tree && env_int("CP_GAMMA_JOBS", 1) != 0;
+  const bool jobs = L.tree && knob("CP_GAMMA_JOBS", 1) != 0;
   auto gamma_job = [&](int n) -> GammaJob {
     GammaJob g;
     memset(&g, 0, sizeof(g));
@@ -869,7 +904,7 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
       if (launch_yl_fixup(yg, cs) != cudaSuccess) return CP_ECUDA;
       ++launches;
     }
-    const bool ylsolve = env_int("CP_YLSOLVE", 1) != 0;
+    const bool ylsolve = path_flag("CP_YLSOLVE", 1) != 0;
     if (ylsolve) {
       // modes 0 and 1: M rows from Y_L, Gamma, Cholesky and the solves in one kernel each
       // (ylsolve.cu); Gamma^(0) from the Y_L pass's job when it ran, else factored in-block
@@ -970,7 +1005,7 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
         ya.M = mb;
         // Gamma^(2) came with pass 2; Gamma^(m > 2) in an extra yr block when CP_GAMMA_JOBS=2
         // (measured: the yr kernels are too short to hide it)
-        const bool jm = (m == 2) ? job2 : (jobs && env_int("CP_GAMMA_JOBS", 1) >= 2);
+        const bool jm = (m == 2) ? job2 : (jobs && knob("CP_GAMMA_JOBS", 1) >= 2);
         if (m > 2 && jm) ya.gj = gamma_job(m);
         if (launch_yr(ya, cs) != cudaSuccess) return CP_ECUDA;
         ++launches;
@@ -1046,13 +1081,14 @@ static int fit_impl(const cp_shape *s, const double *Z, const double *normZ2, co
   PrepArgs pa;
   PrepGrams pg;
   fill_prep(*s, L, w, A, -1, true, nullptr, pa, pg);
-  const bool yl_inline = L.tree && L.yl_plan.mma && env_int("CP_YL_INLINE_FIX", 1);
+  const bool yl_inline = L.tree && L.yl_plan.mma && knob("CP_YL_INLINE_FIX", 1);
   if (yl_inline) {  // Y_L segment tickets (stream_mma.cuh yl_complete_segment)
     pa.zero = reinterpret_cast<unsigned *>(w + L.segtab);
     pa.nzero = (int)(s->dims[1] * L.yl_plan.RB);
   }
-  // experiments only: CP_SWEEP_SKIP bitmask drops launches (timing of the rest; results wrong)
-  const int skip = env_int("CP_SWEEP_SKIP", 0);
+  // experiments only (-DCP_EXPERIMENTS builds): CP_SWEEP_SKIP bitmask drops launches (timing of
+  // the rest; results wrong).  Always 0 in the shipped library.
+  const int skip = knob("CP_SWEEP_SKIP", 0);
   if (!(skip & 1) && launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
   int launches = 1;
   // residual pass 1/2 ||Z - [[A]]||^2 (eq:CPfunctional): one partial per CTA

@@ -78,7 +78,7 @@ struct StreamPlan {
   int gjsm;         // shared-memory doubles reserved for it
   int64_t keep_q;   // L2 residency across passes: Z columns q < keep_q are fetched with an
                     // evict_last policy, the rest evict_first (0: no hints).  See DESIGN 6.8.
-  int dbg;          // experiments only (env CP_STREAM_DBG): 1 = consumers skip the FMAs, 2 = weight warp skips forming
+  int dbg;          // experiments only (knob CP_STREAM_DBG, -DCP_EXPERIMENTS builds): 1 = consumers skip the FMAs
   // MMA plans whose row block is the whole column (RB = 1): one 3-D tensor-map TMA per full
   // stage instead of one bulk copy per column.  View {I1, qsd[0], Q / qsd[0]} of Z, box
   // {zcs, 1, cps}: the stage's columns are consecutive along dim 2, and the box rows past I1
@@ -117,6 +117,19 @@ constexpr int mma_index(int nt, int mt, int op) {
 constexpr int kMmaTableSize = mma_index(4, 8, OP_RESID) + 1;
 void register_stream_mma(StreamEntry *t);
 const StreamEntry &stream_mma_entry(int nt, int mt, int op);
+
+// ---------------------------------------------------------------- host configuration
+// Path selectors (documented in include/cp.h): environment switches between result-equivalent
+// code paths that the parity tests cover (e.g. CP_STREAM_MMA=0: DFMA consumers).  Read on every
+// call (nothing cached).  Any other variable name is rejected (returns dflt).
+int path_flag(const char *name, int dflt);
+// Tuning and debugging knobs (stage sizes, ring depth, kernel-skip masks ...): read from the
+// environment ONLY in a library built with -DCP_EXPERIMENTS (tools/); the shipped library
+// always uses the defaults, so no environment variable can change what it computes.
+int knob(const char *name, int dflt);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, bytes).
+cudaError_t ensure_smem_attr(const void *kernel, int bytes);
+int current_device();
 
 // Host: build the plan (geometry only; pointers filled by the caller).
 bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms);

@@ -19,9 +19,11 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "../../include/cp.h"
+#include "cp_internal.cuh"
 #include "mg_kernels.cuh"
 
 namespace cpk {
@@ -29,16 +31,13 @@ namespace {
 
 constexpr int kMaxTest = 8;
 constexpr int kMaxLevels = 40;
+// device `out` words of the relaxation calls (4 doubles each): every cp_als_sweep(s) call of a
+// cycle writes its own slot, and the host checks every slot's status at the next stopping test
+// (which synchronizes anyway), so a Cholesky failure on any level is reported (CP_ENOTSPD)
+constexpr int kOutSlots = 4096;
 
-static bool env_flag(const char *name, bool dflt) {
-  const char *e = getenv(name);
-  return (e && *e) ? atoi(e) != 0 : dflt;
-}
-
-static bool structured_restriction() {
-  const char *e = getenv("CP_MG_STRUCTURED");
-  return !(e && *e && atoi(e) == 0);
-}
+// CP_MG_STRUCTURED=0 (path selector): Galerkin tensors by the dense mode product
+static bool structured_restriction() { return path_flag("CP_MG_STRUCTURED", 1) != 0; }
 
 struct Arena {
   char *base = nullptr;
@@ -73,7 +72,10 @@ struct MG {
   int N = 0, R = 0, nt = 0, L = 0;
   Level lv[kMaxLevels];
   double *scratch[2] = {nullptr, nullptr};
-  double *out_fit = nullptr, *out_sweep = nullptr;
+  double *out_fit = nullptr, *out_slots = nullptr;
+  int nslot = 0, slot_hi = 0;  // next slot; slots used so far (checked at every stopping test)
+  std::vector<double> h_slots;
+  int failed_mode = -1;
   void *ws = nullptr;
   size_t ws_bytes = 0;
   cudaStream_t st = nullptr;
@@ -152,7 +154,7 @@ struct MG {
     scratch[0] = a.take((size_t)(lv[0].P / 2 + 1));
     scratch[1] = a.take((size_t)(lv[0].P / 4 + 1));
     out_fit = a.take(2 + N);
-    out_sweep = a.take(4);
+    out_slots = a.take((size_t)4 * kOutSlots);
     a.off = (a.off + 255) & ~(size_t)255;
     ws = a.dry ? nullptr : a.base + a.off;
     ws_bytes = wsb;
@@ -163,6 +165,24 @@ struct MG {
   bool ok(int rc) {
     if (rc != CP_OK && err == CP_OK) err = rc;
     return err == CP_OK;
+  }
+  // the out word of the next relaxation call (wraps: slots are re-read at every stopping test,
+  // and a cycle issues far fewer than kOutSlots relaxation calls)
+  double *next_out() {
+    double *o = out_slots + 4 * (size_t)(nslot % kOutSlots);
+    ++nslot;
+    if (nslot > slot_hi) slot_hi = nslot < kOutSlots ? nslot : kOutSlots;
+    return o;
+  }
+  // after fit()'s read-back: CP_ENOTSPD if any relaxation since the solve began failed
+  void check_slots() {
+    if (err != CP_OK) return;
+    for (int k = 0; k < (int)h_slots.size() / 4; ++k)
+      if (h_slots[4 * k + 2] != 0.0) {
+        err = CP_ENOTSPD;
+        failed_mode = (int)h_slots[4 * k + 3];
+        return;
+      }
   }
   void copy(double *dst, const double *src, size_t n) {
     if (err == CP_OK && cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
@@ -178,17 +198,17 @@ struct MG {
     Level &v = lv[l];
     // sweep + normalization (no sort) nu times: one fused launch on small levels
     if (sweeps > 0)
-      ok(cp_als_sweeps(&v.s, v.Z, v.nz2, A, nullptr, sweeps, CP_SWEEPS_NORMALIZE, out_sweep, ws, ws_bytes, cst));
+      ok(cp_als_sweeps(&v.s, v.Z, v.nz2, A, nullptr, sweeps, CP_SWEEPS_NORMALIZE, next_out(), ws, ws_bytes, cst));
   }
   // BNGS with RHS (eq:relaxinnersolve); finest level: normalize + sort
   void relax_fas(int l, double *const *A, const double *const *F, int sweeps) {
     Level &v = lv[l];
     if (l > 0) {  // coarse levels: no normalization between sweeps -> one call (fused when small)
-      if (sweeps > 0) ok(cp_als_sweeps(&v.s, v.Z, v.nz2, A, F, sweeps, 0, out_sweep, ws, ws_bytes, cst));
+      if (sweeps > 0) ok(cp_als_sweeps(&v.s, v.Z, v.nz2, A, F, sweeps, 0, next_out(), ws, ws_bytes, cst));
       return;
     }
     for (int k = 0; k < sweeps && err == CP_OK; ++k) {
-      ok(cp_als_sweep(&v.s, v.Z, v.nz2, A, F, out_sweep, ws, ws_bytes, cst));
+      ok(cp_als_sweep(&v.s, v.Z, v.nz2, A, F, next_out(), ws, ws_bytes, cst));
       ok(cp_normalize_sort(&v.s, A, 1, nullptr, ws, ws_bytes, cst));
     }
   }
@@ -206,12 +226,17 @@ struct MG {
     ok(cp_gradient(&v.s, v.Z, v.nz2, A, nullptr, out_fit, G, ws, ws_bytes, cst));  // NEXT-2: no residual pass
     cudaEventRecord(fev[1], st);
     h_fit.assign(2 + N, NAN);
+    h_slots.assign((size_t)4 * slot_hi, 0.0);
     if (err == CP_OK &&
-        cudaMemcpyAsync(h_fit.data(), out_fit, (2 + N) * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        (cudaMemcpyAsync(h_fit.data(), out_fit, (2 + N) * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+         (slot_hi > 0 &&
+          cudaMemcpyAsync(h_slots.data(), out_slots, h_slots.size() * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)))
       err = CP_ECUDA;
     if (err == CP_OK && cudaStreamSynchronize(st) != cudaSuccess) err = CP_ECUDA;
     float ms = 0.f;
     if (err == CP_OK && cudaEventElapsedTime(&ms, fev[0], fev[1]) == cudaSuccess) fit_seconds += 1e-3 * ms;
+    check_slots();
+    if (err != CP_OK) return NAN;
     if (gradnorm2)
       for (int n = 0; n < N; ++n) gradnorm2[n] = h_fit[2 + n];
     return h_fit[1];
@@ -470,14 +495,15 @@ void cp_mg_default_params(cp_mg_params *p) {
   p->coarsest = 0;
   p->solve_stagnation_after = 5;
   p->max_trace = 0;
+  p->fmg_guard = 0;
 }
 
 size_t cp_mg_workspace_bytes(const cp_shape *s, const cp_mg_params *p) {
   if (!s || !p || s->N < 2 || s->N > CP_MAX_N || s->R < 1 || s->R > CP_MAX_R) return 0;
-  static MG mg;  // large struct: keep off the stack
-  if (!mg.plan(*s, *p)) return 0;
+  std::unique_ptr<MG> mg(new MG());  // large struct: on the heap, one per call (reentrant)
+  if (!mg->plan(*s, *p)) return 0;
   Arena a;
-  return mg.layout(a);
+  return mg->layout(a);
 }
 
 int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const double *const *T,
@@ -486,10 +512,14 @@ int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const doub
   if (!s || !Z || !A || !T || !prm || !report || !ws) return CP_EINVAL;
   if (s->N < 2 || s->N > CP_MAX_N || s->R < 1 || s->R > CP_MAX_R) return CP_EINVAL;
   if (prm->use_fmg && !A_fmg) return CP_EINVAL;
-  static MG mgs;
-  MG &mg = mgs;
-  mg.destroy_events();
-  mg = MG();
+  // all driver state lives in this call's MG (heap) and the caller's workspace: two solves may
+  // run concurrently (different workspaces, streams or devices)
+  std::unique_ptr<MG> mgp(new MG());
+  MG &mg = *mgp;
+  struct EvGuard {
+    MG &m;
+    ~EvGuard() { m.destroy_events(); }
+  } evguard{mg};
   if (!mg.plan(*s, *prm)) return CP_EINVAL;
   {
     Arena dry;
@@ -526,7 +556,7 @@ int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const doub
     stream = reinterpret_cast<cp_stream_t>(own.s);
   }
   mg.cst = stream;
-  const bool want_graph = env_flag("CP_MG_GRAPH", true) && mg.st != nullptr;
+  const bool want_graph = path_flag("CP_MG_GRAPH", 1) != 0 && mg.st != nullptr;
   bool captured = false;
   // one FAS V-cycle from the finest level (Algorithm 2), replayed from a graph when possible
   auto v_cycle = [&]() {
@@ -566,6 +596,7 @@ int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const doub
   cp_shape s1 = *s;
   s1.R = 1;
   mg.ok(cp_norm2(&s1, Z, f.nz2, mg.ws, mg.ws_bytes, stream));
+  if (cudaMemsetAsync(mg.out_slots, 0, (size_t)4 * kOutSlots * 8, mg.st) != cudaSuccess) mg.err = CP_ECUDA;
 
   int ntrace = 0, cycles = 0, setup_cycles = 0, solve_cycles = 0, rebuilds = 0;
   auto record = [&](int phase, int cyc, double g) {
@@ -595,21 +626,23 @@ int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const doub
     if (cyc >= prm->min_setup_cycles && gn > (1.0 - prm->stagnation_eps) * g_old) break;
     g_old = gn;
   }
-  // optional FMG cycle, then a down-sweep rebuild of the operators
-  // (reading R29: the FMG approximation replaces the setup iterate only if it lowers g;
-  // otherwise the setup iterate is restored and the operators are kept)
+  // "Multilevel + FMG": one FMG-CP-FAS cycle computes a new approximation to the boot
+  // factors, then the transfer operators are rebuilt by one down-sweep of CP-AMG-mult (boot
+  // factors not updated).  fmg_guard = 1 selects reading R29 instead (not the paper's default):
+  // the FMG result is kept only if it lowers g, else the setup iterate is restored and the
+  // operators are not rebuilt.
   if (!converged && prm->use_fmg && mg.err == CP_OK) {
     for (int n = 0; n < N; ++n) mg.copy(f.prev[n], f.A[n], (size_t)s->dims[n] * R);
     mg.fmg(A_fmg);
     const double gf = mg.fit(0, f.A, nullptr);
     ++cycles;
     record(1, cycles, gf);
-    if (gf < g) {
+    if (prm->fmg_guard && !(gf < g)) {
+      for (int n = 0; n < N; ++n) mg.copy(f.A[n], f.prev[n], (size_t)s->dims[n] * R);
+    } else {
       g = gf;
       converged = g < prm->tol;
       if (!converged) mg.setup_cycle(0, false, false);
-    } else {
-      for (int n = 0; n < N; ++n) mg.copy(f.A[n], f.prev[n], (size_t)s->dims[n] * R);
     }
   }
   // solve phase
@@ -653,20 +686,27 @@ int cp_mg_solve(const cp_shape *s, const double *Z, double *const *A, const doub
   report[8] = rebuilds;
   report[9] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   report[10] = mg.fit_seconds;
+  report[11] = mg.failed_mode;
   return (mg.err == CP_ENOTSPD) ? CP_OK : mg.err;
 }
 
+// cp_als_solve's own region after the sweep workspace: ||Z||^2, the fit output and one out word
+// per sweep slot (a sweep k writes slot k mod kAlsSlots; every slot written since the last check
+// is read back with g)
+constexpr int kAlsSlots = 256;
+constexpr size_t kAlsSmall = 64 + 4 * kAlsSlots;  // doubles
+
 size_t cp_als_solve_workspace_bytes(const cp_shape *s) {
   const size_t w = cp_workspace_bytes(s);
-  return w == 0 ? 0 : w + 4096;
+  return w == 0 ? 0 : w + kAlsSmall * sizeof(double);
 }
 
 int cp_als_solve(const cp_shape *s, const double *Z, double *const *A, double tol, int32_t max_iters,
                  int32_t check_every, double *report, void *ws, size_t ws_bytes, cp_stream_t stream) {
-  if (!s || !Z || !A || !report || !ws || check_every < 1) return CP_EINVAL;
+  if (!s || !Z || !A || !report || !ws || check_every < 1 || max_iters < 1) return CP_EINVAL;
   const size_t w = cp_workspace_bytes(s);
   if (w == 0) return CP_EINVAL;
-  if (ws_bytes < w + 4096) return CP_EWORKSPACE;
+  if (ws_bytes < w + kAlsSmall * sizeof(double)) return CP_EWORKSPACE;
   // the legacy default stream cannot be captured: run the solve on a private blocking stream
   // (implicitly ordered with the legacy stream) and graph-capture there
   struct Own {
@@ -686,31 +726,35 @@ int cp_als_solve(const cp_shape *s, const double *Z, double *const *A, double to
     stream = reinterpret_cast<cp_stream_t>(st);
   }
   double *small = reinterpret_cast<double *>(static_cast<char *>(ws) + w);
-  double *nz2 = small, *out = small + 8, *fitout = small + 16;
+  double *nz2 = small, *fitout = small + 16, *slots = small + 64;
   const auto t0 = std::chrono::steady_clock::now();
   double fit_s = 0.0;
   cp_shape s1 = *s;
   s1.R = 1;
   int rc = cp_norm2(&s1, Z, nz2, ws, w, stream);
   if (rc) return rc;
-  std::vector<double> h(2 + s->N);
+  if (cudaMemsetAsync(slots, 0, 4 * kAlsSlots * sizeof(double), st) != cudaSuccess) return CP_ECUDA;
+  const int nslots = check_every < kAlsSlots ? check_every : kAlsSlots;
+  std::vector<double> h(2 + s->N), hs((size_t)4 * nslots);
   double g = NAN;
-  int it = 0, status = 1;
+  int it = 0, status = 1, failed_mode = -1;
+  // one sweep (+ normalization) into out slot k
+  auto sweep = [&](int k) -> int {
+    int r = cp_als_sweep(s, Z, nz2, A, nullptr, slots + 4 * (k % kAlsSlots), ws, w, stream);
+    if (r == CP_OK) r = cp_normalize_sort(s, A, 0, nullptr, ws, w, stream);
+    return r;
+  };
   // The check_every sweeps (+ normalization) between two stopping tests are captured once into
   // a CUDA graph and replayed: for small tensors the loop is launch-bound (~10 launches per
   // sweep).  Same kernels in the same order -- results are bitwise those of the plain loop.
   // Needs a capturable stream (not the legacy default stream); CP_ALS_GRAPH=0 disables.
   cudaGraphExec_t &gexec = own.g;
   {
-    const char *e = getenv("CP_ALS_GRAPH");
-    const bool want = !(e && *e && atoi(e) == 0) && st != nullptr && check_every > 1;
+    const bool want = path_flag("CP_ALS_GRAPH", 1) != 0 && st != nullptr && check_every > 1;
     if (want) {
       cudaGraph_t graph = nullptr;
       bool okc = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-      for (int k = 0; okc && k < check_every; ++k) {
-        okc = cp_als_sweep(s, Z, nz2, A, nullptr, out, ws, w, stream) == CP_OK &&
-              cp_normalize_sort(s, A, 0, nullptr, ws, w, stream) == CP_OK;
-      }
+      for (int k = 0; okc && k < check_every; ++k) okc = sweep(k) == CP_OK;
       const cudaError_t ec = cudaStreamEndCapture(st, &graph);
       if (okc && ec == cudaSuccess && graph != nullptr &&
           cudaGraphInstantiate(&gexec, graph, 0) != cudaSuccess)
@@ -725,18 +769,23 @@ int cp_als_solve(const cp_shape *s, const double *Z, double *const *A, double to
       if (cudaGraphLaunch(gexec, st) != cudaSuccess) return CP_ECUDA;
       it += check_every - 1;  // the graph ran sweeps it .. it + check_every - 1
     } else {
-      if ((rc = cp_als_sweep(s, Z, nz2, A, nullptr, out, ws, w, stream))) return rc;
-      if ((rc = cp_normalize_sort(s, A, 0, nullptr, ws, w, stream))) return rc;
+      if ((rc = sweep((it - 1) % check_every))) return rc;
     }
     if (it % check_every == 0 || it == max_iters) {
       const auto tf = std::chrono::steady_clock::now();
       if ((rc = cp_gradient(s, Z, nz2, A, nullptr, fitout, nullptr, ws, w, stream))) return rc;
       if (cudaMemcpyAsync(h.data(), fitout, (2 + s->N) * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+          cudaMemcpyAsync(hs.data(), slots, hs.size() * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
           cudaStreamSynchronize(st) != cudaSuccess)
         return CP_ECUDA;
       fit_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - tf).count();
       g = h[1];
-      if (g != g) {
+      for (int k = 0; k < nslots; ++k)
+        if (hs[4 * k + 2] != 0.0) {
+          status = CP_ENOTSPD;
+          failed_mode = (int)hs[4 * k + 3];
+        }
+      if (status == CP_ENOTSPD || g != g) {
         status = CP_ENOTSPD;
         break;
       }
@@ -754,6 +803,7 @@ int cp_als_solve(const cp_shape *s, const double *Z, double *const *A, double to
   report[3] = status;
   report[4] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   report[5] = fit_s;
+  report[6] = failed_mode;
   return CP_OK;
 }
 

@@ -235,25 +235,14 @@ static size_t dmma_smem(bool a_mc, bool b_nc) {
   return 2 * sizeof(double) * (size_t)((a_mc ? TBK * AMS : TBM * AKS) + (b_nc ? TBK * BNS : TBN * BKS));
 }
 static cudaError_t dmma_attrs() {
-  static cudaError_t done = [] {
-    cudaError_t e = cudaFuncSetAttribute(gemm_dmma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)dmma_smem(true, true));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(gemm_dmma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)dmma_smem(true, false));
-    return e;
-  }();
-  return done;
-}
-
-static int env_flag(const char *name, int dflt) {
-  const char *v = getenv(name);
-  return (v && *v) ? atoi(v) : dflt;
+  cudaError_t e = ensure_smem_attr((const void *)gemm_dmma_kernel<true, true>, (int)dmma_smem(true, true));
+  if (e == cudaSuccess) e = ensure_smem_attr((const void *)gemm_dmma_kernel<true, false>, (int)dmma_smem(true, false));
+  return e;
 }
 
 cudaError_t launch_mode_product(int N, const int64_t *dims, const double *Z, int mode,
                                 const double *U, int64_t J, double *X, cudaStream_t st) {
-  if (env_flag("CP_MODEPROD_DMMA", 1)) {
+  if (path_flag("CP_MODEPROD_DMMA", 1)) {
     if (cudaError_t e = dmma_attrs()) return e;
     int64_t left = 1, right = 1;
     for (int k = 0; k < mode; ++k) left *= dims[k];

@@ -298,10 +298,8 @@ extern "C" int cp_restrict_structured(int32_t N, const int64_t *dims, const doub
     const int64_t nfib = S * O;
     const bool v2 = (S % 2 == 0) && ((uintptr_t)Z % 16 == 0) && ((uintptr_t)X % 16 == 0);
     const int64_t nthr = v2 ? nfib / 2 : nfib;
-    const char *eb = getenv("CP_RESTRICT_BLOCK");
-    const int bs = (eb && *eb) ? atoi(eb) : 128;  // 128: ~7 blocks per SM, small tail
-    const char *et = getenv("CP_RESTRICT_TMA");
-    const bool tma = !(et && *et && atoi(et) == 0) && (S % 2 == 0) && ((uintptr_t)Z % 16 == 0);
+    const int bs = knob("CP_RESTRICT_BLOCK", 128);  // 128: ~7 blocks per SM, small tail
+    const bool tma = knob("CP_RESTRICT_TMA", 1) != 0 && (S % 2 == 0) && ((uintptr_t)Z % 16 == 0);
     if (tma) {
       const int64_t nslab = (S + kRtW - 1) / kRtW;
       e = launch_k(restrict_tma_kernel, dim3((unsigned)(O * nslab)), dim3(kRtW), 0, st, Z, I, Ic, S, nslab,

@@ -119,8 +119,10 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
   const double *A = a.A[k];
   const int tid = threadIdx.x;
   if (blockIdx.x == 0 && tid == 0 && a.status != nullptr) {
-    a.status[0] = 0.0;
-    a.status[1] = -1.0;
+    if (!a.keep_status) {
+      a.status[0] = 0.0;
+      a.status[1] = -1.0;
+    }
     *reinterpret_cast<unsigned *>(a.status + kTicketSlot) = 0u;  // solve completion ticket
     *reinterpret_cast<unsigned *>(a.status + kTicketSlot2) = 0u;  // ylsolve ticket
   }

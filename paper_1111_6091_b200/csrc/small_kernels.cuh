@@ -92,6 +92,8 @@ struct PrepArgs {
   double *At[CP_MAX_N];
   double *gpre;    // per-block partial Grams (may be null: no Grams)
   double *status;  // may be null
+  int keep_status; // 1: leave status[0..1] as they are (a later sweep of one cp_als_sweeps call:
+                   // an earlier failure stays reported and the later solves skip); tickets reset
   unsigned *zero;  // zeroed by block 0 (Y_L segment tickets), may be null
   int nzero;
 };

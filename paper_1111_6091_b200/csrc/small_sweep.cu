@@ -472,11 +472,9 @@ cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double 
   a.normZ2 = normZ2;
   a.out = out;
   const size_t smem = small_sweep_smem_bytes(s);
-  static size_t attr_set = 0;
-  if (smem > 48 * 1024 && smem > attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(small_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (smem > 48 * 1024) {
+    cudaError_t e = ensure_smem_attr((const void *)small_sweep_kernel, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = smem;
   }
   return launch_k(small_sweep_kernel, dim3(1), dim3(kT), smem, st, a);
 }

@@ -25,19 +25,7 @@ struct SmallSweepArgs {
   int grad;               // 1: cp_gradient at this iterate (no updates): out = f, g, ||G^(n)||^2
   int normalize;          // 1: eq:ALSnorm (no sort) after every sweep (CP_SWEEPS_NORMALIZE)
   double *G[CP_MAX_N];    // gradient mode: G^(n) outputs (entries may be null)
-  unsigned *bar;          // medium kernel: grid-barrier counter (zeroed before the launch)
-  double *mpart;          // medium kernel: 2 x G x imax x R partial M buffers
 };
-
-constexpr int64_t kMediumSweepMaxP = 1536 * 1024;  // medium_sweep.cu: ~6 K elements per CTA, <= 1 CTA/SM
-
-// medium_sweep.cu: CTAs for shape s (0: not a medium tensor), shared memory per CTA, workspace
-// doubles (barrier + partial M buffers) and the cooperative launch
-int medium_sweep_ctas(const cp_shape &s, int sms);
-size_t medium_sweep_smem_bytes(const cp_shape &s, int G);
-size_t medium_sweep_ws_doubles(const cp_shape &s, int G);
-cudaError_t launch_medium_sweep(const cp_shape &s, int G, const double *Z, const double *normZ2, double *const *A,
-                                const double *const *F, int nsweeps, double *out, double *ws, cudaStream_t st);
 
 // dynamic shared memory the kernel needs for shape s, or 0 if s is not small enough
 size_t small_sweep_smem_bytes(const cp_shape &s);

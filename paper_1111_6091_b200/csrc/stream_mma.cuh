@@ -455,12 +455,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 template <int NT, int MT, int OP>
 cudaError_t launch_stream_mma_t(const StreamPlan &p, cudaStream_t st) {
   auto kern = stream_mma_kernel<NT, MT, OP>;
-  static bool attr_done = false;  // per instantiation
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  if (cudaError_t e = ensure_smem_attr((const void *)kern, 200 * 1024)) return e;
   return launch_kc(kPdlStream, kern, dim3(p.Gc * p.RB), dim3(kStreamThreads), (size_t)p.smem_bytes, st, p);
 }
 

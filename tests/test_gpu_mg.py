@@ -159,3 +159,38 @@ def test_mg_graph_replayed_v_cycles_are_bitwise_the_plain_launches(monkeypatch):
         np.testing.assert_array_equal(t1[:, :3], t0[:, :3])
         for a, b in zip(A1, A0_):
             np.testing.assert_array_equal(a, b)
+
+
+def test_als_solve_reports_enotspd():
+    """A zero factor column makes every Gamma^(n) with n != that mode singular (the Keller
+    condition of P:362 fails): the first sweep's mode-0 solve hits a non-positive pivot.  The
+    factors stay finite, so g alone would not show it; cp_als_solve must stop with CP_ENOTSPD
+    and the failing mode (the oracle sweep reports the same), not run to max_iters."""
+    dims, R = (12, 10, 8), 3
+    Z, A0 = cpsynth.random_problem(dims, R, seed=31)
+    A0[1][:, 1] = 0.0
+    _, oo = oracle.als_sweep(Z, dims, A0)
+    assert oo[2] == cp.CP_ENOTSPD and oo[3] == 0
+    for check_every in (1, 10):
+        Ad = [dev_factor(a) for a in A0]
+        rep = cp.als_solve(dev_tensor(Z), dims, Ad, tol=1e-12, max_iters=200, check_every=check_every)
+        assert int(rep["status"]) == cp.CP_ENOTSPD
+        assert int(rep["failed_mode"]) == 0
+        assert int(rep["iterations"]) == check_every
+
+
+def test_mg_solve_reports_enotspd():
+    """The same zero boot-factor column in cp_mg_solve: the finest-level setup relaxation fails;
+    the driver reads every relaxation's status word at the next stopping test and reports
+    CP_ENOTSPD (report status and failing mode) instead of iterating to the cycle limit."""
+    d = cpsynth.make_config("c0", with_transfer=False)
+    dims, R, Z = d["dims"], d["R"], d["Z"]
+    A0 = [a.copy(order="F") for a in d["A0"]]
+    A0[2][:, 0] = 0.0
+    T0 = [cpsynth.uniform_init(dims, R, seed=10 + t) for t in range(2)]
+    Ad = [dev_factor(a) for a in A0]
+    rep, tr = cp.mg_solve(dev_tensor(Z), dims, Ad, [[dev_factor(t) for t in b] for b in T0],
+                          params=cp.MGParams.default(coarsest=10, max_cycles=20))
+    assert int(rep["status"]) == cp.CP_ENOTSPD
+    assert int(rep["failed_mode"]) == 0
+    assert int(rep["cycles"]) <= 1

@@ -255,13 +255,9 @@ def test_fused_small_multi_sweep_vs_oracle(dims, R, F):
 
 
 @pytest.mark.parametrize("name", ["c1", "c2"])
-@pytest.mark.parametrize("medium", ["1", "0"])
-def test_multi_sweep_call_general_path_vs_oracle(name, medium, monkeypatch):
+def test_multi_sweep_call_general_path_vs_oracle(name):
     """cp_als_sweeps on tensors above the single-CTA fused-kernel limit (P > 16384): nu = 3
-    sweeps in one call -- one cooperative launch of the medium fused kernel (medium_sweep.cu),
-    or with CP_MEDIUM_SWEEP=0 the general multi-kernel path -- equal 3 oracle sweeps, F
-    included."""
-    monkeypatch.setenv("CP_MEDIUM_SWEEP", medium)
+    sweeps in one call on the general multi-kernel path equal 3 oracle sweeps, F included."""
     d = config(name)
     dims, Z, A = d["dims"], d["Z"], d["A0"]
     R = A[0].shape[1]
@@ -269,7 +265,7 @@ def test_multi_sweep_call_general_path_vs_oracle(name, medium, monkeypatch):
     Fh = [0.01 * cpsynth.random_matrix(I, R, 30 + k) for k, I in enumerate(dims)]
     Zd, Ad = dev_problem(Z, A)
     out = host_tensor(cp.als_sweep(Zd, dims, Ad, cp.norm2(Zd, dims), F=[dev_factor(f) for f in Fh], nsweeps=3))
-    assert (cp.last_launch_count() == 1) if medium == "1" else (cp.last_launch_count() > 3)
+    assert cp.last_launch_count() > 3
     Ao = [a.copy(order="F") for a in A]
     for _ in range(3):
         Ao, oo = oracle.als_sweep(Z, dims, Ao, F=Fh, normZ2=nz2)
@@ -297,19 +293,25 @@ def test_multi_sweep_normalized_vs_oracle(dims, R, small, monkeypatch):
 
 
 @pytest.mark.parametrize("R", [2, 8])
-def test_fused_small_sweep_reports_enotspd_mid_run(R):
+@pytest.mark.parametrize("small", ["1", "0"])
+def test_multi_sweep_reports_enotspd_mid_run(R, small, monkeypatch):
     """Z = 0: the mode-0 update gives A^(0) = 0, so Gamma^(1) = 0 is singular in the first sweep of
     a multi-sweep call: status CP_ENOTSPD, failed mode 1, f = NaN -- as the oracle reports
-    (R = 2: one-thread Cholesky; R = 8: warp Cholesky)."""
-    dims = (6, 5, 4)
+    (R = 2: one-thread Cholesky; R = 8: warp Cholesky) -- on the fused path and on the general
+    path, where the later sweeps of the call must neither clear the status nor touch the factors
+    (they equal the oracle's after its failing sweep)."""
+    monkeypatch.setenv("CP_SMALL_SWEEP", small)
+    dims = (6, 5, 4) if small == "1" else (40, 30, 20)
     _, A = cpsynth.random_problem(dims, R, seed=9)
     Z = np.zeros(tuple(reversed(dims)))
     Zd, Ad = dev_problem(Z, A)
     out = host_tensor(cp.als_sweep(Zd, dims, Ad, cp.norm2(Zd, dims), nsweeps=5))
-    _, oo = oracle.als_sweep(Z, dims, A)
+    Ao, oo = oracle.als_sweep(Z, dims, A)
     assert out[2] == cp.CP_ENOTSPD == oo[2]
     assert out[3] == oo[3] == 1
     assert math.isnan(out[0])
+    for a, b in zip(Ad, Ao):
+        np.testing.assert_array_equal(host_factor(a), b)
 
 
 def test_sweep_rank1_exact():

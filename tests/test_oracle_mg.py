@@ -82,3 +82,85 @@ def test_dense_problem_converges(fmg):
     # and the minimizer is a stationary point of the plain functional
     g = oracle.gradient(Z, dims, A, want_G=False)[0][1]
     assert g < 1e-10
+
+
+def _linear_exact_problem(I=17, R=2, seed=1):
+    """Z = [[A*]] whose factor columns lie in span{1, i}: orthonormal basis of the linear
+    vectors, rotated and scaled per mode.  Relaxation keeps every factor in that span (for an
+    exact Z, M^(n) = A*^(n) (*_k A*^(k)T A^(k)) has columns in range(A*^(n))), linear vectors are
+    fitted exactly by the weights (1/2, 1/2) at interior F points (eq:LSQinterp; odd I: no
+    one-sided end), so range(Phat) contains A* and the Galerkin tensor Z x_n Phat^T is exactly
+    [[Phat^T A*]] -- a two-level hierarchy on which the exact solution is reachable."""
+    rng = np.random.default_rng(seed)
+    x = np.arange(I) / (I - 1)
+    Qb = np.linalg.qr(np.stack([np.ones(I), x], 1))[0]
+
+    def lin():
+        th = rng.uniform(0, 2 * np.pi)
+        Rm = np.array([[np.cos(th), -np.sin(th)], [np.sin(th), np.cos(th)]])
+        return np.asfortranarray(Qb @ Rm * rng.uniform(0.5, 2))
+
+    dims = (I,) * 3
+    At = [lin() for _ in dims]
+    Z = cpsynth.kruskal(At)
+    T0 = [[lin() for _ in dims] for _ in range(2)]
+    return dims, R, Z, At, T0, lin, rng
+
+
+@pytest.mark.parametrize("nu_fmg", [1, 50])
+def test_fmg_reaches_exact_solution_two_levels(nu_fmg):
+    """Pin of the FMG cycle on its own (Algorithm 3).  On the two-level exact problem
+    above: nu ALS iterations on the coarsest level from a random guess, Phat-interpolation
+    (step 3) and one CP-FAS V-cycle with F = 0 (step 4) must give g < 1e-12.  With nu_fmg = 1 the
+    coarse ALS is far from converged and interpolation alone leaves g ~ 0.5 -- only a working
+    CP-FAS cycle inside fmg() closes the gap; with nu_fmg = 50 the coarse ALS converges and the
+    interpolation must reproduce the exact factors.  A broken interpolation, a skipped
+    coarse-grid correction or a wrong FAS right-hand side fails one of the two.  (Deterministic
+    instance, seed 1; like any nonlinear solve, an unlucky random guess can end at another
+    stationary point -- seed 5 does, with and without FMG.)"""
+    dims, R, Z, At, T0, lin, rng = _linear_exact_problem()
+    o = mg.MGOracle(Z, dims, R, dict(mg.DEFAULTS, coarsest=9, nu_fmg=nu_fmg))
+    assert [l.dims for l in o.lv] == [(17,) * 3, (9,) * 3]
+    o.lv[0].A = [lin() for _ in dims]
+    o.lv[0].T = T0
+    o.setup_cycle(0, True, False)            # operators from the (relaxed) test blocks only
+    for n in range(3):                       # range(Phat) contains the exact factors
+        Ph = o.lv[0].Ph[n]
+        assert np.linalg.norm(Ph @ (Ph.T @ At[n]) - At[n]) <= 1e-12 * np.linalg.norm(At[n])
+    Af = [np.asfortranarray(rng.uniform(size=(d, R))) for d in o.lv[-1].dims]
+    # interpolation of the coarse ALS result alone (steps 1 and 3, no step 4)
+    Ac = o.relax_setup(1, [a.copy(order="F") for a in Af], nu_fmg)
+    g_interp = o.fit(0, o.interp(0, Ac))[0][1]
+    o.fmg(Af)
+    g = o.fit(0, o.lv[0].A)[0][1]
+    assert g < 1e-12, (g, g_interp)
+    if nu_fmg == 1:
+        assert g_interp > 1e-2, g_interp
+
+
+def test_fmg_combination_paper_default_and_guard():
+    """"Multilevel + FMG": after the setup cycles ONE FMG cycle computes a new
+    approximation to the boot factors and the operators are rebuilt by one down-sweep; the
+    solve phase continues from the FMG result even if it raised g (the paper's default,
+    fmg_guard = 0).  Reading R29 (fmg_guard = 1) restores the setup iterate when FMG raised g,
+    so its solve cycles are exactly those of the run without FMG.  BASELINE.json c0 with its
+    2-level cycle (coarsest 10)."""
+    d = cpsynth.make_config("c0", with_transfer=False)
+    dims, R = d["dims"], d["R"]
+    T0 = [cpsynth.uniform_init(dims, R, seed=10 + t) for t in range(2)]
+    Af = cpsynth.uniform_init(mg.levels(dims, R, 10)[-1], R, seed=99)
+    kw = dict(coarsest=10, tol=1e-9, max_cycles=40)
+    _, r0, t0 = mg.mg_solve(d["Z"], dims, d["A0"], T0, **kw)
+    _, rp, tp = mg.mg_solve(d["Z"], dims, d["A0"], T0, A_fmg=Af, use_fmg=1, **kw)
+    _, rg, tg = mg.mg_solve(d["Z"], dims, d["A0"], T0, A_fmg=Af, use_fmg=1, fmg_guard=1, **kw)
+    ns = r0["setup_cycles"]
+    assert rp["setup_cycles"] == rg["setup_cycles"] == ns
+    gf = tp[ns, 2]
+    assert tp[ns, 0] == 1 and tg[ns, 0] == 1 and tg[ns, 2] == gf
+    assert gf > tp[ns - 1, 2]                      # on c0 the FMG result is worse than the setup iterate
+    # paper default: the first solve cycle starts from the FMG result, not from the setup iterate
+    assert tp[ns + 1, 2] != t0[ns, 2]
+    # guard: the solve phase is that of the run without FMG, shifted by the one FMG cycle
+    np.testing.assert_array_equal(tg[ns + 1:, 2], t0[ns:, 2])
+    for r in (r0, rp, rg):
+        assert r["status"] == 0 and r["g"] < 1e-9

@@ -63,6 +63,26 @@ def rel(a, b):
 # ---------------------------------------------------------------- MTTKRP
 
 
+def test_norm2_closed_forms_and_library():
+    """||Z||^2 of eq:CPfunctional = sum of squared entries: (i) the all-ones tensor of
+    P elements gives exactly P; (ii) a scaled unit tensor c*e_k gives c^2; (iii) integer entries
+    0..P-1 give the closed form (P-1)P(2P-1)/6 exactly (every partial sum is an integer below
+    2^53); (iv) random data agrees with numpy's dot product (a different summation order) to
+    a few ulps.  Pins oracle_norm2 (previously "parity unpinned")."""
+    for dims in [(1,), (3, 4, 2), (7, 5, 3, 2)]:
+        P = int(np.prod(dims))
+        assert oracle.norm2(np.ones(cpsynth.tensor_shape(dims))) == float(P)
+        e = np.zeros(P)
+        e[P // 2] = -3.5
+        assert oracle.norm2(e) == 12.25
+        v = np.arange(P, dtype=np.float64)
+        assert oracle.norm2(v) == float((P - 1) * P * (2 * P - 1) // 6)
+    Z, _ = cpsynth.random_problem((33, 17, 9), 1, seed=77)
+    ref = float(np.dot(Z.reshape(-1), Z.reshape(-1)))
+    assert abs(oracle.norm2(Z) - ref) <= 1e-13 * ref
+    assert oracle.norm2(np.zeros(5)) == 0.0
+
+
 def test_kr_order_worked_example(golden_dir):
     """KR ordering of Phi: the worked example A (.) B must come out of the
     oracle's mode-3 MTTKRP of a 2x2x4 tensor whose mode-3 unfolding is the identity."""
