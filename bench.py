@@ -34,7 +34,30 @@ import cpsynth  # noqa: E402
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
-DMMA_PEAK_TF = 37.0    # fp64 mma.sync (DMMA) TFLOP/s measured on this pool (tools/microbench.cu)
+PEAKS_LIB = os.path.join(ROOT, "paper_1111_6091_b200", "lib", "libcppeaks.so")
+
+
+def fp64_peaks():
+    """DFMA and DMMA TFLOP/s measured in THIS run (libcppeaks.so, include/cp_peaks.h): the fp64
+    roofline denominators MEASURED_PEAKS.json lacks."""
+    import ctypes
+    L = ctypes.CDLL(PEAKS_LIB)
+    a, b = ctypes.c_double(), ctypes.c_double()
+    rc = L.cpp_fp64_peaks(ctypes.byref(a), ctypes.byref(b), 5)
+    if rc != 0:
+        raise RuntimeError(f"cpp_fp64_peaks failed ({rc})")
+    return {"dfma_tflops": a.value, "dmma_tflops": b.value,
+            "source": "libcppeaks.so in this run: best of 5 event-timed launches, 8 CTAs x 256 threads per SM "
+                      "(DFMA: 8 independent fma chains/thread; DMMA: mma.sync m8n8k4 f64, 8 accumulators/warp)"}
+
+
+def launch_floor_us():
+    import ctypes
+    L = ctypes.CDLL(PEAKS_LIB)
+    u = ctypes.c_double()
+    if L.cpp_launch_floor_us(2000, ctypes.byref(u)) != 0:
+        return None
+    return u.value
 
 
 def parse():
@@ -294,6 +317,12 @@ def main():
         tr = json.load(open(TRAFFIC_PATH)).get(args.workload)
         if tr:
             traffic = tr.get("dram_bytes_per_launch")
+    peaks64 = fp64_peaks()
+    # the FP64 tensor pipe the consumers run on (DMMA, mma.sync m8n8k4): 2 x (8 NT) flops per Z element
+    # per launch (ranks padded to the n-tiles of 8), against the DMMA peak measured in this run;
+    # the DFMA pipe is idle in these kernels (ncu: sm__inst_executed_pipe_fp64 ~1 %)
+    rpad = 8 * ((R + 7) // 8)
+    dmma_tf = (2.0 * rpad * P) / (avg_ms / 1000.0) / 1e12 if nlaunch_prof else None
     roofline = {"kernel": "stream_mma_kernel (the two Z passes of the dimension-tree sweep, FP64 "
                           "tensor-core consumers: Y_L pass + mode-2 MTTKRP pass)", "bound": "hbm",
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -303,7 +332,14 @@ def main():
                 "share_of_step": (prof_ms / ms_prof) if ms_prof > 0 else None,
                 "timed_region": "a second K-step loop of the same sweep with CUDA events around every "
                                 "streaming-kernel launch (the headline loop runs without them)",
-                "frac_of_8TBs_nominal": (achieved / 8000.0) if achieved else None}
+                "frac_of_8TBs_nominal": (achieved / 8000.0) if achieved else None,
+                "pipes": {"fp64_tensor_dmma": {"achieved_tflops": dmma_tf, "peak_tflops": peaks64["dmma_tflops"],
+                                               "frac": dmma_tf / peaks64["dmma_tflops"] if dmma_tf else None,
+                                               "work": f"2 x {rpad} (ranks padded to n-tiles of 8) flops per Z element"},
+                          "fp64_dfma": {"peak_tflops": peaks64["dfma_tflops"],
+                                        "note": "not used by this kernel (DMMA consumers); ncu pipe_fp64 ~1 %"},
+                          "hbm_frac": (achieved / peak) if achieved else None},
+                "fp64_peaks": peaks64}
     # the whole step against the same peak: the sweep's algorithmic bytes (every streaming launch
     # of one sweep, as counted for the kernel above) at the copy peak vs the measured step time
     step_bytes = prof_bytes / max(1, args.steps) if nlaunch_prof < 8192 else float("nan")  # (cp.h: 8192 recorded launches)
@@ -315,7 +351,7 @@ def main():
     # ---- extra rows (same run, outside the timed region)
     rows = {}
     if not args.no_rows:
-        rows = time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P)
+        rows = time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P, peaks64)
 
     # ---- e2e through the public API with host buffers
     e2e = time_e2e(cp, torch, d, Zh, Zd, A0, A, nz, ws, dev, stream, dims, R, P, min(args.steps, 10))
@@ -340,7 +376,8 @@ def main():
             "value_1_thread": val1, "sample_1_thread": f"{steps1} sample steps in {t1:.1f} s on one host core",
             "sample": (f"oracle MTTKRP of a contiguous 1/16 of the output rows of every mode per "
                        f"sample step, {steps} steps in {t:.1f} s on the host cores, scaled to sweeps/s "
-                       f"(R x R solves not timed)")}
+                       f"(R x R solves not timed)"),
+            "rows": oracle_rows(cores)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -348,7 +385,35 @@ def main():
     return 0
 
 
-def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
+def oracle_rows(cores):
+    """The oracle beside the GPU rows: the multigrid solve on c0-c2 (per cycle:
+    the first cycles of each solve, c0 to the tolerance) and a dense restriction mode product
+    (a 1/16 slab of the c3 shape, scaled), on the host cores."""
+    import oracle
+    from oracle import mg
+    out = {"cores": cores}
+    for name, coarsest, maxc in (("c0", 10, 500), ("c1", 0, 4), ("c2", 25, 3)):
+        dc = cpsynth.make_config(name, with_transfer=False)
+        dd, Rc = dc["dims"], dc["R"]
+        T0 = [cpsynth.uniform_init(dd, Rc, seed=10 + t) for t in range(2)]
+        t0 = time.perf_counter()
+        _, rep, _ = mg.mg_solve(dc["Z"], dd, dc["A0"], T0, coarsest=coarsest, tol=1e-9, max_cycles=maxc)
+        dt = time.perf_counter() - t0
+        out[f"mg_solve_{name}_ml"] = {"seconds": dt, "cycles": rep["cycles"], "status": rep["status"],
+                                      "seconds_per_cycle": dt / max(1, rep["cycles"]),
+                                      "note": "to g <= 1e-9" if maxc >= 500 else f"first {rep['cycles']} cycles only (setup cycles run in full)"}
+    Z = np.random.default_rng(1).standard_normal((16, 256, 256))  # 1/16 slab of 256^3 (mode-3 planes)
+    U = np.asfortranarray(np.random.default_rng(2).standard_normal((128, 256)))
+    t0 = time.perf_counter()
+    oracle.mode_product(Z, (256, 256, 16), 0, U)
+    dt = time.perf_counter() - t0
+    out["restriction_c3_dense_mode0"] = {"seconds_full_scaled": 16 * dt,
+                                         "GFLOPs": 2.0 * 128 * 256 * 256 * 16 / dt / 1e9,
+                                         "sample": "Z x_1 U, U 128 x 256, on a 256 x 256 x 16 slab, x16"}
+    return out
+
+
+def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P, peaks64):
     rows = {}
     reps = 20
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -405,8 +470,8 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
         t = timed(lambda: cp.mode_product(Z3, (256, 256, 256), n, U3, X=X3), n=10)
         tf = 2.0 * 128 * 256**3 / t / 1e9
         rows[f"restriction_c3_dense_mode{n}"] = {"ms": t, "TFLOPs": tf,
-                                                 "frac_dmma_peak": tf / DMMA_PEAK_TF,
-                                                 "peak_note": "DMMA peak 37.0 TFLOP/s measured by tools/microbench.cu"}
+                                                 "frac_dmma_peak": tf / peaks64["dmma_tflops"],
+                                                 "peak_note": "DMMA peak measured in this run (libcppeaks.so)"}
         del X3
     del Z3
     # NEXT-3: the same restriction with the structured BAMG operator (cp_restrict_structured:
@@ -477,24 +542,67 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P):
             alg = 8.0 * (P4 + sum(d4[k] * R4 for k in range(4) if k != n) + d4[n] * R4)
             rows[f"c4b_mttkrp_mode{n}"] = {"ms": t, "alg_GBps": alg / t / 1e6}
         del Z4, A4, ws4, M4
-    # 8(d): full multigrid solve time to a stated g tolerance -- BASELINE.json config c1
-    # (50^3, R = 3, C = 0.9: BAMG setup + FAS V-cycles to ||grad f|| <= 1e-9), ML and ML+FMG,
-    # beside the plain ALS solve to the same tolerance; seconds include the stopping tests
-    # (cp_mg_solve reports the fit time separately: the paper excludes it)
+    # 8(d): full multigrid solve time to a stated g tolerance on BASELINE.json configs c0 (2-level
+    # cycle: coarsest 10), c1 (BAMG setup + FAS V-cycles to g <= 1e-9, coarsest 2R) and c2 (3 levels:
+    # coarsest 25): ML, ML+FMG (the paper's P:492 combination) and ML+FMG with reading R29's
+    # guard, beside the plain ALS solve to the same tolerance.  seconds include the stopping tests,
+    # seconds_excl_stop excludes them (the paper excludes them).  A run that does not reach
+    # the tolerance is reported as unsuccessful, as the paper counts them.
     try:
         import importlib.util
         spec = importlib.util.spec_from_file_location("mg_bench", os.path.join(ROOT, "tools", "mg_bench.py"))
         mgb = importlib.util.module_from_spec(spec)
         spec.loader.exec_module(mgb)
-        mgb.run("c1", tol=1e-9)  # warm-up
-        rows["mg_solve_c1"] = mgb.run("c1", tol=1e-9)
-        # and the paper's own dense problem (Table 4 context: s = 50, R = 2)
+        for name, coarsest, mc in (("c0", 10, 500), ("c1", 0, 500), ("c2", 25, 200)):
+            mgb.run(name, tol=1e-9, coarsest=coarsest, max_cycles=min(mc, 20), als=False)  # warm-up
+            rows[f"mg_solve_{name}"] = mgb.run(name, tol=1e-9, coarsest=coarsest, max_cycles=mc)
+        # the paper's own dense problem (Table 4 context: s = 50, R = 2)
         rows["mg_solve_dense50_R2"] = mgb.run("dense50", R=2, tol=1e-9)
         # s = 100, R = 3 (Table 4 context: ML+FMG 9 cycles): the case where the multigrid beats ALS
-        mgb.run("dense100", R=3, tol=1e-10)  # warm-up (plans, graphs)
+        mgb.run("dense100", R=3, tol=1e-10, max_cycles=20, als=False)  # warm-up (plans, graphs)
         rows["mg_solve_dense100_R3"] = mgb.run("dense100", R=3, tol=1e-10)
     except Exception as e:  # the row is informative; the sweep metric stands without it
-        rows["mg_solve_c1"] = {"error": repr(e)}
+        rows["mg_solve_error"] = {"error": repr(e)}
+    # 8(d): c0-c2 are L2-resident and latency/launch-bound: microseconds per sweep (K sweeps captured
+    # in one CUDA graph and replayed, device time by events) and the launch-floor fraction
+    # (launches per sweep x the empty-kernel launch time of this run / the sweep time)
+    floor = launch_floor_us()
+    for name in ("c0", "c1", "c2"):
+        dc = cpsynth.make_config(name, with_transfer=False)
+        dd, Rc = dc["dims"], dc["R"]
+        Zc = torch.from_numpy(dc["Z"]).to(dev)
+        Ac = [colmajor(torch.from_numpy(np.ascontiguousarray(a)).to(dev)) for a in dc["A0"]]
+        wsc = cp.Workspace(dd, Rc)
+        nzc = cp.norm2(Zc, dd, ws=wsc)
+        outc = torch.empty(4, dtype=torch.float64, device=dev)
+        cp.als_sweep(Zc, dd, Ac, nzc, out=outc, ws=wsc)
+        nl = cp.last_launch_count()
+        K = 50
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                cp.als_sweep(Zc, dd, Ac, nzc, out=outc, ws=wsc, stream=side)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(K):
+                cp.als_sweep(Zc, dd, Ac, nzc, out=outc, ws=wsc)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(4):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = 1e3 * e0.elapsed_time(e1) / (4 * K)
+        rows[f"{name}_sweep_latency"] = {
+            "us_per_sweep": us, "sweeps_per_s": 1e6 / us, "launches_per_sweep": nl,
+            "launch_floor_us": floor, "launch_floor_frac": (nl * floor / us) if floor else None,
+            "path": "fused single-CTA kernel (small_sweep.cu)" if nl == 1 else "general dimension-tree sweep",
+            "timing": f"{K} sweeps in one CUDA graph, 4 replays, L2-resident (no flush)"}
+        del g, Zc, Ac, wsc
     # the same sweep with the DFMA streaming consumers (CP_STREAM_MMA=0: FP64 tensor cores only in
     # the mode products, as BASELINE.json's north star first proposed)
     os.environ["CP_STREAM_MMA"] = "0"
@@ -518,6 +626,7 @@ def time_e2e(cp, torch, d, Zh, Zd, A0, A, nz, ws, dev, stream, dims, R, P, K):
     the initial factors from pinned host memory, computes ||Z||^2, runs the sweep and reads f."""
     Ah = [torch.from_numpy(np.ascontiguousarray(a.T)).pin_memory() for a in d["A0"]]
     outh = torch.empty(4, dtype=torch.float64).pin_memory()
+    Aout = [torch.empty_like(h).pin_memory() for h in Ah]
     out = torch.empty(4, dtype=torch.float64, device=dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 
@@ -528,6 +637,8 @@ def time_e2e(cp, torch, d, Zh, Zd, A0, A, nz, ws, dev, stream, dims, R, P, K):
         cp.norm2(Zd, dims, out=nz, ws=ws)
         cp.als_sweep(Zd, dims, A, nz, out=out, ws=ws)
         outh.copy_(out, non_blocking=True)
+        for a, h in zip(A, Aout):
+            h.copy_(a.t(), non_blocking=True)
 
     step()
     torch.cuda.synchronize()
@@ -538,8 +649,10 @@ def time_e2e(cp, torch, d, Zh, Zd, A0, A, nz, ws, dev, stream, dims, R, P, K):
     torch.cuda.synchronize()
     ms = ev[0].elapsed_time(ev[1])
     return {"value": K / (ms / 1000.0), "unit": "sweeps/s", "steps": K,
-            "h2d_bytes_per_step": 8 * P + sum(8 * I * R for I in dims), "d2h_bytes_per_step": 32,
-            "note": "per step: H2D of Z and the factors from pinned memory, cp_norm2, cp_als_sweep, D2H of f"}
+            "h2d_bytes_per_step": 8 * P + sum(8 * I * R for I in dims),
+            "d2h_bytes_per_step": 32 + sum(8 * I * R for I in dims),
+            "note": "per step: H2D of Z and the factors from pinned memory, cp_norm2, cp_als_sweep, D2H of "
+                    "[f, f~, status, mode] and of the updated factors (the sweep's result)"}
 
 
 if __name__ == "__main__":

@@ -17,6 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 OBJDIR = os.path.join(HERE, "lib", "obj")
 LIB = os.path.join(LIBDIR, "libcp.so")
+PEAKS_LIB = os.path.join(LIBDIR, "libcppeaks.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
@@ -59,6 +60,13 @@ def build(verbose=False, force=False):
     objs = [os.path.join(OBJDIR, os.path.basename(s)[:-3] + ".o") for s in sources]
     if force or jobs or _newer(objs, LIB):
         cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    # the fp64 peak microbenchmarks (include/cp_peaks.h): a separate measurement library
+    psrc = os.path.join(HERE, "peaks", "fp64_peaks.cu")
+    if force or _newer([psrc, os.path.join(os.path.dirname(HERE), "include", "cp_peaks.h")], PEAKS_LIB):
+        cmd = [NVCC] + ARCH + FLAGS + ["-shared", "-o", PEAKS_LIB, psrc, "-lcudart_static"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)

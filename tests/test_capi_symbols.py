@@ -110,3 +110,20 @@ def test_product_path_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "cp_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_peaks_library_exports_header_symbols():
+    """libcppeaks.so (bench.py's fp64 peak microbenchmarks, include/cp_peaks.h) loads and exports
+    what its header declares; a bad argument is rejected before any CUDA call."""
+    import paper_1111_6091_b200 as cp
+    src = open(os.path.join(ROOT, "include", "cp_peaks.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    syms = sorted(set(re.findall(r"\b(cpp_[a-z0-9_]+)\s*\(", src)))
+    assert syms == ["cpp_fp64_peaks", "cpp_launch_floor_us"]
+    P = ctypes.CDLL(os.path.join(os.path.dirname(cp.lib_path()), "libcppeaks.so"))
+    for name in syms:
+        assert hasattr(P, name)
+    a, b = ctypes.c_double(), ctypes.c_double()
+    assert P.cpp_fp64_peaks(ctypes.byref(a), ctypes.byref(b), 0) == -1
+    assert P.cpp_fp64_peaks(None, ctypes.byref(b), 1) == -1
+    assert P.cpp_launch_floor_us(0, ctypes.byref(a)) == -1

@@ -165,7 +165,6 @@ def sweep_path(request, monkeypatch):
     """cp_als_sweep runs tensors with P <= 16384 through the fused shared-memory kernel
     (small_sweep.cu); CP_SMALL_SWEEP=0 forces the general multi-kernel path."""
     monkeypatch.setenv("CP_SMALL_SWEEP", "1" if request.param == "fused_small" else "0")
-    monkeypatch.setenv("CP_MEDIUM_SWEEP", "1" if request.param == "fused_small" else "0")  # (opt-in kernel)
     return request.param
 
 
@@ -185,8 +184,9 @@ def test_sweep_single_step_mma_shapes(dims, R):
         _check_sweep(Ag, og, Ao, oo, nz2)
 
 
-@pytest.mark.parametrize("name,nsweeps", [("c0", 20), ("c1", 20), ("c2", 20), ("c3", 4)])
+@pytest.mark.parametrize("name,nsweeps", [("c0", 20), ("c1", 20), ("c2", 20), ("c3", 20)])
 def test_sweep_trajectory_configs(name, nsweeps):
+    """SURVEY 8(c) trajectory protocol: both sides from A0, compared after every sweep (1e-10)."""
     d = config(name)
     dims, Z = d["dims"], d["Z"]
     nz2 = float(np.vdot(Z, Z))
@@ -195,11 +195,13 @@ def test_sweep_trajectory_configs(name, nsweeps):
 
 
 @pytest.mark.parametrize("name", ["c4a", "c4b"])
-def test_sweep_full_size_one_step(name):
+def test_sweep_full_size_trajectory(name):
+    """3 sweeps at the full sizes (the bench launch configuration), every factor and
+    f compared with the oracle after every sweep."""
     d = config(name)
     dims, Z = d["dims"], d["Z"]
     nz2 = float(np.vdot(Z, Z))
-    for k, Ag, og, Ao, oo in _sweep_pair(Z, dims, d["A0"], nsweeps=1, nz2=nz2):
+    for k, Ag, og, Ao, oo in _sweep_pair(Z, dims, d["A0"], nsweeps=3, nz2=nz2):
         _check_sweep(Ag, og, Ao, oo, nz2)
 
 
@@ -417,15 +419,21 @@ def test_fit_ragged(dims, R):
             assert abs(out[2 + n] - oo[2 + n]) <= 1e-10 * oo[2 + n] + 1e-24
 
 
-@pytest.mark.parametrize("name", ["c0", "c1", "c2"])
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c3", "c4a", "c4b"])
 def test_fit_configs(name):
+    """cp_fit (a8): the direct f of the residual pass against oracle_f_direct (the plain definition
+    1/2 ||Z - [[A]]||^2, eq:CPfunctional) and g against oracle_gradient, on every config -- the
+    full sizes included (bench launch configuration)."""
     d = config(name)
     dims, Z, A = d["dims"], d["Z"], d["A0"]
     Zd, Ad = dev_problem(Z, A)
     out = host_tensor(cp.fit(Zd, dims, Ad, cp.norm2(Zd, dims))[0])
+    del Zd
     oo, _ = oracle.gradient(Z, dims, A, want_G=False)
     assert abs(out[0] - oo[0]) <= 1e-12 * abs(oo[0])
     assert abs(out[1] - oo[1]) <= 1e-10 * abs(oo[1]) + 1e-13
+    for n in range(len(dims)):
+        assert abs(out[2 + n] - oo[2 + n]) <= 1e-10 * oo[2 + n]
 
 
 @pytest.mark.parametrize("dims,R", [((5, 7, 3), 3), ((20, 20, 20), 3), ((2, 3, 2, 3), 2), ((700, 5, 4), 16),
@@ -477,8 +485,8 @@ def test_gradient_configs(name):
 
 @pytest.mark.parametrize("name", ["c4a", "c4b"])
 def test_gradient_full_size_matches_fit(name):
-    """At the full sizes (oracle too slow for all N modes): g, ||G^(n)||^2 bitwise cp_fit's, whose
-    parity is tested above; f (expansion) within cancellation of cp_fit's direct f."""
+    """At the full sizes: g, ||G^(n)||^2 bitwise cp_fit's (whose parity against the oracle is
+    test_fit_configs); f (expansion) within cancellation of cp_fit's direct f."""
     d = config(name)
     dims, Z, A = d["dims"], d["Z"], d["A0"]
     Zd, Ad = dev_problem(Z, A)

@@ -164,3 +164,23 @@ def test_fmg_combination_paper_default_and_guard():
     np.testing.assert_array_equal(tg[ns + 1:, 2], t0[ns:, 2])
     for r in (r0, rp, rg):
         assert r["status"] == 0 and r["g"] < 1e-9
+
+
+def test_mg_trace_sensitivity_c0():
+    """The multigrid g trace is ill-conditioned in its setup phase: relaxing U(0,1) test blocks
+     from their transient regime and fitting P to them amplifies a 1e-15 relative
+    perturbation of Z to a ~1e-3..1e-1 change of the cycle-1 g (BASELINE.json c0, 2-level cycle),
+    while the run still converges to the same minimizer in the same number of cycles.  This is
+    why GPU-vs-oracle trace parity is judged against the oracle's own envelope
+    (tests/test_gpu_mg.py), not at 1e-8."""
+    d = cpsynth.make_config("c0", with_transfer=False)
+    dims, R, Z, A0 = d["dims"], d["R"], d["Z"], d["A0"]
+    T0 = [cpsynth.uniform_init(dims, R, seed=10 + t) for t in range(2)]
+    kw = dict(coarsest=10, tol=1e-9, max_cycles=40)
+    A1, r1, t1 = mg.mg_solve(Z, dims, A0, T0, **kw)
+    Zp = Z * (1.0 + 1e-15 * np.random.default_rng(1).standard_normal(Z.shape))
+    A2, r2, t2 = mg.mg_solve(Zp, dims, A0, T0, **kw)
+    assert abs(t1[0, 2] - t2[0, 2]) / t1[0, 2] > 1e-4
+    assert r1["status"] == r2["status"] == 0 and r1["cycles"] == r2["cycles"]
+    for a, b in zip(A1, A2):
+        assert np.linalg.norm(a - b) <= 1e-6 * np.linalg.norm(b)
