@@ -103,19 +103,29 @@ class MGOracle:
         self.lv = [Level(d, R, k + 1 < len(sizes), c) for k, d in enumerate(sizes)]
         self.lv[0].Z = np.ascontiguousarray(Z, dtype=np.float64)
         self.lv[0].nz2 = float(np.vdot(Z, Z))
+        self.fail = None  # failing mode of the first relaxation that hit a non-positive pivot
+
+    def _note(self, out):
+        """A relaxation reported CP_ENOTSPD (out[2] = -3): remember its mode.  The solve stops at
+        the next stopping test with status -3 (Gamma singular: the Keller condition of P:362
+        fails; the factors are then unspecified), as cp_mg_solve does."""
+        if out[2] != 0 and self.fail is None:
+            self.fail = int(out[3])
 
     # ---- building blocks
     def relax_setup(self, l, A, sweeps):
         v = self.lv[l]
         for _ in range(sweeps):
-            A, _ = oracle.als_sweep(v.Z, v.dims, A, normZ2=v.nz2)
+            A, out = oracle.als_sweep(v.Z, v.dims, A, normZ2=v.nz2)
+            self._note(out)
             A, _ = oracle.normalize_sort(v.dims, A, sort=False)
         return A
 
     def relax_fas(self, l, A, F, sweeps):
         v = self.lv[l]
         for _ in range(sweeps):
-            A, _ = oracle.als_sweep(v.Z, v.dims, A, F=F, normZ2=v.nz2)
+            A, out = oracle.als_sweep(v.Z, v.dims, A, F=F, normZ2=v.nz2)
+            self._note(out)
             if l == 0:
                 A, _ = oracle.normalize_sort(v.dims, A, sort=True)
         return A
@@ -203,6 +213,10 @@ class MGOracle:
             self.lv[l - 1].A = self.interp(l - 1, self.lv[l].A)
             self.fas_cycle(l - 1, None)
 
+    def stop_g(self):
+        """g at the finest level for a stopping test; NaN once a relaxation has failed."""
+        return float("nan") if self.fail is not None else self.fit(0, self.lv[0].A)[0][1]
+
     # ---- combination (P:486-492)
     def solve(self, A0, T0, A_fmg=None):
         p = self.p
@@ -218,7 +232,7 @@ class MGOracle:
             if converged:
                 break
             self.setup_cycle(0, cyc == 1, True)
-            gn = self.fit(0, f.A)[0][1]
+            gn = self.stop_g()
             cycles += 1
             setup_cycles += 1
             trace.append((0, cycles, gn))
@@ -229,7 +243,7 @@ class MGOracle:
             if cyc >= p["min_setup_cycles"] and gn > (1.0 - p["stagnation_eps"]) * g_old:
                 break
             g_old = gn
-        if not converged and p["use_fmg"]:
+        if not converged and p["use_fmg"] and self.fail is None:
             # "Multilevel + FMG": one FMG-CP-FAS cycle computes a new approximation to the
             # boot factors, then the transfer operators are rebuilt by one down-sweep of
             # CP-AMG-mult (boot factors not updated).  fmg_guard = 1 is reading R29 (not the
@@ -237,7 +251,7 @@ class MGOracle:
             # iterate is restored and the operators are not rebuilt.
             kept = [a.copy(order="F") for a in f.A]
             self.fmg(A_fmg)
-            gf = self.fit(0, f.A)[0][1]
+            gf = self.stop_g()
             cycles += 1
             trace.append((1, cycles, gf))
             if p["fmg_guard"] and not gf < g:
@@ -245,14 +259,14 @@ class MGOracle:
             else:
                 g = gf
                 converged = g < p["tol"]
-                if not converged:
+                if not converged and self.fail is None:
                     self.setup_cycle(0, False, False)
         rebuilt = False
         g_old = g
-        while not converged and cycles < p["max_cycles"]:
+        while not converged and cycles < p["max_cycles"] and self.fail is None:
             prev = [a.copy(order="F") for a in f.A]
             self.fas_cycle(0, None)
-            gn = self.fit(0, f.A)[0][1]
+            gn = self.stop_g()
             cycles += 1
             solve_cycles += 1
             trace.append((2, cycles, gn))
@@ -271,8 +285,10 @@ class MGOracle:
             g = gn
             g_old = gn
         out = self.fit(0, f.A)[0]
+        status = -3 if self.fail is not None else (0 if converged else 1)
         report = dict(g=g, f=out[0], cycles=cycles, setup_cycles=setup_cycles, solve_cycles=solve_cycles,
-                      levels=len(self.lv), status=0 if converged else 1, rebuilds=rebuilds)
+                      levels=len(self.lv), status=status, rebuilds=rebuilds,
+                      failed_mode=self.fail if self.fail is not None else -1)
         return f.A, report, np.array(trace)
 
 

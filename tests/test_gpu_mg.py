@@ -260,3 +260,15 @@ def test_mg_c2_three_level_unsuccessful_like_the_oracle():
     for k in range(len(tr)):
         assert abs(tr[k, 2] - tro[k, 2]) <= 0.2 * tro[k, 2], (k, tr[k, 2], tro[k, 2])
     assert 1e-4 < rep["g"] < 1e-2 and 1e-4 < repo["g"] < 1e-2
+    # Multilevel + FMG: the FMG cycle's CP-FAS relaxation on the coarsest level (25^3)
+    # drives a factor column to zero and hits a non-positive pivot -- on both sides, reported as
+    # CP_ENOTSPD (status -3) at the FMG cycle (cycle 6, after the 5 setup cycles)
+    Af = cpsynth.uniform_init(mg.levels(dims, R, 25)[-1], R, seed=99)
+    kwf = dict(kw, use_fmg=1, max_cycles=8)
+    _, repo, tro = mg.mg_solve(Z, dims, A0, T0, A_fmg=Af, **kwf)
+    Ad = [dev_factor(a) for a in A0]
+    rep, tr = cp.mg_solve(dev_tensor(Z), dims, Ad, [[dev_factor(t) for t in b] for b in T0],
+                          A_fmg=[dev_factor(a) for a in Af], params=cp.MGParams.default(**kwf))
+    assert int(rep["status"]) == repo["status"] == cp.CP_ENOTSPD
+    assert int(rep["cycles"]) == repo["cycles"] == 6
+    assert int(rep["failed_mode"]) == repo["failed_mode"]

@@ -184,3 +184,18 @@ def test_mg_trace_sensitivity_c0():
     assert r1["status"] == r2["status"] == 0 and r1["cycles"] == r2["cycles"]
     for a, b in zip(A1, A2):
         assert np.linalg.norm(a - b) <= 1e-6 * np.linalg.norm(b)
+
+
+def test_mg_stops_on_singular_gamma():
+    """A zero boot-factor column: the finest-level ALS relaxation of the first setup cycle hits a
+    non-positive Cholesky pivot (Gamma singular, the Keller condition of P:362 fails).  The oracle,
+    like cp_mg_solve, stops at that cycle's stopping test with status -3 (CP_ENOTSPD) and the
+    failing mode, instead of iterating on unspecified factors."""
+    d = cpsynth.make_config("c0", with_transfer=False)
+    dims, R, Z = d["dims"], d["R"], d["Z"]
+    A0 = [a.copy(order="F") for a in d["A0"]]
+    A0[2][:, 0] = 0.0
+    T0 = [cpsynth.uniform_init(dims, R, seed=10 + t) for t in range(2)]
+    _, rep, tr = mg.mg_solve(Z, dims, A0, T0, coarsest=10, max_cycles=20)
+    assert rep["status"] == -3 and rep["failed_mode"] == 0
+    assert rep["cycles"] == 1 and len(tr) == 1 and np.isnan(tr[0, 2])
