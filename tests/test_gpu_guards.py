@@ -1,0 +1,152 @@
+"""Memory-safety checks of the CUDA path without compute-sanitizer (closed on this pool): every
+entry point on small shapes of each code path, with
+  * guard bands (a NaN bit pattern) before and after every output buffer and after the
+    workspace -- any out-of-bounds store changes them;
+  * inputs (Z, F, transfer weights) compared bitwise before and after -- inputs are read-only;
+  * the workspace pre-filled with two different garbage patterns (0xFF.. and 0x00..) -- the
+    outputs must be bitwise equal, so no result depends on uninitialized workspace memory.
+(memcheck- and initcheck-style evidence; races are covered by the bitwise-determinism and
+chained-call tests of test_gpu_parity.py.)"""
+import numpy as np
+import pytest
+
+import cpsynth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1111_6091_b200 as cp  # noqa: E402
+
+GUARD = 4096  # doubles on each side
+NAN_BITS = 0x7FF8DEADBEEF0001
+
+
+class Guarded:
+    """A float64 buffer of n doubles between two guard bands."""
+
+    def __init__(self, n):
+        self.n = n
+        self.buf = torch.empty(2 * GUARD + n, dtype=torch.float64, device="cuda")
+        self.buf.view(torch.int64).fill_(NAN_BITS)
+
+    def view(self):
+        return self.buf[GUARD:GUARD + self.n]
+
+    def factor(self, rows, cols, src=None):
+        t = self.view().view(cols, rows).t()
+        if src is not None:
+            t.copy_(torch.from_numpy(np.ascontiguousarray(src)).cuda())
+        return t
+
+    def intact(self):
+        g = torch.cat([self.buf[:GUARD], self.buf[GUARD + self.n:]]).view(torch.int64)
+        return bool((g == NAN_BITS).all())
+
+
+def guarded_ws(dims, R, fill):
+    ws = cp.Workspace(dims, R)
+    n = ws.nbytes
+    big = torch.empty(n + 8 * GUARD, dtype=torch.uint8, device="cuda")
+    big.fill_(fill)
+    ws.buf = big[:n]
+    ws.tail = big[n:]
+    ws.fill = fill
+    return ws
+
+
+def ws_tail_intact(ws):
+    return bool((ws.tail == ws.fill).all())
+
+
+def run_all(dims, R, fill, small, use_F):
+    import os
+    os.environ["CP_SMALL_SWEEP"] = small
+    Z, A = cpsynth.random_problem(dims, R, seed=sum(dims) + R)
+    Zd = torch.from_numpy(Z).cuda()
+    Z0 = Zd.clone()
+    Fh = [0.05 * cpsynth.random_matrix(I, R, 3 + k) for k, I in enumerate(dims)] if use_F else None
+    Fd = None if Fh is None else [torch.from_numpy(np.ascontiguousarray(f.T)).cuda().t() for f in Fh]
+    F0 = None if Fd is None else [f.clone() for f in Fd]
+    ws = guarded_ws(dims, R, fill)
+    guards, res = [], []
+    gA = [Guarded(I * R) for I in dims]
+    Ad = [g.factor(I, R, a.T) for g, I, a in zip(gA, dims, A)]
+    guards += gA
+    gn = Guarded(1)
+    nz = gn.view()
+    cp.norm2(Zd, dims, out=nz, ws=ws)
+    guards.append(gn)
+    for n in range(len(dims)):
+        gM = Guarded(dims[n] * R)
+        cp.mttkrp(Zd, dims, Ad, n, M=gM.factor(dims[n], R), ws=ws)
+        guards.append(gM)
+        res.append(gM.view())
+    for nsw, norm in ((1, False), (3, False), (2, True)):
+        go = Guarded(4)
+        cp.als_sweep(Zd, dims, Ad, nz, F=None if norm else Fd, out=go.view(), ws=ws, nsweeps=nsw, normalize=norm)
+        guards.append(go)
+        res.append(go.view().clone())
+        res += [a.clone() for a in Ad]
+    for fn in (cp.fit, cp.gradient):
+        go = Guarded(2 + len(dims))
+        out, G = fn(Zd, dims, Ad, nz, F=Fd, want_G=True, out=go.view(), ws=ws)
+        guards.append(go)
+        res.append(go.view().clone())
+        res += [g.clone() for g in G]
+    torch.cuda.synchronize()
+    ok_inputs = torch.equal(Zd, Z0) and (F0 is None or all(torch.equal(a, b) for a, b in zip(Fd, F0)))
+    return [r.cpu() for r in res], all(g.intact() for g in guards), ws_tail_intact(ws), ok_inputs
+
+
+SHAPES = [((20, 20, 20), 3, "1", True),     # fused small-sweep kernel
+          ((20, 20, 20), 3, "0", True),     # general path, tensor-map stage loads
+          ((50, 48, 46), 8, "1", True),     # general path (P > 16384), MMA consumers
+          ((9, 8, 7, 6), 5, "0", False),    # 4-way: Y_R path
+          ((7, 5, 6), 3, "0", True),        # odd I1: scalar producer
+          ((130, 9, 6), 20, "0", False),    # NT = 3, ragged m-tiles
+          ((1030, 3, 2), 7, "0", False)]    # I1 > 512: row blocks
+
+
+@pytest.mark.parametrize("dims,R,small,use_F", SHAPES)
+def test_guard_bands_inputs_and_uninitialized_workspace(dims, R, small, use_F, monkeypatch):
+    monkeypatch.setenv("CP_SMALL_SWEEP", small)
+    r1, g1, w1, i1 = run_all(dims, R, 0xFF, small, use_F)
+    r2, g2, w2, i2 = run_all(dims, R, 0x00, small, use_F)
+    assert g1 and g2, "an output guard band was overwritten"
+    assert w1 and w2, "a store past the workspace end"
+    assert i1 and i2, "an input was modified"
+    for a, b in zip(r1, r2):
+        assert torch.equal(a, b) or (torch.isnan(a).all() and torch.isnan(b).all()), \
+            "a result depends on uninitialized workspace memory"
+
+
+@pytest.mark.parametrize("dims", [(20, 18, 16), (33, 7, 5), (96, 10, 12)])
+def test_guard_bands_mode_products(dims):
+    Z, _ = cpsynth.random_problem(dims, 1, seed=sum(dims))
+    Zd = torch.from_numpy(Z).cuda()
+    Z0 = Zd.clone()
+    for n in range(len(dims)):
+        I, Ic = dims[n], (dims[n] + 1) // 2
+        nd = list(dims)
+        nd[n] = Ic
+        P = int(np.prod(nd))
+        wl, wr = cpsynth.transfer_weights(I, seed=n + 1)
+        wld, wrd = torch.from_numpy(wl).cuda(), torch.from_numpy(wr).cuda()
+        outs = []
+        for fill in (0xFF, 0x00):
+            gx = Guarded(P)
+            X = gx.view().view(tuple(reversed(nd)))
+            rws = torch.empty(1 << 16, dtype=torch.uint8, device="cuda").fill_(fill)
+            cp.restrict_structured(Zd, dims, n, wld, wrd, X=X, ws=rws)
+            gy = Guarded(P)
+            Y = gy.view().view(tuple(reversed(nd)))
+            U = cpsynth.random_matrix(Ic, I, 9 + n)
+            cp.mode_product(Zd, dims, n, torch.from_numpy(np.ascontiguousarray(U.T)).cuda().t(), X=Y)
+            torch.cuda.synchronize()
+            assert gx.intact() and gy.intact()
+            outs.append((X.clone(), Y.clone()))
+        assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    assert torch.equal(Zd, Z0)
