@@ -711,7 +711,7 @@ static bool use_small_sweep(const cp_shape &s) {
 
 static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
                       const double *const *F, double *out, void *ws, size_t ws_bytes, cp_stream_t stream,
-                      bool first);
+                      bool first, bool steady);
 
 int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
                  const double *const *F, double *out, void *ws, size_t ws_bytes,
@@ -742,7 +742,9 @@ int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, doub
   }
   int total = 0;
   for (int k = 0; k < nsweeps; ++k) {
-    if ((st = sweep_impl(s, Z, normZ2, A, F, out, ws, ws_bytes, stream, k == 0))) return st;
+    // sweeps k >= 1 without normalization in between run steady-state: the previous sweep's
+    // solves left every At copy and Gram total current, so no prep launch
+    if ((st = sweep_impl(s, Z, normZ2, A, F, out, ws, ws_bytes, stream, k == 0, k > 0 && !norm))) return st;
     total += g_launches;
     if (norm) {  // cp_normalize_sort(sort = 0) with the sweep workspace's own scratch region
       NormArgs na;
@@ -767,10 +769,14 @@ int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, doub
 
 // One sweep of the general path.  first = false: a later sweep of the same cp_als_sweeps call --
 // the status word is not reset, so a failure in an earlier sweep stays reported and every later
-// solve skips (the fused small kernel likewise stops at the first failure).
+// solve skips (the fused small kernel likewise stops at the first failure).  steady: the factors
+// are unchanged since the previous sweep of this call (no normalization in between), whose solves
+// wrote the row-major copies At and the Gram totals Ups of every mode -- the prep launch (At
+// copies + partial Grams) is skipped and every Gram of a not-yet-updated factor is read as a total
+// (bitwise the same as the previous sweep's totals; the tickets were reset by their last users).
 static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
                       const double *const *F, double *out, void *ws, size_t ws_bytes, cp_stream_t stream,
-                      bool first) {
+                      bool first, bool steady) {
   g_launches = 0;
   int st;
   Layout L;
@@ -791,8 +797,13 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
   // experiments only (-DCP_EXPERIMENTS builds): CP_SWEEP_SKIP bitmask drops launches (timing of
   // the rest; results wrong).  Always 0 in the shipped library.
   const int skip = knob("CP_SWEEP_SKIP", 0);
-  if (!(skip & 1) && launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
-  int launches = 1;
+  int launches = 0;
+  if (steady) {
+    pg.tot = w + L.Ups;
+  } else {
+    if (!(skip & 1) && launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
+    launches = 1;
+  }
   double *gp[2] = {w + L.gpart0, w + L.gpart1};
   int grid_of[CP_MAX_N] = {0};
   // a4 for mode n from M given by rg (stream partials or a plain M buffer)
@@ -858,7 +869,10 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
     g.mode = n;
     for (int k = 0; k < N; ++k) {
       if (k == n) continue;
-      if (k > n) {
+      if (k > n && steady) {
+        g.src[k] = w + L.Ups + (size_t)k * RR;
+        g.cnt[k] = 0;
+      } else if (k > n) {
         g.src[k] = w + L.gpre + (size_t)pg.blk_off[k] * RR;
         g.cnt[k] = pg.nblk[k];
       } else if (k == n - 1) {
@@ -924,6 +938,7 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
         ya.In = s->dims[n];
         ya.RS = RS;
         ya.Bfac = (n == 0) ? w + L.At[1] : A[0];
+        ya.vec1 = (n == 1 && (s->dims[0] % 4) == 0 && aligned(A[0], 32)) ? 1 : 0;
         ya.gin = gp[0];
         ya.nin = grid_of[0];
         ya.linv = (n == 0 && job0) ? w + L.linv : nullptr;
@@ -931,7 +946,7 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
         // Upsilon^(k >= 2) as totals (written by job 0 or by the mode-0 kernel)
         ya.total = nullptr;
         ya.ticket = reinterpret_cast<unsigned *>(w + L.status + kTicketSlot2);
-        ya.ups_total = (n == 0) ? 0 : (((1 << N) - 1) & ~2);
+        ya.ups_total = (n == 0) ? (steady ? (((1 << N) - 1) & ~1) : 0) : (((1 << N) - 1) & ~2);
         ya.F = (F != nullptr) ? F[n] : nullptr;
         ya.A = A[n];
         ya.At = w + L.At[n];

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
 
 // Upsilon^(k) entry e from the prep partials of mode k (fixed chunk order)
 __device__ __forceinline__ double prep_gram(const PrepGrams &pg, int k, int e, int RR) {
+  if (pg.tot != nullptr) return pg.tot[(int64_t)k * RR + e];
   return sum_strided(pg.gpre + (int64_t)pg.blk_off[k] * RR + e, RR, pg.nblk[k]);
 }
 

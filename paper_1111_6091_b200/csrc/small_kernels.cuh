@@ -103,6 +103,9 @@ struct PrepGrams {
   const double *gpre;
   int blk_off[CP_MAX_N + 1];
   int nblk[CP_MAX_N];
+  const double *tot;  // non-null: the Gram TOTALS (N x R x R) of the current factors instead of the
+                      // prep partials -- a steady-state sweep (cp_als_sweeps, sweep k >= 1: the
+                      // previous sweep left At and every Upsilon total current; no prep launch)
 };
 
 struct FinalizeArgs {
@@ -229,6 +232,8 @@ struct YLSolveArgs {
   double *gcur;            // per-cluster partial Grams of the new rows
   double *dotF;            // per-cluster <F, A>
   double *status;
+  int vec1;                // mode 1: Y_L rows and A^(0)_new columns read as 32-byte vectors (I0 % 4 == 0,
+                           // 32-B aligned A^(0)_new)
 };
 int ylsolve_clusters(int64_t In);  // grid = 8 x this
 cudaError_t launch_ylsolve(const YLSolveArgs &a, cudaStream_t st);

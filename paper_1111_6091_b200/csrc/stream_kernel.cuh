@@ -19,7 +19,7 @@
 //    (warp shuffles + shared memory), writing one R-vector partial per (CTA, segment).
 #pragma once
 #include "cp_internal.cuh"
-#ifdef CP_STREAM_TIMING
+#if defined(CP_STREAM_TIMING) || defined(CP_CTA_TIMELINE)
 #include <cstdio>
 #endif
 

@@ -126,9 +126,23 @@ __device__ __forceinline__ void yl_complete_segment(const StreamPlan &p, int64_t
   (void)scratch;
 }
 
+#ifdef CP_CTA_TIMELINE
+__device__ __forceinline__ unsigned long long cta_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 template <int NT, int MT, int OP>
 __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __grid_constant__ StreamPlan p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+#ifdef CP_CTA_TIMELINE
+  // timing build only (tools/cta_timeline.py): per-CTA entry, first stage landed, loop end, exit
+  unsigned long long tl_enter = cta_gtimer(), tl_first = 0, tl_loop = 0;
+  unsigned tl_smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(tl_smid));
+#endif
   StreamSmem sm;
   {
     // carve (as carve<R, OP> in stream_kernel.cuh)
@@ -217,6 +231,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   uint32_t fph = 0;
   for (;;) {
     mbar_wait(p.direct_w ? &sm.full[stage] : &sm.wready[stage], fph);
+#ifdef CP_CTA_TIMELINE
+    if (tl_first == 0) tl_first = cta_gtimer();
+#endif
     const int *h = sm.hdr + stage * kHdrInts;
     const int ncols = h[0];
     const int flags = h[1];
@@ -417,6 +434,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     }
     if (flags & 2) break;
   }
+#ifdef CP_CTA_TIMELINE
+  tl_loop = cta_gtimer();
+#endif
 
   if (OP == OP_RESID) {
     // ---- this CTA's sum of (z - x)^2: lanes, then warps in order ----
@@ -450,6 +470,11 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
       }
     }
   }
+#ifdef CP_CTA_TIMELINE
+  if (tid == 0)
+    printf("CTL %d %d %d %u %llu %llu %llu %llu\n", OP, p.mode, blockIdx.x, tl_smid, tl_enter, tl_first, tl_loop,
+           cta_gtimer());
+#endif
 }
 
 template <int NT, int MT, int OP>

@@ -90,7 +90,8 @@ __device__ __forceinline__ void ys_gamma_warp(const YLSolveArgs &a, double *sL, 
         u = a.Ups[(int64_t)k * RR + e];
       } else {
         u = (a.mode == 1 && k == 0) ? ys_sum(a.gin + e, RR, a.nin)
-                                    : ys_sum(a.pg.gpre + (int64_t)a.pg.blk_off[k] * RR + e, RR, a.pg.nblk[k]);
+            : (a.pg.tot != nullptr ? a.pg.tot[(int64_t)k * RR + e]
+                                   : ys_sum(a.pg.gpre + (int64_t)a.pg.blk_off[k] * RR + e, RR, a.pg.nblk[k]));
         if (blockIdx.x == 0) a.Ups[(int64_t)k * RR + e] = u;
       }
       gm *= u;
@@ -233,12 +234,22 @@ __global__ void __launch_bounds__(256, 2) __cluster_dims__(kYsCluster, 1, 1) yls
 #pragma unroll
               for (int u = 0; u < 4; ++u) acc[u] = fma(y[j][u], b[j], acc[u]);
           }
-          for (; i1 < I1; i1 += nsl) {
-            double y[4];
-            ld_v4(yb + i1 * blk, y);
-            const double b = __ldg(bt + i1 * a.RS);
+          if (i1 < I1) {
+            // the remainder as ONE predicated batch (a serial loop here paid one memory round
+            // trip per i1: 5 of the 9 round trips of the c4a contraction)
+            double y[8][4], b[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc[u] = fma(y[u], b, acc[u]);
+            for (int j = 0; j < 8; ++j) {
+              const int64_t ij = i1 + j * nsl;
+              const int64_t ic = ij < I1 ? ij : (int64_t)sl;
+              ld_v4(yb + ic * blk, y[j]);
+              b[j] = __ldg(bt + ic * a.RS);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (i1 + j * nsl < I1)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc[u] = fma(y[j][u], b[j], acc[u]);
           }
         } else {
           for (int64_t i1 = sl; i1 < I1; i1 += nsl) {
@@ -258,6 +269,44 @@ __global__ void __launch_bounds__(256, 2) __cluster_dims__(kYsCluster, 1, 1) yls
         double m = 0.0;
         for (int sl = 0; sl < nsl; ++sl) m += sP[(sl * R + r) * kYsRows + u];
         sMv[u * R + r] = m;
+      }
+    } else if (warp < CW && a.vec1) {
+      // warp w owns the ranks r = w, w + CW, ...: for each, the column A^(0)_new(:, r) and the
+      // block's Y_L rows (i1 = r0 + u, r) in 32-byte vectors, 2 chunks of 4 x 32 lanes per
+      // round trip (A reused over the rows u); lane partials, then a fixed xor tree
+      const int64_t nch = I0 / 4;  // 32-B chunks per row
+      for (int r = warp; r < R; r += CW) {
+        const double *ab = a.Bfac + (int64_t)r * I0;
+        const double *yb = a.yl + (int64_t)r * I0 + r0 * blk;
+        double acc[kYsRows] = {0.0, 0.0, 0.0, 0.0};
+        for (int64_t c0 = lane; c0 < nch; c0 += 64) {
+          const int64_t c1 = c0 + 32;
+          const bool ok1 = c1 < nch;
+          double av[2][4], yv[2][kYsRows][4];
+          ld_v4(ab + 4 * c0, av[0]);
+          ld_v4(ab + 4 * (ok1 ? c1 : c0), av[1]);
+#pragma unroll
+          for (int u = 0; u < kYsRows; ++u) {
+            const int uc = u < nrows ? u : 0;
+            ld_v4(yb + uc * blk + 4 * c0, yv[0][u]);
+            ld_v4(yb + uc * blk + 4 * (ok1 ? c1 : c0), yv[1][u]);
+          }
+#pragma unroll
+          for (int u = 0; u < kYsRows; ++u) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[u] = fma(yv[0][u][q], av[0][q], acc[u]);
+            if (ok1)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) acc[u] = fma(yv[1][u][q], av[1][q], acc[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kYsRows; ++u) {
+          double t = acc[u];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+          if (lane == 0 && u < nrows) sMv[u * R + r] = t;
+        }
       }
     } else if (warp < CW) {
       // warp w owns the entries en = w + CW j (row u = en / R, rank r = en % R) and works on all

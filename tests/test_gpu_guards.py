@@ -73,7 +73,7 @@ def run_all(dims, R, fill, small, use_F):
     ws = guarded_ws(dims, R, fill)
     guards, res = [], []
     gA = [Guarded(I * R) for I in dims]
-    Ad = [g.factor(I, R, a.T) for g, I, a in zip(gA, dims, A)]
+    Ad = [g.factor(I, R, a) for g, I, a in zip(gA, dims, A)]
     guards += gA
     gn = Guarded(1)
     nz = gn.view()

@@ -274,6 +274,33 @@ def test_multi_sweep_call_general_path_vs_oracle(name):
     _check_sweep([host_factor(a) for a in Ad], out, Ao, oo, nz2)
 
 
+@pytest.mark.parametrize("dims,R,F", [((40, 36, 30), 20, True), ((30, 28, 26, 12), 6, True), ((33, 2), 5, False),
+                                      ((64, 9, 7, 5, 3), 4, True), ((130, 9, 6), 20, False)])
+def test_multi_sweep_steady_state_vs_oracle(dims, R, F, monkeypatch):
+    """cp_als_sweeps on the general path: sweeps k >= 1 of one call run steady-state (no prep
+    launch; the previous sweep's At copies and Gram totals) -- the tree sweep (N = 3, 4, 5: Y_R
+    path), the N = 2 mode-by-mode sweep and an MMA k-split shape; nu = 4 sweeps equal 4 oracle
+    sweeps, F included, and fewer launches than 4 separate calls."""
+    monkeypatch.setenv("CP_SMALL_SWEEP", "0")
+    Z, A = cpsynth.random_problem(dims, R, seed=900 + R)
+    if not _well_posed(dims, R):
+        pytest.skip("Gamma singular for every iterate")
+    nz2 = float(np.vdot(Z, Z))
+    Fh = [0.02 * cpsynth.random_matrix(I, R, 40 + k) for k, I in enumerate(dims)] if F else None
+    Zd, Ad = dev_problem(Z, A)
+    Fd = None if Fh is None else [dev_factor(f) for f in Fh]
+    nzd = cp.norm2(Zd, dims)
+    out = host_tensor(cp.als_sweep(Zd, dims, Ad, nzd, F=Fd, nsweeps=4))
+    n4 = cp.last_launch_count()
+    cp.als_sweep(Zd, dims, [a.clone() for a in Ad], nzd, F=Fd)
+    n1 = cp.last_launch_count()
+    assert n4 == 4 * n1 - 3  # the prep launch of sweeps 2..4 is gone
+    Ao = [a.copy(order="F") for a in A]
+    for _ in range(4):
+        Ao, oo = oracle.als_sweep(Z, dims, Ao, F=Fh, normZ2=nz2)
+    _check_sweep([host_factor(a) for a in Ad], out, Ao, oo, nz2)
+
+
 @pytest.mark.parametrize("dims,R", [((7, 7, 7), 3), ((13, 12, 11), 4), ((50, 50, 50), 3), ((9, 8, 7, 6), 2)])
 @pytest.mark.parametrize("small", ["1", "0"])
 def test_multi_sweep_normalized_vs_oracle(dims, R, small, monkeypatch):
