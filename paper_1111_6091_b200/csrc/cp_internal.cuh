@@ -2,6 +2,9 @@
 // Product code: nothing here is shared with, or derived from, oracle/.
 #pragma once
 #include <cstdint>
+#ifdef CP_CTA_TIMELINE
+#include <cstdio>
+#endif
 #include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -145,6 +148,25 @@ __device__ __forceinline__ void griddep() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+// Timing builds only (-DCP_CTA_TIMELINE, tools/sweep_timeline.py): every block's thread 0 prints
+// its entry time, the time its griddep() wait returned and its exit time (globaltimer, ns).
+#ifdef CP_CTA_TIMELINE
+__device__ __forceinline__ unsigned long long ctl_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTL_BEGIN const unsigned long long ctl_e = ctl_clock();
+#define CTL_AFTER_WAIT const unsigned long long ctl_w = ctl_clock();
+#define CTL_END(tag)                                                                                   \
+  if (threadIdx.x == 0)                                                                                \
+    printf("CTK %s %d %llu %llu %llu\n", tag, (int)blockIdx.x, ctl_e, ctl_w, ctl_clock());
+#else
+#define CTL_BEGIN
+#define CTL_AFTER_WAIT
+#define CTL_END(tag)
+#endif
+
 // PDL per launch class (env CP_PDL_MASK, bit c = class c; CP_PDL=0 clears all):
 //   kPdlStream: the Z-streaming kernels, kPdlCluster: ylsolve (8-CTA clusters), kPdlSmall: the rest
 enum { kPdlStream = 0, kPdlCluster = 1, kPdlSmall = 2 };

@@ -106,7 +106,9 @@ __global__ void __launch_bounds__(256) reduce_mode0_kernel(const double *part, i
 // One block per (mode k, chunk of kPrepRows rows): At^(k) rows (row-major copy, padded stride
 // RS) and the chunk's partial Gram A_chunk^T A_chunk, summed later in chunk order.
 __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
+  CTL_BEGIN
   griddep();
+  CTL_AFTER_WAIT
   // chunk x R, column-major (r * kPrepLd + ii); the odd column stride keeps the Gram loop's
   // 16 different r of a warp in 16 different banks (stride 64 put them all in one bank)
   constexpr int kPrepLd = kPrepRows + 1;
@@ -158,6 +160,7 @@ __global__ void __launch_bounds__(256) prep_kernel(const PrepArgs a) {
       a.gpre[(int64_t)blockIdx.x * RR + e] = (g0 + g1) + (g2 + g3);
     }
   }
+  CTL_END("prep")
 }
 
 // Upsilon^(k) entry e from the prep partials of mode k (fixed chunk order)
@@ -233,7 +236,9 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
   unsigned long long tstamp[10] = {0};
 #endif
   SOLVE_T(0);
+  CTL_BEGIN
   griddep();
+  CTL_AFTER_WAIT
   SOLVE_T(1);
   constexpr int RR = R * R;
   constexpr int LS = R + 1;  // smem row stride of the R x R matrices
@@ -408,6 +413,7 @@ __global__ void __launch_bounds__(256) solve_kernel_t(const SolveArgs a) {
     }
   }
   SOLVE_T(8);
+  CTL_END("solve")
 #ifdef CP_SOLVE_TIMING
   if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
     printf("solve mode %d blk %d: griddep %llu | pre %llu gather %llu gamma %llu chol %llu apply %llu gram/dot %llu tail %llu\n",

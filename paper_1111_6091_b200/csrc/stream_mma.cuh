@@ -177,7 +177,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     fence_mbar_init();
   }
   __syncthreads();
+  CTL_BEGIN
   griddep();  // (PDL) predecessor's At / factor writes visible from here on
+  CTL_AFTER_WAIT
 
   if (warp == kConsumerWarps) {
     produce<8, 2>(p, lane, v0, v1, row0, Wb, sm);  // (template args only select the TMA path)
@@ -475,6 +477,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     printf("CTL %d %d %d %u %llu %llu %llu %llu\n", OP, p.mode, blockIdx.x, tl_smid, tl_enter, tl_first, tl_loop,
            cta_gtimer());
 #endif
+  CTL_END(OP == OP_YL ? "streamYL" : (OP == OP_RESID ? "streamRES" : (p.mode == 0 ? "streamM0" : "streamMn")))
 }
 
 template <int NT, int MT, int OP>

@@ -162,7 +162,9 @@ __global__ void __launch_bounds__(256, 2) __cluster_dims__(kYsCluster, 1, 1) yls
   unsigned long long tst[10] = {0};
 #endif
   YS_T(0);
+  CTL_BEGIN
   griddep();
+  CTL_AFTER_WAIT
   constexpr int RR = R * R;
   constexpr int LS = R + 1;
   constexpr int NSL = 256 / R;        // mode 0: i1 slices (8 contraction warps)
@@ -438,6 +440,7 @@ __global__ void __launch_bounds__(256, 2) __cluster_dims__(kYsCluster, 1, 1) yls
     }
   }
   YS_T(5);
+  CTL_END(a.mode == 0 ? "ylsolve0" : "ylsolve1")
 #ifdef CP_SOLVE_TIMING
   if (threadIdx.x == 0)
     printf("YS %d %d %llu %llu %llu %llu %llu %llu %llu %llu\n", a.mode, blockIdx.x, tst[0], tst[1], tst[6], tst[7], tst[2], tst[3], tst[4], tst[5]);

@@ -107,7 +107,7 @@ SHAPES = [((20, 20, 20), 3, "1", True),     # fused small-sweep kernel
           ((9, 8, 7, 6), 5, "0", False),    # 4-way: Y_R path
           ((7, 5, 6), 3, "0", True),        # odd I1: scalar producer
           ((130, 9, 6), 20, "0", False),    # NT = 3, ragged m-tiles
-          ((1030, 3, 2), 7, "0", False)]    # I1 > 512: row blocks
+          ((1030, 3, 2), 7, "0", False)]    # I1 > 512: row blocks; R > P / I1: Gamma singular (ENOTSPD)
 
 
 @pytest.mark.parametrize("dims,R,small,use_F", SHAPES)
@@ -118,8 +118,8 @@ def test_guard_bands_inputs_and_uninitialized_workspace(dims, R, small, use_F, m
     assert g1 and g2, "an output guard band was overwritten"
     assert w1 and w2, "a store past the workspace end"
     assert i1 and i2, "an input was modified"
-    for a, b in zip(r1, r2):
-        assert torch.equal(a, b) or (torch.isnan(a).all() and torch.isnan(b).all()), \
+    for a, b in zip(r1, r2):  # bitwise, NaN == NaN (the (1030, 3, 2) R = 7 case is singular: CP_ENOTSPD)
+        assert torch.equal(a.view(torch.int64), b.view(torch.int64)), \
             "a result depends on uninitialized workspace memory"
 
 
