@@ -548,6 +548,11 @@ static bool make_layout(Layout &L, const cp_shape &s) {
       }
       const int n2 = (int)ceil_div(s.dims[2], L.rpc2);
       if (n2 > L.gp_max) L.gp_max = n2;
+      // the ylsolve kernels (modes 0, 1) write one Gram partial and one <F, A> per 8-CTA cluster
+      for (int k = 0; k < 2; ++k) {
+        const int nc = ylsolve_clusters(s.dims[k]);
+        if (nc > L.gp_max) L.gp_max = nc;
+      }
       if (L.gp_max > L.grad_max) L.grad_max = L.gp_max;  // cp_fit's gradient grids (same blocking)
     }
     L.nyr = (int)ceil_div(L.s3.dims[2], L.rpc2);

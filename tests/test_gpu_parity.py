@@ -205,11 +205,14 @@ def test_sweep_full_size_trajectory(name):
         _check_sweep(Ag, og, Ao, oo, nz2)
 
 
-def test_sweep_with_rhs(sweep_path):
-    """BNGS with a FAS right-hand side (eq:relaxinnersolve), including NULL entries."""
-    dims, R = (12, 10, 9), 3
+@pytest.mark.parametrize("dims,R", [((12, 10, 9), 3), ((64, 9, 7, 5, 3), 4), ((96, 10, 12), 24)])
+def test_sweep_with_rhs(sweep_path, dims, R):
+    """BNGS with a FAS right-hand side (eq:relaxinnersolve), including NULL entries; f and f~.
+    (64, 9, 7, 5, 3): the mode-0 ylsolve runs 2 clusters while every other blocking of the shape
+    has 1 -- the per-cluster <F, A> and Gram partials need their own slots (a round-1 layout bug
+    counted one cluster's <F, A> into mode 1's)."""
     Z, A = cpsynth.random_problem(dims, R, seed=5)
-    F = [0.05 * cpsynth.random_matrix(dims[0], R, 1), None, 0.05 * cpsynth.random_matrix(dims[2], R, 2)]
+    F = [0.05 * cpsynth.random_matrix(dims[k], R, 1 + k) if k != 1 else None for k in range(len(dims))]
     nz2 = float(np.vdot(Z, Z))
     for _, Ag, og, Ao, oo in _sweep_pair(Z, dims, A, F=F, nsweeps=3, nz2=nz2):
         _check_sweep(Ag, og, Ao, oo, nz2)
