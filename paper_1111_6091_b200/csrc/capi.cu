@@ -71,7 +71,7 @@ static int parse_env(const char *name, int dflt) {
 }
 
 int path_flag(const char *name, int dflt) {
-  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP",
+  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_GATHER",
                                        "CP_SWEEP_TREE", "CP_YLSOLVE", "CP_MODEPROD_DMMA", "CP_MG_GRAPH",
                                        "CP_ALS_GRAPH", "CP_MG_STRUCTURED", "CP_PDL"};
   for (const char *k : kPaths)
@@ -210,7 +210,7 @@ static bool plan_mma(StreamPlan &p, const cp_shape &s, int op) {
   return true;
 }
 
-bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms) {
+bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms, bool gw) {
   memset(&p, 0, sizeof(p));
   p.N = s.N;
   p.R = s.R;
@@ -261,6 +261,11 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     p.direct_w = has_f0 ? 1 : 0;
     p.srows = (has_f0 && slow && knob("CP_MMA_SROWS", 1)) ? 1 : 0;
     if (has_f0 && slow && !p.srows) p.direct_w = 0;
+    if (gw && op == OP_MTTKRP) {  // (cp_mttkrp) the weight warp gathers from the column-major factors
+      p.gw = 1;
+      p.direct_w = 0;
+      p.srows = 0;
+    }
     const int RP = 8 * p.nt;
     if (op == OP_YL) p.red_doubles = (p.ks - 1) * p.Wmax * RP + 8;
     else if (p.mode != 0) p.red_doubles = kConsumerWarps * RP + 8;
@@ -342,6 +347,10 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     }
     p.wstr = knob("CP_MMA_PAD_W", 0) ? st : WSTR;
     if (p.direct_w && knob("CP_MMA_WSTR0", 1)) p.wstr = 0;  // no weight rows
+    if (p.gw) {
+      p.ars = 0;   // nothing staged from the factors
+      p.wstr = st; // gathered weight rows at 8 (mod 16) doubles: conflict-free B fragments
+    }
   } else {
     p.ars = p.RS;
     p.wstr = WSTR;
@@ -484,6 +493,7 @@ struct Layout {
   int rpc[CP_MAX_N], sp[CP_MAX_N];  // row blocking of the solve / gradient / reduce kernels
   int nsolve[CP_MAX_N], ngrad[CP_MAX_N];
   StreamPlan plans[CP_MAX_N];
+  StreamPlan gplans[CP_MAX_N];  // cp_mttkrp: gather-weight variants (gw) of the MMA plans
   StreamPlan resid;
   // dimension-tree sweep (N >= 3): pass 1 = OP_YL over Z (mode-1 segments), pass 2 = mode-2
   // MTTKRP of Z viewed as I0 x I1 x J (J = prod_{k>=2} I_k)
@@ -505,8 +515,10 @@ static bool make_layout(Layout &L, const cp_shape &s) {
   int64_t maxI = 1;
   for (int n = 0; n < s.N; ++n) {
     if (!make_stream_plan(L.plans[n], s, n, OP_MTTKRP, sms)) return false;
-    const size_t d = stream_part_doubles(L.plans[n]);
+    size_t d = stream_part_doubles(L.plans[n]);
     if (d > part) part = d;
+    if (!L.plans[n].mma || !make_stream_plan(L.gplans[n], s, n, OP_MTTKRP, sms, true)) L.gplans[n].mma = 0;
+    if (L.gplans[n].mma && (d = stream_part_doubles(L.gplans[n])) > part) part = d;
     row_blocking(L.plans[n], &L.rpc[n], &L.sp[n]);
     L.nsolve[n] = (int)ceil_div(s.dims[n], L.rpc[n]);
     if (L.nsolve[n] > L.gp_max) L.gp_max = L.nsolve[n];
@@ -685,26 +697,36 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
   if ((st = check_ws(L, ws, ws_bytes))) return st;
   double *w = static_cast<double *>(ws);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
-  PrepArgs pa;
-  PrepGrams pg;
-  fill_prep(*s, L, w, A, mode, false, nullptr, pa, pg);
-  if (launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
-  StreamPlan p = L.plans[mode];
+  int nl = 2;
+  StreamPlan p;
+  if (L.gplans[mode].mma && path_flag("CP_MTTKRP_GATHER", 1)) {
+    // MMA plans: the stream kernel gathers the Khatri-Rao rows from the caller's column-major
+    // factors itself -- no prep launch (stream + reduce: 2 launches)
+    p = L.gplans[mode];
+    for (int k = 0; k < s->N; ++k) p.Af[k] = A[k];
+  } else {
+    PrepArgs pa;
+    PrepGrams pg;
+    fill_prep(*s, L, w, A, mode, false, nullptr, pa, pg);
+    if (launch_prep(pa, cs) != cudaSuccess) return CP_ECUDA;
+    p = L.plans[mode];
+    for (int k = 0; k < s->N; ++k) p.At[k] = w + L.At[k];
+    nl = 3;
+  }
   p.Z = Z;
-  for (int k = 0; k < s->N; ++k) p.At[k] = w + L.At[k];
   p.part = w + L.part;
   if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
   const ReduceGeom g = reduce_geom(p);
   if (g.mode0 && !g.direct && knob("CP_REDUCE0_COALESCED", 1)) {
     const int64_t S = g.In_rows * g.R;
-    if (launch_k(reduce_mode0_kernel, dim3((unsigned)ceil_div(S, 32)), dim3(256), 0, cs, (const double *)g.part, g.Gc,
-                 S, M) != cudaSuccess)
+    if (launch_k(reduce_mode0_kernel, dim3((unsigned)ceil_div(S, 32)), dim3(1024), 0, cs, (const double *)g.part,
+                 g.Gc, S, M) != cudaSuccess)
       return CP_ECUDA;
   } else if (launch_k(reduce_mttkrp_kernel, dim3(L.nsolve[mode]), dim3(256), 0, cs, g, L.rpc[mode], L.sp[mode], M) !=
              cudaSuccess) {
     return CP_ECUDA;
   }
-  g_launches = 3;
+  g_launches = nl;
   return CP_OK;
 }
 

@@ -87,6 +87,12 @@ struct StreamPlan {
   // {zcs, 1, cps}: the stage's columns are consecutive along dim 2, and the box rows past I1
   // are out of bounds -> zero-filled padding of the zcs column slots (no extra HBM bytes).
   int use_tmap;
+  // cp_mttkrp (MMA plans): gw = 1 -- the weight warp gathers the Khatri-Rao rows of each stage
+  // straight from the caller's column-major factors Af (its own copy of the producer's odometer,
+  // gated by the empty ring), so no prep launch (row-major At copies) precedes the pass; the
+  // producer stages Z only, and the mode >= 1 epilogue reads A^(1) rows from Af[0].
+  int gw;
+  const double *Af[CP_MAX_N];
   alignas(64) CUtensorMap tmap;
 };
 
@@ -135,7 +141,7 @@ cudaError_t ensure_smem_attr(const void *kernel, int bytes);
 int current_device();
 
 // Host: build the plan (geometry only; pointers filled by the caller).
-bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms);
+bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms, bool gw = false);
 size_t stream_part_doubles(const StreamPlan &p);
 cudaError_t launch_stream(const StreamPlan &p, cudaStream_t st);
 

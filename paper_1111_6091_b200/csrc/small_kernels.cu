@@ -84,20 +84,21 @@ __global__ void __launch_bounds__(256) reduce_mttkrp_kernel(const ReduceGeom g, 
 }
 
 // cp_mttkrp, mode 0: M[e] = sum_c part[c * S + e] over the Gc column-group partials, e = i + I*r
-// (the partial and the output share the column-major layout).  A block covers 32 consecutive e
-// (coalesced 256-byte rows) x 8 fixed chunks of c, combined in chunk order.
-__global__ void __launch_bounds__(256) reduce_mode0_kernel(const double *part, int Gc, int64_t S, double *M) {
+// (the partial and the output share the column-major layout).  A 1024-thread block covers 32
+// consecutive e (coalesced 256-byte rows) x 32 fixed chunks of c (~Gc/32 loads per thread, all
+// in flight: one or two memory round trips), combined in chunk order.
+__global__ void __launch_bounds__(1024) reduce_mode0_kernel(const double *part, int Gc, int64_t S, double *M) {
   griddep();
-  __shared__ double red[8][33];
+  __shared__ double red[32][33];
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
   const int64_t e = (int64_t)blockIdx.x * 32 + lx;
-  const int c0 = (Gc * ly) / 8, c1 = (Gc * (ly + 1)) / 8;
+  const int c0 = (Gc * ly) / 32, c1 = (Gc * (ly + 1)) / 32;
   red[ly][lx] = (e < S) ? sum_strided(part + (int64_t)c0 * S + e, S, c1 - c0) : 0.0;
   __syncthreads();
   if (ly == 0 && e < S) {
     double t = 0.0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += red[k][lx];
+    for (int k = 0; k < 32; ++k) t += red[k][lx];
     M[e] = t;
   }
 }

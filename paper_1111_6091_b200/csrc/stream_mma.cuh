@@ -187,6 +187,10 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   }
   if (warp == kConsumerWarps + 1) {
     // weight rows (returns at once when direct_w), then the optional Gamma job of CTA 0
+    if (p.gw) {
+      gather_weights(p, lane, v0, v1, sm);
+      return;
+    }
     form_weights(p, lane, sm);
     if (p.gj.on && blockIdx.x == 0) gamma_job_run(p.gj, sm.gjbuf, lane, 32, false);
     return;
@@ -232,6 +236,8 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   int stage = 0;
   uint32_t fph = 0;
   for (;;) {
+    // (gw: the weight warp does not wait on full -- wait for the Z bytes AND the weights)
+    if (p.gw) mbar_wait(&sm.full[stage], fph);
     mbar_wait(p.direct_w ? &sm.full[stage] : &sm.wready[stage], fph);
 #ifdef CP_CTA_TIMELINE
     if (tl_first == 0) tl_first = cta_gtimer();
@@ -394,17 +400,19 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
       double pr[NT][2];
 #pragma unroll
       for (int n = 0; n < NT; ++n) pr[n][0] = pr[n][1] = 0.0;
-      const double *a1b = p.At[0] + row0 * p.RS;
+      // A^(1) rows: the row-major copy, or (gw) the caller's column-major factor
+      const double *a1b = p.gw ? p.Af[0] + row0 : p.At[0] + row0 * p.RS;
+      const int64_t a1rs = p.gw ? 1 : p.RS, a1cs = p.gw ? p.dims[0] : 1;
 #pragma unroll
       for (int j = 0; j < MT; ++j) {
         const int m = arow0 + 8 * j;
         if (m < Wq) {
-          const double *a1 = a1b + (int64_t)m * p.RS;
+          const double *a1 = a1b + (int64_t)m * a1rs;
 #pragma unroll
           for (int n = 0; n < NT; ++n) {
             const int r = n * 8 + 2 * tq;
-            if (r < R) pr[n][0] = fma(__ldg(a1 + r), acc[j][n][0], pr[n][0]);
-            if (r + 1 < R) pr[n][1] = fma(__ldg(a1 + r + 1), acc[j][n][1], pr[n][1]);
+            if (r < R) pr[n][0] = fma(__ldg(a1 + r * a1cs), acc[j][n][0], pr[n][0]);
+            if (r + 1 < R) pr[n][1] = fma(__ldg(a1 + (r + 1) * a1cs), acc[j][n][1], pr[n][1]);
           }
         }
       }
