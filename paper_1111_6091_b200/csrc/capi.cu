@@ -71,7 +71,7 @@ static int parse_env(const char *name, int dflt) {
 }
 
 int path_flag(const char *name, int dflt) {
-  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_GATHER",
+  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM",
                                        "CP_SWEEP_TREE", "CP_YLSOLVE", "CP_MODEPROD_DMMA", "CP_MG_GRAPH",
                                        "CP_ALS_GRAPH", "CP_MG_STRUCTURED", "CP_PDL"};
   for (const char *k : kPaths)
@@ -210,7 +210,7 @@ static bool plan_mma(StreamPlan &p, const cp_shape &s, int op) {
   return true;
 }
 
-bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms, bool gw) {
+bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms, bool fcm) {
   memset(&p, 0, sizeof(p));
   p.N = s.N;
   p.R = s.R;
@@ -261,11 +261,8 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     p.direct_w = has_f0 ? 1 : 0;
     p.srows = (has_f0 && slow && knob("CP_MMA_SROWS", 1)) ? 1 : 0;
     if (has_f0 && slow && !p.srows) p.direct_w = 0;
-    if (gw && op == OP_MTTKRP) {  // (cp_mttkrp) the weight warp gathers from the column-major factors
-      p.gw = 1;
-      p.direct_w = 0;
-      p.srows = 0;
-    }
+    // (cp_mttkrp) factor rows straight from the caller's column-major factors (tensor maps)
+    if (fcm && op == OP_MTTKRP && p.direct_w) p.fcm = 1;
     const int RP = 8 * p.nt;
     if (op == OP_YL) p.red_doubles = (p.ks - 1) * p.Wmax * RP + 8;
     else if (p.mode != 0) p.red_doubles = kConsumerWarps * RP + 8;
@@ -347,9 +344,9 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     }
     p.wstr = knob("CP_MMA_PAD_W", 0) ? st : WSTR;
     if (p.direct_w && knob("CP_MMA_WSTR0", 1)) p.wstr = 0;  // no weight rows
-    if (p.gw) {
-      p.ars = 0;   // nothing staged from the factors
-      p.wstr = st; // gathered weight rows at 8 (mod 16) doubles: conflict-free B fragments
+    if (p.fcm) {
+      p.ars = 0;
+      p.wstr = 0;
     }
   } else {
     p.ars = p.RS;
@@ -361,8 +358,25 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
   p.gjsm = (p.mma && p.direct_w) ? gamma_job_smem_doubles(s.R) : 0;  // Gamma job (gamma_job.cuh)
   const int unit = p.mma ? 4 * p.ks : 1;
   int stage_doubles = 0, nst = 2;
+  // staged factor rows per stage (abuf) and slow-row slots (sbuf); fcm: the rank-major box
+  // [R][fs], fs = 4 (mod 16) doubles >= cps, slots padded to 128 B (TMA destinations)
+  auto stage_bufs = [&]() {
+    if (p.fcm) {
+      p.fs = cps + 1;  // (+1: the box starts at an even row, TMA coordinates are 16-B aligned)
+      while (p.fs % 16 != 4) ++p.fs;
+      p.astage = (int)(ceil_div((int64_t)s.R * p.fs, 16) * 16);
+      p.srs = (int)(ceil_div(2 * (int64_t)s.R, 16) * 16);
+      p.sstr = 2;
+    } else {
+      p.fs = 0;
+      p.astage = cps * p.ars;
+      p.srs = p.RS;
+      p.sstr = 1;
+    }
+  };
   for (;;) {
-    stage_doubles = p.zst + cps * p.ars + cps * p.wstr + (p.srows ? kMaxDigits * p.RS : 0);
+    stage_bufs();
+    stage_doubles = p.zst + p.astage + cps * p.wstr + (p.srows ? kMaxDigits * p.srs : 0);
     nst = knob("CP_RING_BYTES", 96 * 1024) / (stage_doubles * 8);
     if (nst < 2) nst = 2;
     if (nst > 8) nst = 8;
@@ -375,6 +389,7 @@ bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int nu
     p.cps = cps;
     p.zst = cps * p.zcs;
   }
+  stage_bufs();
   p.nstages = nst;
   p.dbg = knob("CP_STREAM_DBG", 0);
   p.keep_q = 0;
@@ -459,6 +474,40 @@ static bool encode_stage_tmap(StreamPlan &p) {
   return r == CUDA_SUCCESS;
 }
 
+// The factor tensor maps of an fcm plan (StreamPlan::fcm): 2-D views {I_k, R} of the caller's
+// column-major factors (row stride I_k * 8 bytes, a multiple of 16: I_k even, 16-B aligned base;
+// fcm_ok() checks before the plan is chosen).  fmap[0]: box {fs, R} of A^(ord[0]); fmap[j]:
+// box {2, R} of the slow digit j's factor (TMA box rows must be 16-byte multiples).
+static bool encode_factor_maps(StreamPlan &p) {
+  auto enc = tmap_encoder();
+  if (enc == nullptr) return false;
+  auto one = [&](CUtensorMap *m, int k, unsigned box0) -> bool {
+    const int64_t I = p.dims[k];
+    if ((I & 1) || ((uintptr_t)p.Af[k] % 16) != 0 || I > 0x7fffffffLL) return false;
+    const cuuint64_t gdim[2] = {(cuuint64_t)I, (cuuint64_t)p.R};
+    const cuuint64_t gstride[1] = {(cuuint64_t)I * 8};
+    const cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)p.R};
+    const cuuint32_t es[2] = {1u, 1u};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(p.Af[k]), gdim, gstride, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+  };
+  if (!one(&p.fmap[0], p.ord[0], (unsigned)p.fs)) return false;
+  for (int j = 1; j < p.nd; ++j)
+    if (p.ord[j] != p.mode && !one(&p.fmap[j], p.ord[j], 2u)) return false;
+  return true;
+}
+
+// the caller's factors can be staged through tensor maps (every factor mode of the plan)
+static bool fcm_ok(const StreamPlan &p, const cp_shape &s, const double *const *A) {
+  for (int k = 0; k < s.N; ++k) {
+    if (k == p.mode) continue;
+    if ((s.dims[k] & 1) || A[k] == nullptr || ((uintptr_t)A[k] % 16) != 0) return false;
+  }
+  return true;
+}
+
 cudaError_t launch_stream(const StreamPlan &p0, cudaStream_t st) {
   StreamPlan p = p0;
   {
@@ -472,6 +521,7 @@ cudaError_t launch_stream(const StreamPlan &p0, cudaStream_t st) {
   }
   p.use_tmap = 0;
   if (p.mma && path_flag("CP_STREAM_TMAP", 1)) p.use_tmap = encode_stage_tmap(p) ? 1 : 0;
+  if (p.fcm && !encode_factor_maps(p)) return cudaErrorInvalidValue;
   const StreamEntry &e = p.mma ? stream_mma_entry(p.nt, p.mt, p.op) : stream_entry(p.R, p.V, p.op);
   ++g_launches;
   const bool prof = g_prof_on && g_prof_n < kProfMax;
@@ -493,7 +543,7 @@ struct Layout {
   int rpc[CP_MAX_N], sp[CP_MAX_N];  // row blocking of the solve / gradient / reduce kernels
   int nsolve[CP_MAX_N], ngrad[CP_MAX_N];
   StreamPlan plans[CP_MAX_N];
-  StreamPlan gplans[CP_MAX_N];  // cp_mttkrp: gather-weight variants (gw) of the MMA plans
+  StreamPlan gplans[CP_MAX_N];  // cp_mttkrp: column-major-factor (fcm) variants of the MMA plans
   StreamPlan resid;
   // dimension-tree sweep (N >= 3): pass 1 = OP_YL over Z (mode-1 segments), pass 2 = mode-2
   // MTTKRP of Z viewed as I0 x I1 x J (J = prod_{k>=2} I_k)
@@ -517,7 +567,8 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     if (!make_stream_plan(L.plans[n], s, n, OP_MTTKRP, sms)) return false;
     size_t d = stream_part_doubles(L.plans[n]);
     if (d > part) part = d;
-    if (!L.plans[n].mma || !make_stream_plan(L.gplans[n], s, n, OP_MTTKRP, sms, true)) L.gplans[n].mma = 0;
+    if (!L.plans[n].mma || !make_stream_plan(L.gplans[n], s, n, OP_MTTKRP, sms, true) || !L.gplans[n].fcm)
+      L.gplans[n].mma = 0;
     if (L.gplans[n].mma && (d = stream_part_doubles(L.gplans[n])) > part) part = d;
     row_blocking(L.plans[n], &L.rpc[n], &L.sp[n]);
     L.nsolve[n] = (int)ceil_div(s.dims[n], L.rpc[n]);
@@ -699,9 +750,9 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   int nl = 2;
   StreamPlan p;
-  if (L.gplans[mode].mma && path_flag("CP_MTTKRP_GATHER", 1)) {
-    // MMA plans: the stream kernel gathers the Khatri-Rao rows from the caller's column-major
-    // factors itself -- no prep launch (stream + reduce: 2 launches)
+  if (L.gplans[mode].mma && path_flag("CP_MTTKRP_FCM", 1) && fcm_ok(L.gplans[mode], *s, A)) {
+    // MMA plans: the producer stages the factor rows from the caller's column-major factors
+    // through tensor maps -- no prep launch (stream + reduce: 2 launches)
     p = L.gplans[mode];
     for (int k = 0; k < s->N; ++k) p.Af[k] = A[k];
   } else {
@@ -719,8 +770,8 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
   const ReduceGeom g = reduce_geom(p);
   if (g.mode0 && !g.direct && knob("CP_REDUCE0_COALESCED", 1)) {
     const int64_t S = g.In_rows * g.R;
-    if (launch_k(reduce_mode0_kernel, dim3((unsigned)ceil_div(S, 32)), dim3(1024), 0, cs, (const double *)g.part,
-                 g.Gc, S, M) != cudaSuccess)
+    if (launch_kc(kPdlWide, reduce_mode0_kernel, dim3((unsigned)ceil_div(S, 32)), dim3(1024), 0, cs,
+                  (const double *)g.part, g.Gc, S, M) != cudaSuccess)
       return CP_ECUDA;
   } else if (launch_k(reduce_mttkrp_kernel, dim3(L.nsolve[mode]), dim3(256), 0, cs, g, L.rpc[mode], L.sp[mode], M) !=
              cudaSuccess) {

@@ -87,13 +87,19 @@ struct StreamPlan {
   // {zcs, 1, cps}: the stage's columns are consecutive along dim 2, and the box rows past I1
   // are out of bounds -> zero-filled padding of the zcs column slots (no extra HBM bytes).
   int use_tmap;
-  // cp_mttkrp (MMA plans): gw = 1 -- the weight warp gathers the Khatri-Rao rows of each stage
-  // straight from the caller's column-major factors Af (its own copy of the producer's odometer,
-  // gated by the empty ring), so no prep launch (row-major At copies) precedes the pass; the
-  // producer stages Z only, and the mode >= 1 epilogue reads A^(1) rows from Af[0].
-  int gw;
+  int astage;       // doubles per stage of the staged factor rows (abuf)
+  int srs;          // doubles per staged slow-digit row slot (sbuf)
+  int sstr;         // rank stride inside a slow-row slot (1; fcm: 2 -- a {2, R} box, TMA needs
+                    // 16-byte box rows)
+  // cp_mttkrp (MMA plans, direct_w): fcm = 1 -- the producer stages the factor rows straight
+  // from the caller's column-major factors Af through 2-D tensor maps (fmap[0]: box {fs, R} of
+  // A^(ord[0]), landing rank-major [R][fs], fs = 4 mod 16 doubles for conflict-free B
+  // fragments; fmap[j], j >= 1: box {2, R} of the slow digit j's factor), so no prep launch
+  // (row-major At copies) precedes the pass; the mode >= 1 epilogue reads A^(1) from Af[0].
+  int fcm, fs;
   const double *Af[CP_MAX_N];
   alignas(64) CUtensorMap tmap;
+  alignas(64) CUtensorMap fmap[kMaxDigits];
 };
 
 // Kernel table: one entry per (R, V, op) instantiation of stream_kernel.
@@ -141,7 +147,7 @@ cudaError_t ensure_smem_attr(const void *kernel, int bytes);
 int current_device();
 
 // Host: build the plan (geometry only; pointers filled by the caller).
-bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms, bool gw = false);
+bool make_stream_plan(StreamPlan &p, const cp_shape &s, int mode, int op, int num_sms, bool fcm = false);
 size_t stream_part_doubles(const StreamPlan &p);
 cudaError_t launch_stream(const StreamPlan &p, cudaStream_t st);
 
@@ -174,8 +180,10 @@ __device__ __forceinline__ unsigned long long ctl_clock() {
 #endif
 
 // PDL per launch class (env CP_PDL_MASK, bit c = class c; CP_PDL=0 clears all):
-//   kPdlStream: the Z-streaming kernels, kPdlCluster: ylsolve (8-CTA clusters), kPdlSmall: the rest
-enum { kPdlStream = 0, kPdlCluster = 1, kPdlSmall = 2 };
+//   kPdlStream: the Z-streaming kernels, kPdlCluster: ylsolve (8-CTA clusters), kPdlSmall: the rest,
+//   kPdlWide: 1024-thread reduction kernels (off by default: launched early, their waiting CTAs
+//   took the SM slots the streaming pass before them could use)
+enum { kPdlStream = 0, kPdlCluster = 1, kPdlSmall = 2, kPdlWide = 3 };
 bool pdl_enabled(int cls = kPdlSmall);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_kc(int cls, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -252,6 +260,14 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// 2-D tensor-map TMA (box -> shared memory, complete_tx on the stage barrier)
+__device__ __forceinline__ void tma_load_2d(void *dst_smem, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
 // 3-D tensor-map TMA (box -> shared memory, complete_tx on the stage barrier)

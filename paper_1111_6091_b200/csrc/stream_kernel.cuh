@@ -25,7 +25,7 @@
 
 namespace cpk {
 
-constexpr int kHdrInts = 16;  // per-stage header: ncols, flags, slot, -, digits[kMaxDigits]
+constexpr int kHdrInts = 16;  // per-stage header: ncols, flags, slot, fcm row offset, digits[kMaxDigits]
 
 // Register budget: up to this many accumulators per thread (V rows x R ranks) the kernel is
 // compiled for 2 CTAs/SM (<= 96 registers); above it for 1 CTA/SM.
@@ -46,9 +46,9 @@ __device__ __forceinline__ StreamSmem carve(unsigned char *raw, const StreamPlan
   StreamSmem s;
   s.zbuf = reinterpret_cast<double *>(raw);
   s.abuf = s.zbuf + (size_t)p.nstages * p.zst;
-  s.wbuf = s.abuf + (size_t)p.nstages * p.cps * p.ars;
+  s.wbuf = s.abuf + (size_t)p.nstages * p.astage;
   s.sbuf = s.wbuf + (size_t)p.nstages * p.cps * p.wstr;
-  s.red = s.sbuf + (p.srows ? (size_t)p.nstages * kMaxDigits * p.RS : 0);
+  s.red = s.sbuf + (p.srows ? (size_t)p.nstages * kMaxDigits * p.srs : 0);
   (void)WSTR;
   s.gjbuf = s.red + p.red_doubles;
   s.sS = s.gjbuf + p.gjsm;
@@ -140,8 +140,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
     ++tm_n;
 #endif
     double *zs = sm.zbuf + (size_t)stage * p.zst;
-    double *as = sm.abuf + (size_t)stage * p.cps * p.ars;
-    const bool copy_f0 = has_f0 && !p.gw;  // gw: the weight warp gathers the factor rows itself
+    double *as = sm.abuf + (size_t)stage * p.astage;
     if (V >= 2) {
       int nslow = 0;
       if (p.srows) {
@@ -152,15 +151,21 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       const bool tstage = p.use_tmap && ncols == p.cps;  // full stage: one tensor-map TMA
       const uint32_t zbytes = tstage ? (uint32_t)(p.zcs * p.cps * 8) : (uint32_t)(ncols * Wb * 8);
       if (lane == 0)
-        mbar_expect_tx(&sm.full[stage], zbytes + (copy_f0 ? ncols * p.RS * 8 : 0) + nslow * p.RS * 8);
+        mbar_expect_tx(&sm.full[stage], zbytes + (has_f0 ? (p.fcm ? p.fs * p.R * 8 : ncols * p.RS * 8) : 0) +
+                                            nslow * (p.fcm ? 2 * p.R : p.RS) * 8);
       __syncwarp();
       if (p.srows) {
-        // the factor rows of the slow digits (constant over the stage), one copy each
+        // the factor rows of the slow digits (constant over the stage), one copy each (fcm: a
+        // {2, R} box of the column-major factor's tensor map: rank r at 2r, p.sstr)
 #pragma unroll
         for (int j = 1; j < kMaxDigits; ++j)
-          if (j < nd && p.ord[j] != p.mode && lane == j)
-            bulk_g2s(sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.RS, p.At[p.ord[j]] + (int64_t)B[j] * p.RS,
-                     (uint32_t)(p.RS * 8), &sm.full[stage]);
+          if (j < nd && p.ord[j] != p.mode && lane == j) {
+            double *dst = sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.srs;
+            if (p.fcm)  // (even start row, as for digit 0: the slot holds rows B_j & ~1, +1)
+              tma_load_2d(dst, &p.fmap[j], B[j] & ~1, 0, &sm.full[stage]);
+            else
+              bulk_g2s(dst, p.At[p.ord[j]] + (int64_t)B[j] * p.RS, (uint32_t)(p.RS * 8), &sm.full[stage]);
+          }
       }
       // Z columns: q advances by qsd[0] per column within a stage (digit 0 only).  Strided
       // columns are issued by all 32 lanes (one bulk copy per column).
@@ -192,7 +197,13 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
             bulk_g2s(zs + (size_t)col * zstride, p.Z + q * p.I1 + row0, (uint32_t)(Wb * 8), &sm.full[stage]);
         }
       }
-      if (copy_f0) {
+      if (has_f0 && p.fcm) {
+        // rows B0 .. B0 + fs - 1 of the column-major factor as one {fs, R} box: rank-major
+        // [R][fs] in shared memory (rows past I_k zero-filled)
+        // (the innermost TMA coordinate must be 16-byte aligned: the box starts at the even row
+        // B0 & ~1 and the consumers skip B0 & 1 rows, header word 3)
+        if (lane == 31) tma_load_2d(as, &p.fmap[0], B[0] & ~1, 0, &sm.full[stage]);
+      } else if (has_f0) {
         if (p.ars == p.RS) {
           if (lane == 31)
             bulk_g2s(as, A0 + (int64_t)B[0] * p.RS, (uint32_t)(ncols * p.RS * 8), &sm.full[stage]);
@@ -218,6 +229,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       h[0] = ncols;
       h[1] = (eos ? 1 : 0) | (last ? 2 : 0);
       h[2] = seg_slot;
+      h[3] = B[0] & 1;  // fcm: first staged factor row of the even-aligned box
 #pragma unroll
       for (int j = 0; j < kMaxDigits; ++j) h[4 + j] = B[j];
       mbar_arrive(&sm.full[stage]);
@@ -246,97 +258,6 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
   if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 101))
     printf("[cta %d] producer: total %lld wait_empty %lld stages %lld\n", blockIdx.x, clock64() - tm0, tm_wait, tm_n);
 #endif
-}
-
-// ------------------------------------------------------------------------ gather warp (gw plans)
-// The weight warp of a gw plan: the same odometer as produce() (identical stage boundaries), and
-// for each stage, once the consumers have released its slot (empty ring), the Khatri-Rao rows
-// w[col][r] = A^(ord[0])(B0 + col, r) * S[r],  S[r] = prod_{j >= 1, ord[j] != mode} A^(ord[j])(B_j, r)
-// read from the caller's column-major factors (lanes along col: coalesced), 8 loads in flight per
-// lane, written at the row stride wstr (= 8 mod 16 doubles: conflict-free B fragments).
-static __device__ __noinline__ void gather_weights(const StreamPlan &p, int lane, int64_t v0, int64_t v1,
-                                                  const StreamSmem &sm) {
-  const int R = p.R, W = p.wstr, nd = p.nd;
-  const bool has_f0 = (p.ord[0] != p.mode);
-  const double *F0 = p.Af[p.ord[0]];
-  const int64_t If0 = p.dims[p.ord[0]];
-  int B[kMaxDigits], Bc[kMaxDigits];
-  {
-    int64_t t = v0;
-#pragma unroll
-    for (int j = 0; j < kMaxDigits; ++j) {
-      B[j] = 0;
-      Bc[j] = -1;
-      if (j < nd) {
-        B[j] = (int)(t % p.rad[j]);
-        t /= p.rad[j];
-      }
-    }
-  }
-  int64_t seg_left = p.Qn - (v0 % p.Qn);
-  int stage = 0;
-  uint32_t eph = 1;
-  int64_t v = v0;
-  while (v < v1) {
-    int64_t lim = (seg_left < v1 - v) ? seg_left : (v1 - v);
-    if (lim > p.rad[0] - B[0]) lim = p.rad[0] - B[0];
-    const int ncols = (int)(lim < p.cps ? lim : p.cps);
-    bool changed = false;
-#pragma unroll
-    for (int j = 1; j < kMaxDigits; ++j)
-      if (j < nd && B[j] != Bc[j]) changed = true;
-    if (changed) {
-      double s = 1.0;
-#pragma unroll
-      for (int j = 1; j < kMaxDigits; ++j) {
-        if (j < nd) {
-          Bc[j] = B[j];
-          const int k = p.ord[j];
-          if (k != p.mode && lane < R) s *= __ldg(p.Af[k] + B[j] + p.dims[k] * lane);
-        }
-      }
-      if (lane < R) sm.sS[lane] = s;
-    }
-    mbar_wait(&sm.empty[stage], eph);
-    __syncwarp();
-    double *ws = sm.wbuf + (size_t)stage * p.cps * W;
-    const int n = ncols * R;
-    for (int e0 = lane; e0 < n; e0 += 8 * 32) {
-      double x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + 32 * u;
-        const int ec = e < n ? e : 0;
-        const int r = ec / ncols, col = ec - r * ncols;
-        x[u] = has_f0 ? __ldg(F0 + (B[0] + col) + If0 * r) : 1.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + 32 * u;
-        if (e < n) {
-          const int r = e / ncols, col = e - r * ncols;
-          ws[col * W + r] = x[u] * sm.sS[r];
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.wready[stage]);
-    v += ncols;
-    B[0] += ncols;
-#pragma unroll
-    for (int j = 0; j + 1 < kMaxDigits; ++j) {
-      if (j + 1 < nd && B[j] >= p.rad[j]) {
-        B[j] -= p.rad[j];
-        B[j + 1] += 1;
-      }
-    }
-    seg_left -= ncols;
-    if (seg_left == 0) seg_left = p.Qn;
-    if (++stage == p.nstages) {
-      stage = 0;
-      eph ^= 1u;
-    }
-  }
 }
 
 // ------------------------------------------------------------------------ weight warp (warp 9)
@@ -383,7 +304,7 @@ static __device__ __noinline__ void form_weights(const StreamPlan &p, int lane, 
       if (lane < R) sm.sS[lane] = s;
       __syncwarp();
     }
-    const double *as = sm.abuf + (size_t)stage * p.cps * p.ars;
+    const double *as = sm.abuf + (size_t)stage * p.astage;
     double *ws = sm.wbuf + (size_t)stage * p.cps * WSTR;
     {
       // lane -> (column, rank) pairs e = lane + 32 i without divisions in the loop

@@ -148,9 +148,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     // carve (as carve<R, OP> in stream_kernel.cuh)
     sm.zbuf = reinterpret_cast<double *>(smem_raw);
     sm.abuf = sm.zbuf + (size_t)p.nstages * p.zst;
-    sm.wbuf = sm.abuf + (size_t)p.nstages * p.cps * p.ars;
+    sm.wbuf = sm.abuf + (size_t)p.nstages * p.astage;
     sm.sbuf = sm.wbuf + (size_t)p.nstages * p.cps * p.wstr;
-    sm.red = sm.sbuf + (p.srows ? (size_t)p.nstages * kMaxDigits * p.RS : 0);
+    sm.red = sm.sbuf + (p.srows ? (size_t)p.nstages * kMaxDigits * p.srs : 0);
     sm.gjbuf = sm.red + p.red_doubles;
     sm.sS = sm.gjbuf + p.gjsm;
     sm.full = reinterpret_cast<uint64_t *>(sm.sS + 32);
@@ -187,10 +187,6 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   }
   if (warp == kConsumerWarps + 1) {
     // weight rows (returns at once when direct_w), then the optional Gamma job of CTA 0
-    if (p.gw) {
-      gather_weights(p, lane, v0, v1, sm);
-      return;
-    }
     form_weights(p, lane, sm);
     if (p.gj.on && blockIdx.x == 0) gamma_job_run(p.gj, sm.gjbuf, lane, 32, false);
     return;
@@ -204,6 +200,10 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   const int gq = lane >> 2, tq = lane & 3;  // fragment coordinates
   const int zcs = p.zcs;
   const int wstride = p.direct_w ? p.ars : p.wstr;
+  // B-fragment strides: (column, rank) at col * bcs + rank * brs -- staged rows [col][rank], or
+  // (fcm) the rank-major [rank][fs] box of the column-major factor
+  const int bcs = p.fcm ? 1 : wstride;
+  const int bstage = p.direct_w ? p.astage : p.cps * p.wstr;
   const int arow0 = wi * MT * 8 + gq;  // first A row of this lane (m-tile j adds 8 j)
 
   double acc[MT][NT][2];
@@ -212,10 +212,16 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
 
-  // B-fragment rank mask (ranks >= R are zero)
+  // B-fragment rank mask (ranks >= R are zero) and the fragment's offset in a staged stage: rank
+  // 8n + gq at rank stride fs (fcm) or 1; a masked rank reads rank 0 instead (stays inside the stage of the
+  // rank-major fcm layout) and is zeroed in registers
   bool nok[NT];
+  int boff[NT];
 #pragma unroll
-  for (int n = 0; n < NT; ++n) nok[n] = (n * 8 + gq) < R;
+  for (int n = 0; n < NT; ++n) {
+    nok[n] = (n * 8 + gq) < R;
+    boff[n] = (nok[n] ? n * 8 + gq : 0) * (p.fcm ? p.fs : 1);
+  }
 
   // residual pass (OP_RESID, the mode-0 plan): x(rows, cols) = A^(0)(rows, :) W(cols, :)^T on the
   // tensor cores -- M = rows, N = 8 columns, K = 4 ranks per DMMA; the A fragments (A^(0) rows,
@@ -236,8 +242,6 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   int stage = 0;
   uint32_t fph = 0;
   for (;;) {
-    // (gw: the weight warp does not wait on full -- wait for the Z bytes AND the weights)
-    if (p.gw) mbar_wait(&sm.full[stage], fph);
     mbar_wait(p.direct_w ? &sm.full[stage] : &sm.wready[stage], fph);
 #ifdef CP_CTA_TIMELINE
     if (tl_first == 0) tl_first = cta_gtimer();
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     const int flags = h[1];
     const int slot = h[2];
     const double *zs = sm.zbuf + (size_t)stage * p.zst + arow0;
-    const double *ws = (p.direct_w ? sm.abuf : sm.wbuf) + (size_t)stage * p.cps * wstride + gq;
+    const double *ws = (p.direct_w ? sm.abuf : sm.wbuf) + (size_t)stage * bstage + (p.fcm ? h[3] : 0);
     // Khatri-Rao rows = staged factor rows x S, S = product of the slow digits' rows (staged by
     // the producer; S = 1 when there are none)
     double sl[NT];
@@ -257,9 +261,10 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #pragma unroll
       for (int j = 1; j < kMaxDigits; ++j) {
         if (j < p.nd && p.ord[j] != p.mode) {
-          const double *sr = sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.RS + gq;
+          const double *sr = sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.srs + gq * p.sstr + (p.fcm ? (h[4 + j] & 1) : 0);
 #pragma unroll
-          for (int n = 0; n < NT; ++n) sl[n] *= sr[8 * n];
+          for (int n = 0; n < NT; ++n)
+            if (nok[n]) sl[n] *= sr[8 * n * p.sstr];
         }
       }
     }
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #pragma unroll
         for (int j = 1; j < kMaxDigits; ++j) {
           if (j < p.nd && p.ord[j] != p.mode) {
-            const double *sr = sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.RS;
+            const double *sr = sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.srs;
 #pragma unroll
             for (int kk = 0; kk < KR; ++kk)
               if (4 * kk + tq < R) slr[kk] *= sr[4 * kk + tq];
@@ -280,7 +285,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
         }
       }
       const double *zb = sm.zbuf + (size_t)stage * p.zst;
-      const double *wbase = (p.direct_w ? sm.abuf : sm.wbuf) + (size_t)stage * p.cps * wstride;
+      const double *wbase = (p.direct_w ? sm.abuf : sm.wbuf) + (size_t)stage * bstage;
       for (int nc = kg; nc * 8 < ncols; nc += KS) {
         const int col = nc * 8 + gq;
         const double *wb = wbase + (col < ncols ? col : 0) * wstride;
@@ -322,12 +327,12 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     for (; k0 + 4 <= ncols; k0 += 4 * KS) {
       const int col = k0 + tq;
       const double *za = zs + col * zcs;
-      const double *wb = ws + col * wstride;
+      const double *wb = ws + col * bcs;
       double a[MT], b[NT];
 #pragma unroll
       for (int j = 0; j < MT; ++j) a[j] = za[8 * j];
 #pragma unroll
-      for (int n = 0; n < NT; ++n) b[n] = wb[8 * n];
+      for (int n = 0; n < NT; ++n) b[n] = wb[boff[n]];
 #pragma unroll
       for (int n = 0; n < NT; ++n) b[n] = nok[n] ? b[n] * sl[n] : 0.0;
 #pragma unroll
@@ -342,12 +347,12 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
       const bool ok = col < ncols;
       const int colc = ok ? col : 0;
       const double *za = zs + colc * zcs;
-      const double *wb = ws + colc * wstride;
+      const double *wb = ws + colc * bcs;
       double a[MT], b[NT];
 #pragma unroll
       for (int j = 0; j < MT; ++j) a[j] = za[8 * j];
 #pragma unroll
-      for (int n = 0; n < NT; ++n) b[n] = wb[8 * n];
+      for (int n = 0; n < NT; ++n) b[n] = wb[boff[n]];
 #pragma unroll
       for (int j = 0; j < MT; ++j) a[j] = ok ? a[j] : 0.0;
 #pragma unroll
@@ -400,9 +405,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
       double pr[NT][2];
 #pragma unroll
       for (int n = 0; n < NT; ++n) pr[n][0] = pr[n][1] = 0.0;
-      // A^(1) rows: the row-major copy, or (gw) the caller's column-major factor
-      const double *a1b = p.gw ? p.Af[0] + row0 : p.At[0] + row0 * p.RS;
-      const int64_t a1rs = p.gw ? 1 : p.RS, a1cs = p.gw ? p.dims[0] : 1;
+      // A^(1) rows: the row-major copy, or (fcm) the caller's column-major factor
+      const double *a1b = p.fcm ? p.Af[0] + row0 : p.At[0] + row0 * p.RS;
+      const int64_t a1rs = p.fcm ? 1 : p.RS, a1cs = p.fcm ? p.dims[0] : 1;
 #pragma unroll
       for (int j = 0; j < MT; ++j) {
         const int m = arow0 + 8 * j;

@@ -1,5 +1,5 @@
 """cp_mttkrp device times per mode (L2 flushed before each rep), gather path vs prep path
-(CP_MTTKRP_GATHER=1/0).  python tools/mttkrp_ab.py c3 [reps]"""
+(CP_MTTKRP_FCM=1/0).  python tools/mttkrp_ab.py c3 [reps]"""
 import os
 import sys
 
@@ -40,16 +40,16 @@ def timed(fn):
 
 res = {}
 for g in ("1", "0"):
-    os.environ["CP_MTTKRP_GATHER"] = g
+    os.environ["CP_MTTKRP_FCM"] = g
     for n in range(len(dims)):
         us = timed(lambda: cp.mttkrp(Z, dims, A, n, M=M[n], ws=ws))
         alg = 8.0 * (P + sum(dims[k] * R for k in range(len(dims)) if k != n) + dims[n] * R)
         res[(g, n)] = (us, alg / us / 1e3, cp.last_launch_count())
 for n in range(len(dims)):
-    print(f"{name} mode {n}: gather {res[('1', n)][0]:.1f} us ({res[('1', n)][1]:.0f} GB/s, {res[('1', n)][2]} launches)"
+    print(f"{name} mode {n}: fcm {res[('1', n)][0]:.1f} us ({res[('1', n)][1]:.0f} GB/s, {res[('1', n)][2]} launches)"
           f" | prep {res[('0', n)][0]:.1f} us ({res[('0', n)][1]:.0f} GB/s, {res[('0', n)][2]} launches)")
-os.environ["CP_MTTKRP_GATHER"] = "1"
+os.environ["CP_MTTKRP_FCM"] = "1"
 Mg = [cp.mttkrp(Z, dims, A, n).clone() for n in range(len(dims))]
-os.environ["CP_MTTKRP_GATHER"] = "0"
+os.environ["CP_MTTKRP_FCM"] = "0"
 Mp = [cp.mttkrp(Z, dims, A, n).clone() for n in range(len(dims))]
-print("max rel diff gather vs prep:", max(float((a - b).norm() / b.norm()) for a, b in zip(Mg, Mp)))
+print("max rel diff fcm vs prep:", max(float((a - b).norm() / b.norm()) for a, b in zip(Mg, Mp)))
