@@ -71,7 +71,7 @@ static int parse_env(const char *name, int dflt) {
 }
 
 int path_flag(const char *name, int dflt) {
-  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM",
+  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MODEPROD_PIPE",
                                        "CP_SWEEP_TREE", "CP_YLSOLVE", "CP_MODEPROD_DMMA", "CP_MG_GRAPH",
                                        "CP_ALS_GRAPH", "CP_MG_STRUCTURED", "CP_PDL"};
   for (const char *k : kPaths)

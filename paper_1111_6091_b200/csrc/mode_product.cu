@@ -231,6 +231,131 @@ __global__ void __launch_bounds__(256) gemm_dmma_kernel(const GemmArgs g) {
       }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Pipelined FP64 tensor-core GEMM (round 2): the same 64 x 128 CTA tile, 8 warps of 32 x 32 and
+// conflict-free padded fragment layouts as gemm_dmma_kernel, but the operand tiles move
+// global -> shared with cp.async (16-byte LDGSTS, zero-filled past the matrix edges) through an
+// NS-stage ring: NS - 1 k-tiles are in flight while one is multiplied, and the loads never pass
+// through registers.  Needs 16-byte pairs along each operand's contiguous dimension (even M, N,
+// K, even strides, 16-B aligned bases); launch_mode_product falls back to gemm_dmma_kernel
+// otherwise.
+__device__ __forceinline__ void cp_async16(void *dst_smem, const void *src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst_smem)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <bool A_MC, bool B_NC, int NS>
+__global__ void __launch_bounds__(256, 2) gemm_dmma_pipe_kernel(const GemmArgs g) {
+  constexpr int ASZ = A_MC ? TBK * AMS : TBM * AKS, BSZ = B_NC ? TBK * BNS : TBN * BKS;
+  extern __shared__ __align__(16) double gsm[];
+  double *As = gsm, *Bs = gsm + NS * ASZ;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int64_t bm = (int64_t)(g.swap ? blockIdx.y : blockIdx.x) * TBM;
+  const int64_t bn = (int64_t)(g.swap ? blockIdx.x : blockIdx.y) * TBN;
+  const int64_t b = blockIdx.z;
+  const double *A = g.A + b * g.sab;
+  const double *B = g.B + b * g.sbb;
+  double *C = g.C + b * g.scb;
+  const int64_t nk = (g.K + TBK - 1) / TBK;
+
+  // k-tile kt -> ring slot: A 512 pairs (2 per thread), B 1024 pairs (4 per thread)
+  auto issue = [&](int64_t kt) {
+    const int slot = (int)(kt % NS);
+    const int64_t k0 = kt * TBK;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int pr = t + 256 * j;
+      int mm, kk, so;
+      if (A_MC) { kk = pr >> 5; mm = (pr & 31) * 2; so = kk * AMS + mm; }
+      else { mm = pr >> 3; kk = (pr & 7) * 2; so = mm * AKS + kk; }
+      const int64_t m = bm + mm, k = k0 + kk;
+      const bool ok = m < g.M && k < g.K;
+      cp_async16(As + slot * ASZ + so, ok ? A + m * g.sam + k * g.sak : A, ok ? 16 : 0);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int pr = t + 256 * j;
+      int nn, kk, so;
+      if (B_NC) { kk = pr >> 6; nn = (pr & 63) * 2; so = kk * BNS + nn; }
+      else { nn = pr >> 3; kk = (pr & 7) * 2; so = nn * BKS + kk; }
+      const int64_t n = bn + nn, k = k0 + kk;
+      const bool ok = n < g.N && k < g.K;
+      cp_async16(Bs + slot * BSZ + so, ok ? B + k * g.sbk + n * g.sbn : B, ok ? 16 : 0);
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) {
+    if (s < nk) issue(s);
+    cp_async_commit();
+  }
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    cp_async_wait<NS - 2>();  // k-tile kt landed (this thread's copies) ...
+    __syncthreads();          // ... and everyone's; slot (kt - 1) % NS is free again
+    if (kt + NS - 1 < nk) issue(kt + NS - 1);
+    cp_async_commit();
+    const double *as = As + (int)(kt % NS) * ASZ;
+    const double *bs = Bs + (int)(kt % NS) * BSZ;
+#pragma unroll
+    for (int ks = 0; ks < TBK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int m = wm * 32 + i * 8 + gq, k = ks + tq;
+        af[i] = A_MC ? as[k * AMS + m] : as[m * AKS + k];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n = wn * 32 + j * 8 + gq, k = ks + tq;
+        bf[j] = B_NC ? bs[k * BNS + n] : bs[n * BKS + k];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t m = bm + wm * 32 + i * 8 + gq;
+        const int64_t n = bn + wn * 32 + j * 8 + 2 * tq + h;
+        if (m < g.M && n < g.N) C[m * g.scm + n * g.scn] = acc[i][j][h];
+      }
+}
+
+template <bool A_MC, bool B_NC, int NS>
+static size_t dmma_pipe_smem() {
+  return NS * sizeof(double) * (size_t)((A_MC ? TBK * AMS : TBM * AKS) + (B_NC ? TBK * BNS : TBN * BKS));
+}
+
+// the pipelined kernel's 16-byte pair copies are legal for this problem
+static bool pipe_ok(const GemmArgs &g, bool a_mc, bool b_nc) {
+  auto ev = [](int64_t x) { return (x & 1) == 0; };
+  if (!ev(g.M) || !ev(g.N) || !ev(g.K) || !ev(g.sab) || !ev(g.sbb)) return false;
+  if (((uintptr_t)g.A % 16) || ((uintptr_t)g.B % 16)) return false;
+  if (a_mc ? (g.sam != 1 || !ev(g.sak)) : (g.sak != 1 || !ev(g.sam))) return false;
+  if (b_nc ? (g.sbn != 1 || !ev(g.sbk)) : (g.sbk != 1 || !ev(g.sbn))) return false;
+  return true;
+}
+
 static size_t dmma_smem(bool a_mc, bool b_nc) {
   return 2 * sizeof(double) * (size_t)((a_mc ? TBK * AMS : TBM * AKS) + (b_nc ? TBK * BNS : TBN * BKS));
 }
@@ -274,8 +399,22 @@ cudaError_t launch_mode_product(int N, const int64_t *dims, const double *Z, int
       gb.B = g.B + b0 * g.sbb;
       gb.C = g.C + b0 * g.scb;
       dim3 grid((unsigned)gbig, (unsigned)gsmall, (unsigned)gb.batch);
-      if (a_mc && b_nc) gemm_dmma_kernel<true, true><<<grid, 256, dmma_smem(true, true), st>>>(gb);
-      else gemm_dmma_kernel<true, false><<<grid, 256, dmma_smem(true, false), st>>>(gb);
+      if (path_flag("CP_MODEPROD_PIPE", 1) && pipe_ok(gb, a_mc, b_nc)) {
+        // 4-stage ring for A_MC/B_NC (106 KB), 3 stages when B is k-contiguous (89 KB): 2 CTAs/SM
+        if (a_mc && b_nc) {
+          const size_t sm = dmma_pipe_smem<true, true, 4>();
+          if (cudaError_t e = ensure_smem_attr((const void *)gemm_dmma_pipe_kernel<true, true, 4>, (int)sm)) return e;
+          gemm_dmma_pipe_kernel<true, true, 4><<<grid, 256, sm, st>>>(gb);
+        } else {
+          const size_t sm = dmma_pipe_smem<true, false, 3>();
+          if (cudaError_t e = ensure_smem_attr((const void *)gemm_dmma_pipe_kernel<true, false, 3>, (int)sm)) return e;
+          gemm_dmma_pipe_kernel<true, false, 3><<<grid, 256, sm, st>>>(gb);
+        }
+      } else if (a_mc && b_nc) {
+        gemm_dmma_kernel<true, true><<<grid, 256, dmma_smem(true, true), st>>>(gb);
+      } else {
+        gemm_dmma_kernel<true, false><<<grid, 256, dmma_smem(true, false), st>>>(gb);
+      }
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
     }
