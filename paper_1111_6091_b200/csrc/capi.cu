@@ -750,9 +750,10 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   int nl = 2;
   StreamPlan p;
-  if (L.gplans[mode].mma && path_flag("CP_MTTKRP_FCM", 1) && fcm_ok(L.gplans[mode], *s, A)) {
-    // MMA plans: the producer stages the factor rows from the caller's column-major factors
-    // through tensor maps -- no prep launch (stream + reduce: 2 launches)
+  if (mode != 0 && L.gplans[mode].mma && path_flag("CP_MTTKRP_FCM", 1) && fcm_ok(L.gplans[mode], *s, A)) {
+    // MMA plans, modes >= 1: the producer stages the factor rows from the caller's column-major
+    // factors through tensor maps -- no prep launch (stream + reduce: 2 launches).  (Mode 0 keeps
+    // the prep path: measured 3-7 % faster there, tools/mttkrp_ab.py.)
     p = L.gplans[mode];
     for (int k = 0; k < s->N; ++k) p.Af[k] = A[k];
   } else {

@@ -7,6 +7,7 @@
 // Two kernels: the fp64 tensor-core (DMMA) GEMM below is the default -- measured 1.5x faster
 // than the DFMA register-tiled GEMM (c4a: 26.5 vs 17.1 TFLOP/s, c3: 23 vs 16; profiles/), which
 // stays available with CP_MODEPROD_DMMA=0.
+#include <cmath>
 #include <cstdlib>
 
 #include "cp_internal.cuh"
@@ -249,23 +250,27 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <bool A_MC, bool B_NC, int NS>
+template <bool A_MC, bool B_NC, int NS, int TN>
 __global__ void __launch_bounds__(256, 2) gemm_dmma_pipe_kernel(const GemmArgs g) {
-  constexpr int ASZ = A_MC ? TBK * AMS : TBM * AKS, BSZ = B_NC ? TBK * BNS : TBN * BKS;
+  // TN: CTA n-tile (128: warp tiles 32 x 32; 64: 32 x 16 -- twice the tiles for the wave
+  // quantization of problems with ~1000 tiles, e.g. the c3 restriction)
+  constexpr int WF = TN / 32;  // n-fragments (of 8) per warp
+  constexpr int BNSx = TN + 8, ASZ = A_MC ? TBK * AMS : TBM * AKS, BSZ = B_NC ? TBK * BNSx : TN * BKS;
+  constexpr int BPT = TN * TBK / 2 / 256;  // B pairs per thread
   extern __shared__ __align__(16) double gsm[];
   double *As = gsm, *Bs = gsm + NS * ASZ;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wm = warp >> 2, wn = warp & 3;
   const int gq = lane >> 2, tq = lane & 3;
   const int64_t bm = (int64_t)(g.swap ? blockIdx.y : blockIdx.x) * TBM;
-  const int64_t bn = (int64_t)(g.swap ? blockIdx.x : blockIdx.y) * TBN;
+  const int64_t bn = (int64_t)(g.swap ? blockIdx.x : blockIdx.y) * TN;
   const int64_t b = blockIdx.z;
   const double *A = g.A + b * g.sab;
   const double *B = g.B + b * g.sbb;
   double *C = g.C + b * g.scb;
   const int64_t nk = (g.K + TBK - 1) / TBK;
 
-  // k-tile kt -> ring slot: A 512 pairs (2 per thread), B 1024 pairs (4 per thread)
+  // k-tile kt -> ring slot: A 512 pairs (2 per thread), B TN * 8 pairs (BPT per thread)
   auto issue = [&](int64_t kt) {
     const int slot = (int)(kt % NS);
     const int64_t k0 = kt * TBK;
@@ -280,10 +285,10 @@ __global__ void __launch_bounds__(256, 2) gemm_dmma_pipe_kernel(const GemmArgs g
       cp_async16(As + slot * ASZ + so, ok ? A + m * g.sam + k * g.sak : A, ok ? 16 : 0);
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < BPT; ++j) {
       const int pr = t + 256 * j;
       int nn, kk, so;
-      if (B_NC) { kk = pr >> 6; nn = (pr & 63) * 2; so = kk * BNS + nn; }
+      if (B_NC) { kk = pr / (TN / 2); nn = (pr % (TN / 2)) * 2; so = kk * BNSx + nn; }
       else { nn = pr >> 3; kk = (pr & 7) * 2; so = nn * BKS + kk; }
       const int64_t n = bn + nn, k = k0 + kk;
       const bool ok = n < g.N && k < g.K;
@@ -291,11 +296,11 @@ __global__ void __launch_bounds__(256, 2) gemm_dmma_pipe_kernel(const GemmArgs g
     }
   };
 
-  double acc[4][4][2];
+  double acc[4][WF][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < WF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < NS - 1; ++s) {
@@ -311,39 +316,47 @@ __global__ void __launch_bounds__(256, 2) gemm_dmma_pipe_kernel(const GemmArgs g
     const double *bs = Bs + (int)(kt % NS) * BSZ;
 #pragma unroll
     for (int ks = 0; ks < TBK; ks += 4) {
-      double af[4], bf[4];
+      double af[4], bf[WF];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int m = wm * 32 + i * 8 + gq, k = ks + tq;
         af[i] = A_MC ? as[k * AMS + m] : as[m * AKS + k];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int n = wn * 32 + j * 8 + gq, k = ks + tq;
-        bf[j] = B_NC ? bs[k * BNS + n] : bs[n * BKS + k];
+      for (int j = 0; j < WF; ++j) {
+        const int n = wn * (8 * WF) + j * 8 + gq, k = ks + tq;
+        bf[j] = B_NC ? bs[k * BNSx + n] : bs[n * BKS + k];
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < WF; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
   cp_async_wait<0>();
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < WF; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t m = bm + wm * 32 + i * 8 + gq;
-        const int64_t n = bn + wn * 32 + j * 8 + 2 * tq + h;
+        const int64_t n = bn + wn * (8 * WF) + j * 8 + 2 * tq + h;
         if (m < g.M && n < g.N) C[m * g.scm + n * g.scn] = acc[i][j][h];
       }
 }
 
-template <bool A_MC, bool B_NC, int NS>
+template <bool A_MC, bool B_NC, int NS, int TN>
 static size_t dmma_pipe_smem() {
-  return NS * sizeof(double) * (size_t)((A_MC ? TBK * AMS : TBM * AKS) + (B_NC ? TBK * BNS : TBN * BKS));
+  return NS * sizeof(double) * (size_t)((A_MC ? TBK * AMS : TBM * AKS) + (B_NC ? TBK * (TN + 8) : TN * BKS));
+}
+
+template <bool A_MC, bool B_NC, int NS, int TN>
+static cudaError_t launch_pipe(const GemmArgs &g, dim3 grid, cudaStream_t st) {
+  const size_t sm = dmma_pipe_smem<A_MC, B_NC, NS, TN>();
+  if (cudaError_t e = ensure_smem_attr((const void *)gemm_dmma_pipe_kernel<A_MC, B_NC, NS, TN>, (int)sm)) return e;
+  gemm_dmma_pipe_kernel<A_MC, B_NC, NS, TN><<<grid, 256, sm, st>>>(g);
+  return cudaGetLastError();
 }
 
 // the pipelined kernel's 16-byte pair copies are legal for this problem
@@ -388,7 +401,12 @@ cudaError_t launch_mode_product(int N, const int64_t *dims, const double *Z, int
       g.C = X; g.scm = 1; g.scn = left; g.scb = left * J;
       a_mc = true; b_nc = true;
     }
-    const int64_t gx = (g.M + TBM - 1) / TBM, gy = (g.N + TBN - 1) / TBN;
+    // pipelined kernel, 64 x 128 tiles.  (A 64 x 64 variant, better wave quantization for the
+    // ~1000-tile c3 restriction, measured slower: 25.6 vs 28.4 TFLOP/s -- half the DMMAs per
+    // fragment load; kept selectable with TN = 64 in launch_pipe.)
+    const bool pipe = path_flag("CP_MODEPROD_PIPE", 1) && pipe_ok(g, a_mc, b_nc);
+    const int tn = TBN;
+    const int64_t gx = (g.M + TBM - 1) / TBM, gy = (g.N + tn - 1) / tn;
     g.swap = (gy > gx) ? 1 : 0;
     const int64_t gbig = g.swap ? gy : gx, gsmall = g.swap ? gx : gy;
     if (gsmall > 65535 || gbig > 0x7fffffff) return cudaErrorInvalidConfiguration;
@@ -399,23 +417,18 @@ cudaError_t launch_mode_product(int N, const int64_t *dims, const double *Z, int
       gb.B = g.B + b0 * g.sbb;
       gb.C = g.C + b0 * g.scb;
       dim3 grid((unsigned)gbig, (unsigned)gsmall, (unsigned)gb.batch);
-      if (path_flag("CP_MODEPROD_PIPE", 1) && pipe_ok(gb, a_mc, b_nc)) {
-        // 4-stage ring for A_MC/B_NC (106 KB), 3 stages when B is k-contiguous (89 KB): 2 CTAs/SM
-        if (a_mc && b_nc) {
-          const size_t sm = dmma_pipe_smem<true, true, 4>();
-          if (cudaError_t e = ensure_smem_attr((const void *)gemm_dmma_pipe_kernel<true, true, 4>, (int)sm)) return e;
-          gemm_dmma_pipe_kernel<true, true, 4><<<grid, 256, sm, st>>>(gb);
-        } else {
-          const size_t sm = dmma_pipe_smem<true, false, 3>();
-          if (cudaError_t e = ensure_smem_attr((const void *)gemm_dmma_pipe_kernel<true, false, 3>, (int)sm)) return e;
-          gemm_dmma_pipe_kernel<true, false, 3><<<grid, 256, sm, st>>>(gb);
-        }
+      cudaError_t e;
+      if (pipe) {
+        // 4-stage ring when B is n-contiguous, 3 when k-contiguous: <= 113 KB, 2 CTAs/SM
+        if (a_mc && b_nc) e = (tn == 64) ? launch_pipe<true, true, 4, 64>(gb, grid, st) : launch_pipe<true, true, 4, 128>(gb, grid, st);
+        else e = (tn == 64) ? launch_pipe<true, false, 4, 64>(gb, grid, st) : launch_pipe<true, false, 3, 128>(gb, grid, st);
       } else if (a_mc && b_nc) {
         gemm_dmma_kernel<true, true><<<grid, 256, dmma_smem(true, true), st>>>(gb);
+        e = cudaGetLastError();
       } else {
         gemm_dmma_kernel<true, false><<<grid, 256, dmma_smem(true, false), st>>>(gb);
+        e = cudaGetLastError();
       }
-      cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
