@@ -26,6 +26,10 @@ constexpr int kT = kSmallSweepThreads;
 // smallest R whose Cholesky runs on warp 0 (tools/chol_ab.py: R = 3 one thread 12.4 us/sweep vs
 // warp 12.9 at 4^3; R = 8 34.5 vs 30.2 at 7^3; R = 32 450 vs 209 at 13^3)
 constexpr int kSmallCholWarpMinR = 5;
+// R <= this: warp 0 factors Gamma with its rows in registers (shuffles; round 2) instead of the
+// one-thread loop; R = 5..8 keep the warp loop below (the register variant measured 5 % slower
+// at 7^3 R = 8)
+constexpr int kSmallCholRegMaxR = 4;
 
 // 1/sqrt(x), x > 0: rsqrt.approx.f64 + two Newton steps (as ys_rsqrt in ylsolve.cu): no
 // square root or division on the serial Cholesky chain
@@ -38,13 +42,24 @@ __device__ __forceinline__ double ss_rsqrt(double x) {
   return y;
 }
 
-// fixed-order block sum of one value per thread (red: kT doubles); result in every thread
+// x / d for 0 <= x < 2^22, d >= 1, from a float reciprocal plus one correction (exact): the
+// hardware has no integer divider, and the generic 32-bit division sequence dominated the tiny
+// phases of this kernel
+__device__ __forceinline__ int qdiv(int x, int d, float inv) {
+  int q = __float2int_rz((float)x * inv);
+  const int r = x - q * d;
+  q += (r >= d) - (r < 0);
+  return q;
+}
+
+// fixed-order block sum of one value per thread (red: KT doubles); result in every thread
+template <int KT>
 __device__ double block_sum_fixed(double v, double *red) {
   const int tid = threadIdx.x;
   __syncthreads();
   red[tid] = v;
   __syncthreads();
-  for (int off = kT / 2; off > 0; off >>= 1) {
+  for (int off = KT / 2; off > 0; off >>= 1) {
     if (tid < off) red[tid] += red[tid + off];
     __syncthreads();
   }
@@ -54,20 +69,25 @@ __device__ double block_sum_fixed(double v, double *red) {
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const SmallSweepArgs a) {
+// KT threads (512; a 128-thread instance for 4^3 / 7^3 measured 7-27 % slower)
+template <int KT>
+__global__ void __launch_bounds__(KT) small_sweep_kernel(const SmallSweepArgs a) {
   griddep();
   extern __shared__ double sm[];
   const int tid = threadIdx.x, N = a.N, R = a.R, RR = R * R;
+  const float inv_R = 1.0f / (float)R;
   const int64_t P = a.P;
   // shared layout (doubles): Z | A^(0..N-1) | Ups^(0..N-1) | M | part | WL | WR | Gam | L | red
   double *sZ = sm;
   // factor offsets and dims in shared memory (dynamically indexed: no local-memory copies)
   __shared__ int s_aoff[CP_MAX_N], s_dims[CP_MAX_N];
+  __shared__ float s_inv[CP_MAX_N];
   int64_t off = P;
   for (int k = 0; k < N; ++k) {
     if (tid == 0) {
       s_aoff[k] = (int)off;
       s_dims[k] = (int)a.dims[k];
+      s_inv[k] = 1.0f / (float)a.dims[k];
     }
     off += a.dims[k] * R;
   }
@@ -86,16 +106,16 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
   __shared__ double sDi[kSmallSweepMaxR];  // 1 / L(r, r)
 
   __syncthreads();
-  for (int64_t e = tid; e < P; e += kT) sZ[e] = a.Z[e];
+  for (int64_t e = tid; e < P; e += KT) sZ[e] = a.Z[e];
   for (int k = 0; k < N; ++k)
-    for (int64_t e = tid; e < s_dims[k] * R; e += kT) (sm + s_aoff[k])[e] = a.A[k][e];
+    for (int64_t e = tid; e < s_dims[k] * R; e += KT) (sm + s_aoff[k])[e] = a.A[k][e];
   if (tid == 0) {
     s_status = 0;
     s_failed = -1;
   }
   __syncthreads();
   // Upsilon^(k) = A^(k)T A^(k), sum over i ascending
-  for (int e = tid; e < N * RR; e += kT) {
+  for (int e = tid; e < N * RR; e += KT) {
     const int k = e / RR, rs = e - k * RR, r = rs % R, s = rs / R;
     const double *x = (sm + s_aoff[k]) + s_dims[k] * r, *y = (sm + s_aoff[k]) + s_dims[k] * s;
     double g = 0.0;
@@ -118,17 +138,19 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
       for (int k = 0; k < n; ++k) left *= (int)s_dims[k];
       for (int k = n + 1; k < N; ++k) right *= (int)s_dims[k];
       double *sWL = part + a.npart, *sWR = sWL + (int64_t)left * R;
-      for (int e = tid; e < (left + right) * R; e += kT) {
+      const float inv_left = 1.0f / (float)left, inv_right = 1.0f / (float)right, inv_In = s_inv[n];
+      for (int e = tid; e < (left + right) * R; e += KT) {
         const bool isl = e < left * R;
         const int ee = isl ? e : e - left * R;
         const int len = isl ? left : right;
-        int c = ee % len;
-        const int r = ee / len;
+        const int r = qdiv(ee, len, isl ? inv_left : inv_right);
+        int c = ee - r * len;
         double w = 1.0;
         for (int k = isl ? 0 : n + 1; k < (isl ? n : N); ++k) {
           const int Ik = (int)s_dims[k];
-          const int ik = c % Ik;
-          c /= Ik;
+          const int c2 = qdiv(c, Ik, s_inv[k]);
+          const int ik = c - c2 * Ik;
+          c = c2;
           w *= (sm + s_aoff[k])[ik + Ik * r];
         }
         (isl ? sWL : sWR)[ee] = w;  // ee = c + len * r
@@ -142,8 +164,8 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
       {
         const int warp = tid >> 5, lane = tid & 31;
         const int bstride = left * In;
-        for (int o = warp; o < nout; o += kT / 32) {
-          const int i = o % In, r = o / In;
+        for (int o = warp; o < nout; o += KT / 32) {
+          const int r = qdiv(o, In, inv_In), i = o - r * In;
           const double *wl = sWL + left * r, *wr = sWR + right * r;
           const double *zrow = sZ + left * i;
           double acc = 0.0;
@@ -155,7 +177,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
             for (int q = lane; q < Q; q += 32) acc = fma(zrow[q], wl[q] * w0, acc);
           } else {
             for (int q = lane; q < Q; q += 32) {
-              const int bb = q / left, aa = q - bb * left;
+              const int bb = qdiv(q, left, inv_left), aa = q - bb * left;
               acc = fma(zrow[aa + bstride * bb], wl[aa] * wr[bb], acc);
             }
           }
@@ -167,7 +189,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
       __syncthreads();
       if (n == 0) ST(2);
       // Gamma^(n) = *_{k != n} Upsilon^(k) (eq:Gamma)
-      for (int e = tid; e < RR; e += kT) {
+      for (int e = tid; e < RR; e += KT) {
         double g = 1.0;
         for (int k = 0; k < N; ++k)
           if (k != n) g *= sU[k * RR + e];
@@ -181,8 +203,8 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
         double *G = a.G[n];
         const double *An = sm + s_aoff[n];
         double g2 = 0.0, d = 0.0;
-        for (int o = tid; o < nout; o += kT) {
-          const int i = o % In, r = o / In;
+        for (int o = tid; o < nout; o += KT) {
+          const int r = qdiv(o, In, inv_In), i = o - r * In;
           double gv = -sM[o];
           for (int t = 0; t < R; ++t) gv = fma(An[i + In * t], sG[t + R * r], gv);
           if (Fg != nullptr) gv -= Fg[o];
@@ -190,10 +212,10 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
           g2 = fma(gv, gv, g2);
           if (n == N - 1) d = fma(sM[o], An[o], d);
         }
-        const double g2s = block_sum_fixed(g2, red);
+        const double g2s = block_sum_fixed<KT>(g2, red);
         if (tid == 0) a.out[2 + n] = g2s;
         gsum += g2s;
-        if (n == N - 1) inner_last = block_sum_fixed(d, red);
+        if (n == N - 1) inner_last = block_sum_fixed<KT>(d, red);
         continue;
       }
       // ---- Gamma = L L^T, lower, no pivoting; pivot <= 0 -> CP_ENOTSPD ----
@@ -202,7 +224,45 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
       //   s_i = Gamma(i,j) - sum_{k<j} L(i,k) L(j,k)
       // in the same order and expression the former one-thread loop used (bitwise identical
       // L), so the serial chain per column is j multiply-adds instead of (R - j) * j.
-      if (R < kSmallCholWarpMinR) {
+      if (R <= kSmallCholRegMaxR) {
+        // R <= 8: warp 0 with the rows in registers (lane i = row i), pivots by shuffle -- the
+        // one-thread loop below made every step a dependent shared-memory round trip (~2 k
+        // cycles per mode at R = 3, CP_SMALL_TIMING)
+        if (tid < 32) {
+          const int lane = tid;
+          constexpr int MR = kSmallCholRegMaxR;
+          double g[MR];
+#pragma unroll
+          for (int c = 0; c < MR; ++c) g[c] = (lane < R && c < R) ? sG[lane + R * c] : 0.0;
+          bool okc = true;
+#pragma unroll
+          for (int j = 0; j < MR; ++j) {
+            if (j < R) {
+              const double piv = __shfl_sync(0xffffffffu, g[j], j);
+              okc = okc && (piv > 0.0);
+              const double inv = ss_rsqrt(okc ? piv : 1.0);
+              if (lane == 0) sDi[j] = inv;
+              if (lane == j) g[j] = piv * inv;
+              else if (lane > j) g[j] *= inv;
+#pragma unroll
+              for (int k = j + 1; k < MR; ++k) {
+                const double lkj = __shfl_sync(0xffffffffu, g[j], k);
+                if (k < R && lane >= k) g[k] = fma(-g[j], lkj, g[k]);
+              }
+            }
+          }
+          if (!okc) {
+            if (lane == 0) {
+              s_status = CP_ENOTSPD;
+              s_failed = n;
+            }
+          } else if (lane < R) {
+#pragma unroll
+            for (int c = 0; c < MR; ++c)
+              if (c < R) sL[lane + R * c] = (c <= lane) ? g[c] : 0.0;
+          }
+        }
+      } else if (R < kSmallCholWarpMinR) {
         if (tid == 0) {
           for (int e = 0; e < RR; ++e) sL[e] = 0.0;
           for (int j = 0; j < R && s_status == 0; ++j) {
@@ -268,7 +328,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
         const int lane = tid & 31, warp = tid >> 5;
         double *An = sm + s_aoff[n];
         const double dl = lane < R ? sDi[lane] : 0.0;
-        for (int i = warp; i < In; i += kT / 32) {
+        for (int i = warp; i < In; i += KT / 32) {
           double b = 0.0;
           if (lane < R) b = sM[i + In * lane] + (F != nullptr ? F[i + In * lane] : 0.0);
           for (int r = 0; r < R; ++r) {
@@ -284,25 +344,39 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
           if (lane < R) An[i + In * lane] = b;
         }
       } else
-      for (int i = tid; i < In; i += kT) {
-        double *y = part + (int64_t)i * R;
-        for (int r = 0; r < R; ++r) {
-          double b = sM[i + In * r] + (F != nullptr ? F[i + In * r] : 0.0);
-          for (int k = 0; k < r; ++k) b -= sL[r + R * k] * y[k];
-          y[r] = b * sDi[r];
+      for (int i = tid; i < In; i += KT) {
+        // R < 5: a thread per row with the row in registers (the loads of a step are independent)
+        constexpr int MR = kSmallCholWarpMinR - 1;
+        double y[MR];
+#pragma unroll
+        for (int r = 0; r < MR; ++r)
+          if (r < R) y[r] = sM[i + In * r] + (F != nullptr ? F[i + In * r] : 0.0);
+#pragma unroll
+        for (int r = 0; r < MR; ++r) {
+          if (r < R) {
+            double b = y[r];
+#pragma unroll
+            for (int k = 0; k < r; ++k) b -= sL[r + R * k] * y[k];
+            y[r] = b * sDi[r];
+          }
         }
-        for (int r = R - 1; r >= 0; --r) {
-          double x = y[r];
-          for (int k = r + 1; k < R; ++k) x -= sL[k + R * r] * y[k];
-          y[r] = x * sDi[r];
-          (sm + s_aoff[n])[i + In * r] = y[r];
+#pragma unroll
+        for (int r = MR - 1; r >= 0; --r) {
+          if (r < R) {
+            double x = y[r];
+#pragma unroll
+            for (int k = r + 1; k < MR; ++k)
+              if (k < R) x -= sL[k + R * r] * y[k];
+            y[r] = x * sDi[r];
+            (sm + s_aoff[n])[i + In * r] = y[r];
+          }
         }
       }
       __syncthreads();
       if (n == 0) ST(5);
       // Upsilon^(n) of the new factor
-      for (int e = tid; e < RR; e += kT) {
-        const int r = e % R, s = e / R;
+      for (int e = tid; e < RR; e += KT) {
+        const int s = qdiv(e, R, inv_R), r = e - s * R;
         const double *x = (sm + s_aoff[n]) + In * r, *y = (sm + s_aoff[n]) + In * s;
         double g = 0.0;
         for (int i = 0; i < In; ++i) g = fma(x[i], y[i], g);
@@ -310,34 +384,35 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
       }
       if (n == N - 1 && sweep == a.nsweeps - 1) {
         double d = 0.0;
-        for (int o = tid; o < nout; o += kT) d = fma(sM[o], (sm + s_aoff[n])[o], d);
-        inner_last = block_sum_fixed(d, red);
+        for (int o = tid; o < nout; o += KT) d = fma(sM[o], (sm + s_aoff[n])[o], d);
+        inner_last = block_sum_fixed<KT>(d, red);
       }
       __syncthreads();
+      if (n == 0) ST(6);
     }
     if (a.grad || s_status != 0) continue;
     if (sweep == a.nsweeps - 1) {
       // f pieces of the last sweep, before any normalization (as cp_als_sweep then
       // cp_normalize_sort): ||[[A]]||^2 = 1^T (*_k Upsilon^(k)) 1 and sum_n <F^(n), A^(n)>
       double m2 = 0.0;
-      for (int e = tid; e < RR; e += kT) {
+      for (int e = tid; e < RR; e += KT) {
         double p = 1.0;
         for (int k = 0; k < N; ++k) p *= sU[k * RR + e];
         m2 += p;
       }
-      model2_last = block_sum_fixed(m2, red);
+      model2_last = block_sum_fixed<KT>(m2, red);
       double fa = 0.0;
       for (int k = 0; k < N; ++k)
         if (a.F[k] != nullptr)
-          for (int64_t e = tid; e < s_dims[k] * R; e += kT) fa = fma(a.F[k][e], (sm + s_aoff[k])[e], fa);
-      fa_last = block_sum_fixed(fa, red);
+          for (int64_t e = tid; e < s_dims[k] * R; e += KT) fa = fma(a.F[k][e], (sm + s_aoff[k])[e], fa);
+      fa_last = block_sum_fixed<KT>(fa, red);
     }
     if (a.normalize) {
       // eq:ALSnorm after the sweep (cp_normalize_sort with sort = 0): every column
       // scaled to lambda_r = (prod_n ||a_r^(n)||)^(1/N), unless a column norm is zero
       __shared__ double sNrm[CP_MAX_N * kSmallSweepMaxR], sLam[kSmallSweepMaxR];
       __shared__ int sPos[kSmallSweepMaxR];
-      for (int e = tid; e < N * R; e += kT) {
+      for (int e = tid; e < N * R; e += KT) {
         const int k = e / R, r = e - k * R;
         const double *col = (sm + s_aoff[k]) + s_dims[k] * r;
         double ss = 0.0;
@@ -345,7 +420,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
         sNrm[e] = sqrt(ss);
       }
       __syncthreads();
-      for (int r = tid; r < R; r += kT) {
+      for (int r = tid; r < R; r += KT) {
         double prod = 1.0;
         int pos = 1;
         for (int k = 0; k < N; ++k) {
@@ -358,13 +433,13 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
       __syncthreads();
       for (int k = 0; k < N; ++k) {
         double *Ak = sm + s_aoff[k];
-        for (int e = tid; e < s_dims[k] * R; e += kT) {
+        for (int e = tid; e < s_dims[k] * R; e += KT) {
           const int r = e / s_dims[k];
           if (sPos[r]) Ak[e] = sLam[r] * (Ak[e] / sNrm[k * R + r]);
         }
       }
       __syncthreads();
-      for (int e = tid; e < N * RR; e += kT) {  // the Grams of the normalized factors
+      for (int e = tid; e < N * RR; e += KT) {  // the Grams of the normalized factors
         const int k = e / RR, rs = e - k * RR, r = rs % R, s2 = rs / R;
         const double *x = (sm + s_aoff[k]) + s_dims[k] * r, *y = (sm + s_aoff[k]) + s_dims[k] * s2;
         double g = 0.0;
@@ -377,18 +452,18 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
 
 #ifdef CP_SMALL_TIMING
   if (threadIdx.x == 0)
-    printf("small sweep phases (clk, mode 0 of sweep 1): wlwr %lld mttkrp %lld msum+gamma %lld chol %lld solve %lld\n",
-           tst[1] - tst[0], tst[2] - tst[1], tst[3] - tst[2], tst[4] - tst[3], tst[5] - tst[4]);
+    printf("small sweep phases (clk, mode 0 of sweep 1): wlwr %lld mttkrp %lld msum+gamma %lld chol %lld solve %lld gram %lld\n",
+           tst[1] - tst[0], tst[2] - tst[1], tst[3] - tst[2], tst[4] - tst[3], tst[5] - tst[4], tst[6] - tst[5]);
 #endif
   if (a.grad) {
     // f by the expansion (reading R6), g = (sum_n ||G^(n)||^2)^{1/2} / ||Z|| (eq:gradConv)
     double m2 = 0.0;
-    for (int e = tid; e < RR; e += kT) {
+    for (int e = tid; e < RR; e += KT) {
       double p = 1.0;
       for (int k = 0; k < N; ++k) p *= sU[k * RR + e];
       m2 += p;
     }
-    const double model2 = block_sum_fixed(m2, red);
+    const double model2 = block_sum_fixed<KT>(m2, red);
     if (tid == 0) {
       a.out[0] = 0.5 * a.normZ2[0] - inner_last + 0.5 * model2;
       a.out[1] = sqrt(gsum) / sqrt(a.normZ2[0]);
@@ -397,7 +472,7 @@ __global__ void __launch_bounds__(kSmallSweepThreads) small_sweep_kernel(const S
   }
   // ---- write back, f and f~ (readings R6, R5) ----
   for (int k = 0; k < N; ++k)
-    for (int64_t e = tid; e < s_dims[k] * R; e += kT) a.A[k][e] = (sm + s_aoff[k])[e];
+    for (int64_t e = tid; e < s_dims[k] * R; e += KT) a.A[k][e] = (sm + s_aoff[k])[e];
   if (s_status != 0) {
     if (tid == 0) {
       a.out[0] = nan("");
@@ -473,10 +548,10 @@ cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double 
   a.out = out;
   const size_t smem = small_sweep_smem_bytes(s);
   if (smem > 48 * 1024) {
-    cudaError_t e = ensure_smem_attr((const void *)small_sweep_kernel, (int)smem);
+    cudaError_t e = ensure_smem_attr((const void *)small_sweep_kernel<kT>, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  return launch_k(small_sweep_kernel, dim3(1), dim3(kT), smem, st, a);
+  return launch_k(small_sweep_kernel<kT>, dim3(1), dim3(kT), smem, st, a);
 }
 
 }  // namespace cpk
