@@ -247,29 +247,44 @@ struct MG {
     if (err != CP_OK) return;
     ok(cp_gradient(&v.s, v.Z, v.nz2, A, nullptr, out_fit, G, ws, ws_bytes, cst));
   }
+  // The factor-sized transfers of level l, every mode in ONE launch (xfer_kernel): restriction
+  // R^(n) = Phat^(n)T (Ic x I) or interpolation Phat^(n) (I x Ic) of the coarsened modes, identity
+  // otherwise (eq:coarseapprox_new, eq:CGC_new, eq:FASrhs, eq:FASCGC)
+  XferArgs xfer_args(int l, int op, bool down) {
+    Level &v = lv[l];
+    XferArgs a;
+    memset(&a, 0, sizeof(a));
+    a.N = N;
+    a.R = R;
+    a.op = op;
+    for (int n = 0; n < N; ++n) {
+      a.coarsen[n] = v.coarsen[n] ? 1 : 0;
+      a.rows_in[n] = down ? v.s.dims[n] : v.Ic[n];
+      a.rows_out[n] = down ? v.Ic[n] : v.s.dims[n];
+      a.T[n] = v.coarsen[n] ? (down ? v.Rt[n] : v.Ph[n]) : nullptr;
+    }
+    return a;
+  }
+  void xfer(XferArgs &a) {
+    if (err == CP_OK && launch_xfer(a, st) != cudaSuccess) err = CP_ECUDA;
+  }
   // dst (level l+1 sizes) = R^(n) src^(n) for coarsened modes, copy otherwise
   void restrict_(int l, double *const *src, double *const *dst) {
-    Level &v = lv[l];
-    for (int n = 0; n < N && err == CP_OK; ++n) {
-      if (v.coarsen[n]) {
-        const int64_t d[2] = {v.s.dims[n], R};
-        ok(cp_mode_product(2, d, src[n], 0, v.Rt[n], v.Ic[n], dst[n], nullptr, 0, cst));
-      } else {
-        copy(dst[n], src[n], (size_t)v.s.dims[n] * R);
-      }
+    XferArgs a = xfer_args(l, kXferApply, true);
+    for (int n = 0; n < N; ++n) {
+      a.x[n] = src[n];
+      a.dst[n] = dst[n];
     }
+    xfer(a);
   }
   // dst (level l sizes) = Phat^(n) src^(n) for coarsened modes, copy otherwise
   void interp(int l, double *const *src, double *const *dst) {
-    Level &v = lv[l];
-    for (int n = 0; n < N && err == CP_OK; ++n) {
-      if (v.coarsen[n]) {
-        const int64_t d[2] = {v.Ic[n], R};
-        ok(cp_mode_product(2, d, src[n], 0, v.Ph[n], v.s.dims[n], dst[n], nullptr, 0, cst));
-      } else {
-        copy(dst[n], src[n], (size_t)v.s.dims[n] * R);
-      }
+    XferArgs a = xfer_args(l, kXferApply, false);
+    for (int n = 0; n < N; ++n) {
+      a.x[n] = src[n];
+      a.dst[n] = dst[n];
     }
+    xfer(a);
   }
 
   // Transfer operators of level l fitted to the test blocks (and the boot factors
@@ -441,19 +456,28 @@ struct MG {
     restrict_(l, v.A, nx.Atil);     // A~_c
     grad(l, v.A, v.H);              // H(A)
     grad(l + 1, nx.Atil, nx.H);     // H_c(A~_c)
-    for (int n = 0; n < N; ++n)     // tmp = F - H(A)
-      lincomb(v.tmp[n], -1.0, v.H[n], 1.0, F ? F[n] : nullptr, v.s.dims[n] * R);
-    restrict_(l, v.tmp, nx.tmp);    // R (F - H(A))
-    for (int n = 0; n < N; ++n) {   // F_c = H_c(A~_c) + R (F - H(A))   (eq:FASrhs)
-      lincomb(nx.F[n], 1.0, nx.H[n], 1.0, nx.tmp[n], nx.s.dims[n] * R);
-      copy(nx.A[n], nx.Atil[n], (size_t)nx.s.dims[n] * R);
+    {                               // F_c = H_c(A~_c) + R (F - H(A))  (eq:FASrhs);  A_c = A~_c
+      XferArgs a = xfer_args(l, kXferFasRhs, true);
+      for (int n = 0; n < N; ++n) {
+        a.x[n] = v.H[n];
+        a.y[n] = F ? F[n] : nullptr;
+        a.z[n] = nx.H[n];
+        a.w[n] = nx.Atil[n];
+        a.dst[n] = nx.F[n];
+        a.dst2[n] = nx.A[n];
+      }
+      xfer(a);
     }
     fas_cycle(l + 1, nx.F);
-    for (int n = 0; n < N; ++n)     // A_c - A~_c
-      lincomb(nx.tmp[n], 1.0, nx.A[n], -1.0, nx.Atil[n], nx.s.dims[n] * R);
-    interp(l, nx.tmp, v.tmp);
-    for (int n = 0; n < N; ++n)     // A += Phat (A_c - A~_c)   (eq:FASCGC)
-      lincomb(v.A[n], 1.0, v.A[n], 1.0, v.tmp[n], v.s.dims[n] * R);
+    {                               // A += Phat (A_c - A~_c)  (eq:FASCGC)
+      XferArgs a = xfer_args(l, kXferCorrect, false);
+      for (int n = 0; n < N; ++n) {
+        a.x[n] = nx.A[n];
+        a.y[n] = nx.Atil[n];
+        a.dst[n] = v.A[n];
+      }
+      xfer(a);
+    }
     relax_fas(l, v.A, F, prm.nu2_solve);
   }
 

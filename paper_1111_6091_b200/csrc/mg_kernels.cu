@@ -81,6 +81,53 @@ __global__ void lincomb_kernel(double *out, double alpha, const double *x, doubl
     out[i] = alpha * x[i] + (y != nullptr ? beta * y[i] : 0.0);
 }
 
+// one thread per output entry (row j, rank r) of every mode; dense rows of T are summed in
+// ascending order
+__global__ void __launch_bounds__(256) xfer_kernel(const XferArgs a) {
+  griddep();
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.off[a.N]) return;
+  int n = 0;
+  while (e >= a.off[n + 1]) ++n;
+  const int64_t o = e - a.off[n];
+  const int64_t ro = a.rows_out[n], ri = a.rows_in[n];
+  const int64_t r = o / ro, j = o - r * ro;
+  const double *x = a.x[n], *y = a.y[n];
+  double v = 0.0;
+  if (a.coarsen[n]) {
+    const double *T = a.T[n] + j;
+    const double *xc = x + ri * r, *yc = (y != nullptr) ? y + ri * r : nullptr;
+    if (a.op == kXferApply) {
+      for (int64_t i = 0; i < ri; ++i) v = fma(T[ro * i], xc[i], v);
+    } else if (a.op == kXferFasRhs) {  // T (y - x), y optional
+      for (int64_t i = 0; i < ri; ++i) v = fma(T[ro * i], (yc != nullptr ? yc[i] : 0.0) - xc[i], v);
+    } else {                           // T (x - y)
+      for (int64_t i = 0; i < ri; ++i) v = fma(T[ro * i], xc[i] - yc[i], v);
+    }
+  } else {
+    const int64_t q = j + ri * r;
+    if (a.op == kXferApply) v = x[q];
+    else if (a.op == kXferFasRhs) v = (y != nullptr ? y[q] : 0.0) - x[q];
+    else v = x[q] - y[q];
+  }
+  if (a.op == kXferApply) {
+    a.dst[n][o] = v;
+  } else if (a.op == kXferFasRhs) {
+    a.dst[n][o] = a.z[n][o] + v;
+    a.dst2[n][o] = a.w[n][o];
+  } else {
+    a.dst[n][o] += v;
+  }
+}
+
+cudaError_t launch_xfer(XferArgs &a, cudaStream_t st) {
+  a.off[0] = 0;
+  for (int n = 0; n < a.N; ++n) a.off[n + 1] = a.off[n] + a.rows_out[n] * a.R;
+  const int64_t tot = a.off[a.N];
+  const unsigned blocks = (unsigned)((tot + 255) / 256);
+  return launch_k(xfer_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, st, a);
+}
+
 cudaError_t launch_normalize_sort(const NormArgs &a, cudaStream_t st) {
   normalize_sort_kernel<<<1, 256, 0, st>>>(a);
   return cudaGetLastError();
