@@ -485,12 +485,14 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
       }
     }
   }
-#ifdef CP_CTA_TIMELINE
+#ifdef CP_CTA_TIMELINE_STREAM
   if (tid == 0)
     printf("CTL %d %d %d %u %llu %llu %llu %llu\n", OP, p.mode, blockIdx.x, tl_smid, tl_enter, tl_first, tl_loop,
            cta_gtimer());
 #endif
+#ifdef CP_CTA_TIMELINE_STREAM
   CTL_END(OP == OP_YL ? "streamYL" : (OP == OP_RESID ? "streamRES" : (p.mode == 0 ? "streamM0" : "streamMn")))
+#endif
 }
 
 template <int NT, int MT, int OP>

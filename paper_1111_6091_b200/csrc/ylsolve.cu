@@ -52,6 +52,16 @@ __device__ __forceinline__ void ld_v4(const double *p, double (&v)[4]) {
                : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
                : "l"(p));
 }
+// kYsRows consecutive doubles (the block's rows of one Y_L column) in one vector load
+template <int N>
+__device__ __forceinline__ void ld_rows(const double *p, double (&v)[N]) {
+  if constexpr (N == 4) {
+    ld_v4(p, v);
+  } else {
+    static_assert(N == 2, "kYsRows: 2 or 4");
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "l"(p));
+  }
+}
 
 // Gamma^(mode)(e) for the entries e = lane + 32 q of one warp: products of Upsilon^(k), k !=
 // mode, read as totals (Ups, bit k of a.ups_total; all loads of a lane issued before use) or
@@ -219,39 +229,39 @@ __global__ void __launch_bounds__(256, 2) __cluster_dims__(kYsCluster, 1, 1) yls
       const int nsl = (CW * 32) / R;
       if (tid < nsl * R) {
         const int r = tid % R, sl = tid / R;
-        double acc[kYsRows] = {0.0, 0.0, 0.0, 0.0};
+        double acc[kYsRows] = {};
         const double *yb = a.yl + (int64_t)r * I0 + r0;
         const double *bt = a.Bfac + r;  // At^(1): row-major, stride RS
-        if (nrows == kYsRows && (I0 & 3) == 0) {
+        if (nrows == kYsRows && (I0 % kYsRows) == 0) {
           int64_t i1 = sl;
           for (; i1 + 7 * nsl < I1; i1 += 8 * nsl) {
-            double y[8][4], b[8];
+            double y[8][kYsRows], b[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              ld_v4(yb + (i1 + j * nsl) * blk, y[j]);
+              ld_rows(yb + (i1 + j * nsl) * blk, y[j]);
               b[j] = __ldg(bt + (i1 + j * nsl) * a.RS);
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j)
 #pragma unroll
-              for (int u = 0; u < 4; ++u) acc[u] = fma(y[j][u], b[j], acc[u]);
+              for (int u = 0; u < kYsRows; ++u) acc[u] = fma(y[j][u], b[j], acc[u]);
           }
           if (i1 < I1) {
             // the remainder as ONE predicated batch (a serial loop here paid one memory round
             // trip per i1: 5 of the 9 round trips of the c4a contraction)
-            double y[8][4], b[8];
+            double y[8][kYsRows], b[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const int64_t ij = i1 + j * nsl;
               const int64_t ic = ij < I1 ? ij : (int64_t)sl;
-              ld_v4(yb + ic * blk, y[j]);
+              ld_rows(yb + ic * blk, y[j]);
               b[j] = __ldg(bt + ic * a.RS);
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               if (i1 + j * nsl < I1)
 #pragma unroll
-                for (int u = 0; u < 4; ++u) acc[u] = fma(y[j][u], b[j], acc[u]);
+                for (int u = 0; u < kYsRows; ++u) acc[u] = fma(y[j][u], b[j], acc[u]);
           }
         } else {
           for (int64_t i1 = sl; i1 < I1; i1 += nsl) {
@@ -280,7 +290,7 @@ __global__ void __launch_bounds__(256, 2) __cluster_dims__(kYsCluster, 1, 1) yls
       for (int r = warp; r < R; r += CW) {
         const double *ab = a.Bfac + (int64_t)r * I0;
         const double *yb = a.yl + (int64_t)r * I0 + r0 * blk;
-        double acc[kYsRows] = {0.0, 0.0, 0.0, 0.0};
+        double acc[kYsRows] = {};
         for (int64_t c0 = lane; c0 < nch; c0 += 64) {
           const int64_t c1 = c0 + 32;
           const bool ok1 = c1 < nch;
