@@ -4,6 +4,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <chrono>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -71,7 +74,7 @@ static int parse_env(const char *name, int dflt) {
 }
 
 int path_flag(const char *name, int dflt) {
-  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MODEPROD_PIPE",
+  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MTTKRP_FUSED", "CP_MODEPROD_PIPE",
                                        "CP_SWEEP_TREE", "CP_YLSOLVE", "CP_MODEPROD_DMMA", "CP_MG_GRAPH",
                                        "CP_ALS_GRAPH", "CP_MG_STRUCTURED", "CP_PDL"};
   for (const char *k : kPaths)
@@ -110,6 +113,15 @@ cudaError_t ensure_smem_attr(const void *kernel, int bytes) {
 // c4a ~15 us per sweep (its CTAs, launched early, wait where the pass could run); default: stream +
 // small kernels.  CP_PDL=0 (path selector) disables PDL everywhere; the mask is an experiment knob.
 constexpr int kPdlDefaultMask = (1 << kPdlStream) | (1 << kPdlSmall);
+// Launch nonces of the tagged completion words (cp_internal.cuh tagged_arrive): never 0, seeded
+// per process so a workspace handed between processes does not meet its previous tags.
+static unsigned next_tag() {
+  static std::atomic<unsigned> ctr{(unsigned)std::chrono::steady_clock::now().time_since_epoch().count() * 2654435761u};
+  unsigned t;
+  do t = ctr.fetch_add(1u); while (t == 0u || t == 0xffffffffu);
+  return t;
+}
+
 bool pdl_enabled(int cls) {
   const int mask = path_flag("CP_PDL", 1) != 0 ? knob("CP_PDL_MASK", kPdlDefaultMask) : 0;
   return (mask >> cls) & 1;
@@ -552,6 +564,7 @@ struct Layout {
   cp_shape s3;
   int rpc2, sp2, nyr;
   size_t yl, edge, mbuf, yr, segtab, m0part, linv;
+  size_t tick;  // tagged completion words (StreamPlan::tick): 3 + max I_n
   size_t ntmp;  // cp_als_sweeps with CP_SWEEPS_NORMALIZE: normalization scratch (sum_n I_n R)
 };
 
@@ -579,7 +592,6 @@ static bool make_layout(Layout &L, const cp_shape &s) {
   }
   L.prep_blocks = 0;
   for (int k = 0; k < s.N; ++k) L.prep_blocks += (int)ceil_div(s.dims[k], kPrepRows);
-  (void)maxI;
   if (!make_stream_plan(L.resid, s, 0, OP_RESID, sms)) return false;
   L.tree = (s.N >= 3) && path_flag("CP_SWEEP_TREE", 1) != 0;
   if (L.tree) {
@@ -647,6 +659,7 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     L.yr = off; off = align_up(off + (size_t)L.s3.dims[2] * R);
     L.segtab = off; off = align_up(off + (size_t)(s.dims[1] * y.RB + 1) / 2);  // u32 ticket per (segment, row block)
   }
+  L.tick = off; off = align_up(off + 3 + (size_t)maxI);
   {
     size_t sumIR = 0;
     for (int k = 0; k < s.N; ++k) sumIR += (size_t)s.dims[k] * R;
@@ -655,6 +668,61 @@ static bool make_layout(Layout &L, const cp_shape &s) {
   }
   L.total = off * sizeof(double);
   return true;
+}
+
+// Layouts (all launch plans of a shape) cached per (device, shape, planning path flags): planning
+// costs ~10-20 us of host time per call, as much as a c3 pass on the device.  A small most-
+// recently-used list; entries are immutable and shared.  Experiment builds (knobs from the
+// environment may change between calls) always plan afresh.
+static std::shared_ptr<const Layout> get_layout(const cp_shape &s) {
+#ifdef CP_EXPERIMENTS
+  auto fresh = std::make_shared<Layout>();
+  if (!make_layout(*fresh, s)) return nullptr;
+  return fresh;
+#else
+  struct Key {
+    int dev, N, R, flags[4];
+    int64_t dims[CP_MAX_N];
+    bool operator==(const Key &o) const {
+      if (dev != o.dev || N != o.N || R != o.R) return false;
+      for (int i = 0; i < 4; ++i)
+        if (flags[i] != o.flags[i]) return false;
+      for (int k = 0; k < N; ++k)
+        if (dims[k] != o.dims[k]) return false;
+      return true;
+    }
+  };
+  Key key;
+  memset(&key, 0, sizeof(key));
+  key.dev = current_device();
+  key.N = s.N;
+  key.R = s.R;
+  for (int k = 0; k < s.N && k < CP_MAX_N; ++k) key.dims[k] = s.dims[k];
+  key.flags[0] = path_flag("CP_STREAM_MMA", 1);
+  key.flags[1] = path_flag("CP_RESID_MMA", 1);
+  key.flags[2] = path_flag("CP_STREAM_TMAP", 1);
+  key.flags[3] = path_flag("CP_SWEEP_TREE", 1);
+  static std::mutex mu;
+  static std::vector<std::pair<Key, std::shared_ptr<const Layout>>> cache;  // most recent first
+  constexpr size_t kMaxLayouts = 32;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (size_t i = 0; i < cache.size(); ++i) {
+      if (cache[i].first == key) {
+        auto hit = cache[i];
+        cache.erase(cache.begin() + (long)i);
+        cache.insert(cache.begin(), hit);
+        return hit.second;
+      }
+    }
+  }
+  auto fresh = std::make_shared<Layout>();
+  if (!make_layout(*fresh, s)) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  cache.insert(cache.begin(), {key, fresh});
+  if (cache.size() > kMaxLayouts) cache.pop_back();
+  return fresh;
+#endif
 }
 
 // Arguments of the prep kernel (At copies of every factor except skip_mode; per-block partial
@@ -710,9 +778,8 @@ size_t cp_workspace_bytes(const cp_shape *s) {
     // cp_norm2 only needs its block partials
     return (size_t)(2 * device_sms() + 64) * sizeof(double);
   }
-  Layout L;
-  if (!make_layout(L, *s)) return 0;
-  return L.total;
+  const auto Lp = get_layout(*s);
+  return Lp ? Lp->total : 0;
 }
 
 int cp_norm2(const cp_shape *s, const double *Z, double *out, void *ws, size_t ws_bytes,
@@ -743,17 +810,20 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
   if (!Z || !A || !M || mode < 0 || mode >= s->N || !aligned(Z, 16)) return CP_EINVAL;
   for (int k = 0; k < s->N; ++k)
     if (k != mode && A[k] == nullptr) return CP_EINVAL;
-  Layout L;
-  if (!make_layout(L, *s)) return CP_EINVAL;
+  const auto Lp = get_layout(*s);
+  if (!Lp) return CP_EINVAL;
+  const Layout &L = *Lp;
   if ((st = check_ws(L, ws, ws_bytes))) return st;
   double *w = static_cast<double *>(ws);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   int nl = 2;
   StreamPlan p;
-  if (mode != 0 && L.gplans[mode].mma && path_flag("CP_MTTKRP_FCM", 1) && fcm_ok(L.gplans[mode], *s, A)) {
-    // MMA plans, modes >= 1: the producer stages the factor rows from the caller's column-major
-    // factors through tensor maps -- no prep launch (stream + reduce: 2 launches).  (Mode 0 keeps
-    // the prep path: measured 3-7 % faster there, tools/mttkrp_ab.py.)
+  // 0: never, 1: modes >= 1, 2: every mode (default; r02: mode 0 c3 43.0 -> 40.9 us, c4b
+  // 162.5 -> 150.0 us against prep + At copies, tools/mttkrp_ab.py)
+  const int fcm_sel = path_flag("CP_MTTKRP_FCM", 2);
+  if ((mode != 0 || fcm_sel >= 2) && fcm_sel > 0 && L.gplans[mode].mma && fcm_ok(L.gplans[mode], *s, A)) {
+    // MMA plans: the producer stages the factor rows from the caller's column-major factors
+    // through tensor maps -- no prep launch
     p = L.gplans[mode];
     for (int k = 0; k < s->N; ++k) p.Af[k] = A[k];
   } else {
@@ -767,6 +837,19 @@ int cp_mttkrp(const cp_shape *s, const double *Z, const double *const *A, int32_
   }
   p.Z = Z;
   p.part = w + L.part;
+  // MMA plans finish M inside the pass: no reduce launch.  CP_MTTKRP_FUSED = 1 (default): modes
+  // >= 1 when a CTA touches few segments (tagged tickets, one round trip per 32 segments at the
+  // CTA's end); 2: also mode 0 (grid barrier + sliced sum; measured slower than the separate
+  // reduce: c3 27.6 -> 34.8 us, c4a 199 -> 206 us per call).
+  const int fused = path_flag("CP_MTTKRP_FUSED", 1);
+  if (p.mma && fused > 0 && (mode == 0 ? fused >= 2 : p.slots <= 32)) {
+    p.Mout = M;
+    p.tick = reinterpret_cast<unsigned long long *>(w + L.tick);
+    p.tag = next_tag();
+    if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
+    g_launches = nl - 1;
+    return CP_OK;
+  }
   if (launch_stream(p, cs) != cudaSuccess) return CP_ECUDA;
   const ReduceGeom g = reduce_geom(p);
   if (g.mode0 && !g.direct && knob("CP_REDUCE0_COALESCED", 1)) {
@@ -809,8 +892,9 @@ int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, doub
   const bool norm = (flags & CP_SWEEPS_NORMALIZE) != 0;
   for (int k = 0; k < s->N; ++k)
     if (A[k] == nullptr) return CP_EINVAL;
-  Layout L;
-  if (!make_layout(L, *s)) return CP_EINVAL;
+  const auto Lp = get_layout(*s);
+  if (!Lp) return CP_EINVAL;
+  const Layout &L = *Lp;
   if ((st = check_ws(L, ws, ws_bytes))) return st;
   if (use_small_sweep(*s)) {
     if (launch_small_sweep(*s, Z, normZ2, A, F, nsweeps, out, reinterpret_cast<cudaStream_t>(stream), nullptr,
@@ -858,8 +942,9 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
                       bool first, bool steady) {
   g_launches = 0;
   int st;
-  Layout L;
-  if (!make_layout(L, *s)) return CP_EINVAL;
+  const auto Lp = get_layout(*s);
+  if (!Lp) return CP_EINVAL;
+  const Layout &L = *Lp;
   double *w = static_cast<double *>(ws);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   const int N = s->N, R = s->R;
@@ -1160,8 +1245,9 @@ static int fit_impl(const cp_shape *s, const double *Z, const double *normZ2, co
   if (!Z || !normZ2 || !A || !out || !aligned(Z, 16)) return CP_EINVAL;
   for (int k = 0; k < s->N; ++k)
     if (A[k] == nullptr) return CP_EINVAL;
-  Layout L;
-  if (!make_layout(L, *s)) return CP_EINVAL;
+  const auto Lp = get_layout(*s);
+  if (!Lp) return CP_EINVAL;
+  const Layout &L = *Lp;
   if ((st = check_ws(L, ws, ws_bytes))) return st;
   double *w = static_cast<double *>(ws);
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);

@@ -98,6 +98,14 @@ struct StreamPlan {
   // (row-major At copies) precedes the pass; the mode >= 1 epilogue reads A^(1) from Af[0].
   int fcm, fs;
   const double *Af[CP_MAX_N];
+  // cp_mttkrp in one launch (MMA plans, OP_MTTKRP): Mout != null -- the pass finishes M itself.
+  // Modes >= 1: the last contributor of each segment (tagged ticket tick[segment]) sums the
+  // segment's partials in the fixed order of reduce_mttkrp_kernel; mode 0: a grid barrier
+  // (tick[0..2]), then every CTA sums a slice of the I1 x R entries in the order of
+  // reduce_mode0_kernel.  tag: this launch's nonce (tagged_arrive).
+  double *Mout;
+  unsigned long long *tick;
+  unsigned tag;
   alignas(64) CUtensorMap tmap;
   alignas(64) CUtensorMap fmap[kMaxDigits];
 };
@@ -321,6 +329,80 @@ __device__ __forceinline__ int64_t opaque(int64_t x) {
 }
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ---------------------------------------------------------------- in-kernel completion
+// Tagged arrival counters over caller-owned, uninitialized workspace: a 64-bit word holds
+// (tag << 32 | count).  An arrival whose tag differs from the word's starts a new count (no
+// zeroing launch needed); the last of n arrivals of a launch resets the word to 0.  Tags are
+// per-launch host nonces, never 0, so a word left by a completed launch never matches, and a CUDA
+// graph that replays one tag starts every replay from 0.  Called by one thread; returns true for
+// the last arrival.  The caller fences its data stores before arriving.
+__device__ __forceinline__ bool tagged_arrive(unsigned long long *w, unsigned tag, unsigned n) {
+  const unsigned long long hi = (unsigned long long)tag << 32;
+  unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(w);
+  for (;;) {
+    const unsigned long long nv = ((cur & 0xffffffff00000000ull) == hi) ? cur + 1 : (hi | 1ull);
+    const unsigned long long prev = atomicCAS(w, cur, nv);
+    if (prev == cur) {
+      if ((unsigned)nv != n) return false;
+      atomicExch(w, 0ull);
+      return true;
+    }
+    cur = prev;
+  }
+}
+// Grid-wide barrier of a co-resident grid over words b[0..2] of uninitialized workspace.
+// Arrivals count with atomicAdd (a CAS per arrival serializes a whole grid behind one address):
+// CTA 0 first claims b[0] (arrivals) and b[2] (departures) for its tag -- grid_claim, after its
+// griddep() wait, so the previous launch is done with them; an arrival that lands before the
+// claim (seen as a foreign tag; the claim overwrites it) waits for the claim and arrives again.
+// The last arrival resets b[0] and publishes the tag in b[1]; the others poll b[1].
+// grid_depart (once the CTA no longer needs the barrier): the last CTA out clears b[1], so the
+// next launch -- or graph replay of this one -- waits again.  Bounded: a grid that is not
+// co-resident traps (cudaErrorLaunchFailure) instead of hanging the GPU.
+__device__ __forceinline__ void grid_claim(unsigned long long *b, unsigned tag) {
+  const unsigned long long mine = (unsigned long long)tag << 32;
+  for (int i = 0; i < 3; i += 2) {
+    unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(b + i);
+    while ((cur & 0xffffffff00000000ull) != mine) {
+      const unsigned long long prev = atomicCAS(b + i, cur, mine);
+      if (prev == cur) break;
+      cur = prev;
+    }
+  }
+}
+__device__ __forceinline__ bool counted_arrive(unsigned long long *w, unsigned tag, unsigned n) {
+  const long long t0 = clock64();
+  for (;;) {
+    const unsigned long long old = atomicAdd(w, 1ull);
+    if ((unsigned)(old >> 32) == tag) {
+      if ((unsigned)old + 1u != n) return false;
+      atomicExch(w, 0ull);
+      return true;
+    }
+    while ((unsigned)(*reinterpret_cast<volatile unsigned long long *>(w) >> 32) != tag) {
+      __nanosleep(64);
+      if (clock64() - t0 > 20000000000LL) __trap();
+    }
+  }
+}
+__device__ __forceinline__ void grid_barrier(unsigned long long *b, unsigned tag, unsigned n) {
+  if (counted_arrive(b, tag, n)) {
+    __threadfence();
+    atomicExch(b + 1, (unsigned long long)tag);
+    return;
+  }
+  const volatile unsigned long long *rel = b + 1;
+  const long long t0 = clock64();
+  while (*rel != (unsigned long long)tag) {
+    __nanosleep(64);
+    if (clock64() - t0 > 20000000000LL) __trap();
+  }
+  __threadfence();
+}
+__device__ __forceinline__ void grid_depart(unsigned long long *b, unsigned tag, unsigned n) {
+  if (counted_arrive(b + 2, tag, n)) atomicExch(b + 1, 0ull);
 }
 
 }  // namespace cpk

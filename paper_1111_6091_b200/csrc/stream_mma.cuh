@@ -126,6 +126,87 @@ __device__ __forceinline__ void yl_complete_segment(const StreamPlan &p, int64_t
   (void)scratch;
 }
 
+// cp_mttkrp in one launch, modes >= 1 (StreamPlan::Mout): once the CTA has stored the R-vector
+// partials of all its segments [s0, s1], it takes a tagged ticket per segment (contributors:
+// the CTAs (c, rb), c in [clo, chi]); for every segment where it is the last contributor it sums
+// the partials in reduce_entry_part's order (c ascending, then rb) and writes row s of M (one
+// warp per segment, lane = rank).  Once per CTA, after the streaming loop: no ticket round trip
+// stalls the pipeline.  Called by all consumer threads.
+__device__ __forceinline__ void mttkrp_complete_segments(const StreamPlan &p, int64_t v0, int64_t v1) {
+  __shared__ int s_last[32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t s0 = v0 / p.Qn, s1 = (v1 - 1) / p.Qn;
+  __threadfence();  // the partials' stores before the tickets
+  named_bar_sync(1, kConsumers);
+  for (int64_t sb = s0; sb <= s1; sb += 32) {
+    if (tid < 32) {
+      const int64_t s = sb + tid;
+      int last = 0;
+      if (s <= s1) {
+        const int64_t clo = ((s * p.Qn + 1) * p.Gc - 1) / p.Q;
+        const int64_t chi = (((s + 1) * p.Qn) * p.Gc - 1) / p.Q;
+        last = tagged_arrive(p.tick + s, p.tag, (unsigned)((chi - clo + 1) * p.RB)) ? 1 : 0;
+      }
+      s_last[tid] = last;
+    }
+    named_bar_sync(1, kConsumers);
+    for (int j = warp; j < 32; j += kConsumerWarps) {
+      if (!s_last[j] || lane >= p.R) continue;
+      __threadfence();
+      const int64_t s = sb + j;
+      const int64_t clo = ((s * p.Qn + 1) * p.Gc - 1) / p.Q;
+      const int64_t chi = (((s + 1) * p.Qn) * p.Gc - 1) / p.Q;
+      double sum = 0.0;
+      for (int64_t c = clo; c <= chi; ++c) {
+        const int64_t sf = ((c * p.Q) / p.Gc) / p.Qn;
+        for (int rb = 0; rb < p.RB; ++rb)
+          sum += __ldcg(p.part + ((c * p.RB + rb) * p.slots + (s - sf)) * p.R + lane);
+      }
+      p.Mout[s + p.In * lane] = sum;
+    }
+    named_bar_sync(1, kConsumers);
+  }
+}
+
+// sum of n values at stride, 8 independent accumulators combined in a fixed tree (the order of
+// small_kernels.cu sum_strided), L2 loads (the values were written by this launch)
+__device__ __forceinline__ double sum_strided_cg(const double *q, int64_t stride, int n) {
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int c = 0;
+  for (; c + 8 <= n; c += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j] += __ldcg(q + (int64_t)(c + j) * stride);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (c + j < n) s[j] += __ldcg(q + (int64_t)(c + j) * stride);
+  return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+}
+
+// cp_mttkrp in one launch, mode 0 (StreamPlan::Mout): after the grid barrier every CTA forms the
+// entries e in [S b / G, S (b + 1) / G) of M (S = I1 R, column-major like the partials), each as
+// 32 chunk sums over the column groups combined in chunk order (reduce_mode0_kernel's order).
+// Called by all consumer threads; scratch: 8 x 33 doubles of shared memory.
+__device__ __forceinline__ void mttkrp_mode0_slice(const StreamPlan &p, double *scratch) {
+  const int tid = threadIdx.x;
+  const int64_t S = p.I1 * p.R, G = gridDim.x;
+  const int64_t e0 = S * blockIdx.x / G, e1 = S * (blockIdx.x + 1) / G;
+  const int ly = tid & 31, j = tid >> 5;  // chunk ly of entry e0 + 8 k + j
+  const int c0 = (p.Gc * ly) / 32, c1 = (p.Gc * (ly + 1)) / 32;
+  for (int64_t eb = e0; eb < e1; eb += 8) {
+    const int64_t e = eb + j;
+    scratch[j * 33 + ly] = (e < e1) ? sum_strided_cg(p.part + (int64_t)c0 * S + e, S, c1 - c0) : 0.0;
+    named_bar_sync(1, kConsumers);
+    if (tid < 8 && eb + tid < e1) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) t += scratch[tid * 33 + k];
+      p.Mout[eb + tid] = t;
+    }
+    named_bar_sync(1, kConsumers);
+  }
+}
+
 #ifdef CP_CTA_TIMELINE
 __device__ __forceinline__ unsigned long long cta_gtimer() {
   unsigned long long t;
@@ -180,6 +261,8 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   CTL_BEGIN
   griddep();  // (PDL) predecessor's At / factor writes visible from here on
   CTL_AFTER_WAIT
+  // one-launch cp_mttkrp, mode 0: CTA 0 claims the grid barrier's words for this launch
+  if (OP == OP_MTTKRP && p.mode == 0 && p.Mout != nullptr && blockIdx.x == 0 && tid == 0) grid_claim(p.tick, p.tag);
 
   if (warp == kConsumerWarps) {
     produce<8, 2>(p, lane, v0, v1, row0, Wb, sm);  // (template args only select the TMA path)
@@ -452,6 +535,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #ifdef CP_CTA_TIMELINE
   tl_loop = cta_gtimer();
 #endif
+  if (OP == OP_MTTKRP && p.mode != 0 && p.Mout != nullptr) mttkrp_complete_segments(p, v0, v1);
 
   if (OP == OP_RESID) {
     // ---- this CTA's sum of (z - x)^2: lanes, then warps in order ----
@@ -483,6 +567,15 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
           }
         }
       }
+    }
+    if (p.Mout != nullptr) {
+      // one launch: every CTA's partial stored -> grid barrier -> this CTA's slice of M
+      __threadfence();
+      named_bar_sync(1, kConsumers);
+      if (tid == 0) grid_barrier(p.tick, p.tag, gridDim.x);
+      named_bar_sync(1, kConsumers);
+      mttkrp_mode0_slice(p, sm.zbuf);
+      if (tid == 0) grid_depart(p.tick, p.tag, gridDim.x);
     }
   }
 #ifdef CP_CTA_TIMELINE_STREAM

@@ -1,5 +1,7 @@
-"""cp_mttkrp device times per mode (L2 flushed before each rep), gather path vs prep path
-(CP_MTTKRP_FCM=1/0).  python tools/mttkrp_ab.py c3 [reps]"""
+"""cp_mttkrp device times per mode under environment variants, one process, same box (L2 flushed
+before each rep when Z fits in 2x L2, else back-to-back calls).
+    python tools/mttkrp_ab.py c3 "CP_MTTKRP_FUSED=0" "CP_MTTKRP_FUSED=1,CP_MTTKRP_FCM=2" ...
+(path selectors, include/cp.h; reps via MTTKRP_AB_REPS)"""
 import os
 import sys
 
@@ -12,7 +14,8 @@ import paper_1111_6091_b200 as cp  # noqa: E402
 from paper_1111_6091_b200 import colmajor, empty_factor  # noqa: E402
 
 name = sys.argv[1]
-reps = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+variants = sys.argv[2:] or ["-"]
+reps = int(os.environ.get("MTTKRP_AB_REPS", "30"))
 _, dims, R, *_ = cpsynth.CONFIGS[name]
 P = int(np.prod(dims))
 Z = torch.randn(tuple(reversed(dims)), dtype=torch.float64, device="cuda")
@@ -35,8 +38,7 @@ def timed(fn):
         return e0.elapsed_time(e1) / reps * 1e3
     tot = 0.0
     for _ in range(reps):
-        if flush:
-            fl.zero_()
+        fl.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         fn()
@@ -46,18 +48,27 @@ def timed(fn):
     return tot / reps * 1e3
 
 
-res = {}
-for g in ("1", "0"):
-    os.environ["CP_MTTKRP_FCM"] = g
+ref = None
+for v in variants:
+    saved = {}
+    for kv in v.split(","):
+        if "=" in kv:
+            k, val = kv.split("=")
+            saved[k] = os.environ.get(k)
+            os.environ[k] = val
+    line = []
+    outs = []
     for n in range(len(dims)):
         us = timed(lambda: cp.mttkrp(Z, dims, A, n, M=M[n], ws=ws))
         alg = 8.0 * (P + sum(dims[k] * R for k in range(len(dims)) if k != n) + dims[n] * R)
-        res[(g, n)] = (us, alg / us / 1e3, cp.last_launch_count())
-for n in range(len(dims)):
-    print(f"{name} mode {n}: fcm {res[('1', n)][0]:.1f} us ({res[('1', n)][1]:.0f} GB/s, {res[('1', n)][2]} launches)"
-          f" | prep {res[('0', n)][0]:.1f} us ({res[('0', n)][1]:.0f} GB/s, {res[('0', n)][2]} launches)")
-os.environ["CP_MTTKRP_FCM"] = "1"
-Mg = [cp.mttkrp(Z, dims, A, n).clone() for n in range(len(dims))]
-os.environ["CP_MTTKRP_FCM"] = "0"
-Mp = [cp.mttkrp(Z, dims, A, n).clone() for n in range(len(dims))]
-print("max rel diff fcm vs prep:", max(float((a - b).norm() / b.norm()) for a, b in zip(Mg, Mp)))
+        line.append(f"m{n} {us:6.1f} us {alg / us / 1e3:5.0f} GB/s {cp.last_launch_count()}L")
+        outs.append(M[n].clone())
+    if ref is None:
+        ref = outs
+    d = max(float((a - b).norm() / b.norm()) for a, b in zip(outs, ref))
+    print(f"{name} {v:40s} " + " | ".join(line) + f" | rel diff vs first {d:.1e}", flush=True)
+    for k, old in saved.items():
+        if old is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = old
