@@ -74,7 +74,7 @@ static int parse_env(const char *name, int dflt) {
 }
 
 int path_flag(const char *name, int dflt) {
-  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MTTKRP_FUSED", "CP_MODEPROD_PIPE",
+  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MTTKRP_FUSED", "CP_MODEPROD_PIPE", "CP_SWEEP_TAIL",
                                        "CP_SWEEP_TREE", "CP_YLSOLVE", "CP_MODEPROD_DMMA", "CP_MG_GRAPH",
                                        "CP_ALS_GRAPH", "CP_MG_STRUCTURED", "CP_PDL"};
   for (const char *k : kPaths)
@@ -565,6 +565,10 @@ struct Layout {
   int rpc2, sp2, nyr;
   size_t yl, edge, mbuf, yr, segtab, m0part, linv;
   size_t tick;  // tagged completion words (StreamPlan::tick): 3 + max I_n
+  size_t rowdot;  // TailSolve: per-row <M,A>, <F,A> of the last mode (2 x max I_n)
+  size_t tailtick;  // TailSolve: u32 words (max I_n segment tickets, grid ticket, Gamma-job flag),
+                    // right after segtab: the prep kernel zeroes both in one range
+  int64_t maxI;
   size_t ntmp;  // cp_als_sweeps with CP_SWEEPS_NORMALIZE: normalization scratch (sum_n I_n R)
 };
 
@@ -658,8 +662,11 @@ static bool make_layout(Layout &L, const cp_shape &s) {
     L.linv = off; off = align_up(off + (size_t)s.N * R * R);  // L^{-1} of every Gamma^(n)
     L.yr = off; off = align_up(off + (size_t)L.s3.dims[2] * R);
     L.segtab = off; off = align_up(off + (size_t)(s.dims[1] * y.RB + 1) / 2);  // u32 ticket per (segment, row block)
+    L.tailtick = off; off = align_up(off + (size_t)(maxI + 2 + 1) / 2);
   }
   L.tick = off; off = align_up(off + 3 + (size_t)maxI);
+  L.rowdot = off; off = align_up(off + 2 * (size_t)maxI);
+  L.maxI = maxI;
   {
     size_t sumIR = 0;
     for (int k = 0; k < s.N; ++k) sumIR += (size_t)s.dims[k] * R;
@@ -873,7 +880,8 @@ static bool use_small_sweep(const cp_shape &s) {
 
 static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
                       const double *const *F, double *out, void *ws, size_t ws_bytes, cp_stream_t stream,
-                      bool first, bool steady);
+                      bool first, bool steady, bool defer_ok = false, bool prev_deferred = false,
+                      bool *deferred = nullptr);
 
 int cp_als_sweep(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
                  const double *const *F, double *out, void *ws, size_t ws_bytes,
@@ -904,10 +912,16 @@ int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, doub
     return CP_OK;
   }
   int total = 0;
+  bool deferred = false;
   for (int k = 0; k < nsweeps; ++k) {
     // sweeps k >= 1 without normalization in between run steady-state: the previous sweep's
-    // solves left every At copy and Gram total current, so no prep launch
-    if ((st = sweep_impl(s, Z, normZ2, A, F, out, ws, ws_bytes, stream, k == 0, k > 0 && !norm))) return st;
+    // solves left every At copy and Gram total current, so no prep launch; a sweep that is not the
+    // call's last may solve its last mode inside the pass and leave Upsilon^(N-1) to the next
+    // sweep's Gamma^(0) job (TailSolve; its f is not needed: the call returns the last sweep's)
+    const bool prev = deferred;
+    if ((st = sweep_impl(s, Z, normZ2, A, F, out, ws, ws_bytes, stream, k == 0, k > 0 && !norm,
+                         k + 1 < nsweeps && !norm, prev, &deferred)))
+      return st;
     total += g_launches;
     if (norm) {  // cp_normalize_sort(sort = 0) with the sweep workspace's own scratch region
       NormArgs na;
@@ -937,10 +951,13 @@ int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, doub
 // wrote the row-major copies At and the Gram totals Ups of every mode -- the prep launch (At
 // copies + partial Grams) is skipped and every Gram of a not-yet-updated factor is read as a total
 // (bitwise the same as the previous sweep's totals; the tickets were reset by their last users).
+// defer_ok: another steady sweep of the same call follows; prev_deferred: the previous sweep left
+// Upsilon^(2) to this sweep's Gamma^(0) job; *deferred: this sweep did so.
 static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, double *const *A,
                       const double *const *F, double *out, void *ws, size_t ws_bytes, cp_stream_t stream,
-                      bool first, bool steady) {
+                      bool first, bool steady, bool defer_ok, bool prev_deferred, bool *deferred) {
   g_launches = 0;
+  if (deferred != nullptr) *deferred = false;
   int st;
   const auto Lp = get_layout(*s);
   if (!Lp) return CP_EINVAL;
@@ -954,9 +971,12 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
   fill_prep(*s, L, w, (const double *const *)A, -1, true, w + L.status, pa, pg);
   pa.keep_status = first ? 0 : 1;
   const bool yl_inline = L.tree && L.yl_plan.mma && knob("CP_YL_INLINE_FIX", 1);
-  if (yl_inline) {  // Y_L segment tickets (stream_mma.cuh yl_complete_segment)
-    pa.zero = reinterpret_cast<unsigned *>(w + L.segtab);
-    pa.nzero = (int)(s->dims[1] * L.yl_plan.RB);
+  if (L.tree) {
+    // u32 completion words zeroed by prep: the Y_L segment tickets (stream_mma.cuh
+    // yl_complete_segment) and, contiguous after them, the tail solve's words (sweep_tail)
+    const size_t z0 = yl_inline ? L.segtab : L.tailtick;
+    pa.zero = reinterpret_cast<unsigned *>(w + z0);
+    pa.nzero = (int)((L.tailtick - z0) * 2 + (size_t)L.maxI + 2);
   }
   // experiments only (-DCP_EXPERIMENTS builds): CP_SWEEP_SKIP bitmask drops launches (timing of
   // the rest; results wrong).  Always 0 in the shipped library.
@@ -1050,6 +1070,13 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
     g.ups = w + L.Ups;
     g.linv = w + L.linv + (size_t)n * RR;
     g.status = w + L.status;
+    if (n == 0 && prev_deferred) {
+      // the previous sweep's in-pass tail solve wrote the rows of At^(2) only
+      g.gram_mode = 2;
+      g.gram_RS = RS;
+      g.gram_rows = s->dims[2];
+      g.gram_At = w + L.At[2];
+    }
     return g;
   };
   if (L.tree) {
@@ -1160,9 +1187,45 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
     // Gamma^(2) rides in the pass's idle weight warp
     const bool job2 = jobs && p2.mma && p2.direct_w;
     if (job2) p2.gj = gamma_job(2);
+    // N = 3: the mode-2 solve and the finalize run inside the pass (TailSolve, stream_mma.cuh
+    // sweep_tail) -- no solve launch
+    // sweep_tail) -- no solve launch.  CP_SWEEP_TAIL = 1 (default): only sweeps followed by another
+    // steady sweep of the same call, with Upsilon^(2) and f left out (fin = 0: the next sweep's
+    // Gamma^(0) job forms the Gram off the critical path; measured per steady sweep: c4a 421.5 ->
+    // 419.0 us, c3 80.7 -> 75.9, c2 50.5 -> 46.9, c1 45.0 -> 41.0, tools/tail_ab.sh);
+    // 2: every sweep (fin = 1 on a call's last sweep: measured 2-5 us slower than the solve launch it
+    // replaces -- the last CTA's Gram and sums are a chain of L2 round trips -- so not the default).
+    const int tail_sel = path_flag("CP_SWEEP_TAIL", 1);
+    const bool defer = defer_ok && deferred != nullptr && jobs && L.yl_plan.mma && L.yl_plan.direct_w;
+    const bool tail = N == 3 && job2 && R <= 32 && p2.slots <= 32 && (tail_sel >= 2 || (tail_sel == 1 && defer)) &&
+                      (int64_t)p2.nstages * p2.zst >= sweep_tail_doubles(R);
+    if (tail) {
+      TailSolve &t = p2.tail;
+      t.on = 1;
+      t.fin = defer ? 0 : 1;
+      if (defer && deferred != nullptr) *deferred = true;
+      t.dot_stride = L.gp_max;
+      t.nsolve[0] = grid_of[0];
+      t.nsolve[1] = grid_of[1];
+      t.linv = w + L.linv + (size_t)2 * RR;
+      t.F = (F != nullptr) ? F[2] : nullptr;
+      t.A = A[2];
+      t.At = w + L.At[2];
+      t.rowdot = w + L.rowdot;
+      t.dotF = w + L.dotF;
+      t.Ups = w + L.Ups;
+      t.normZ2 = normZ2;
+      t.status = w + L.status;
+      t.out = out;
+      t.segtick = reinterpret_cast<unsigned *>(w + L.tailtick);
+      t.gtick = t.segtick + L.maxI;
+      t.gjflag = t.segtick + L.maxI + 1;
+    }
     if (!(skip & 256) && launch_stream(p2, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
-    if (N == 3) {
+    if (tail) {
+      // (solved and finalized by the pass)
+    } else if (N == 3) {
       if (!solve_mode(2, reduce_geom(p2), L.rpc2, L.sp2, job2 ? w + L.linv + (size_t)2 * RR : nullptr))
         return CP_ECUDA;
     } else {
@@ -1262,9 +1325,12 @@ static int fit_impl(const cp_shape *s, const double *Z, const double *normZ2, co
   PrepGrams pg;
   fill_prep(*s, L, w, A, -1, true, nullptr, pa, pg);
   const bool yl_inline = L.tree && L.yl_plan.mma && knob("CP_YL_INLINE_FIX", 1);
-  if (yl_inline) {  // Y_L segment tickets (stream_mma.cuh yl_complete_segment)
-    pa.zero = reinterpret_cast<unsigned *>(w + L.segtab);
-    pa.nzero = (int)(s->dims[1] * L.yl_plan.RB);
+  if (L.tree) {
+    // u32 completion words zeroed by prep: the Y_L segment tickets (stream_mma.cuh
+    // yl_complete_segment) and, contiguous after them, the tail solve's words (sweep_tail)
+    const size_t z0 = yl_inline ? L.segtab : L.tailtick;
+    pa.zero = reinterpret_cast<unsigned *>(w + z0);
+    pa.nzero = (int)((L.tailtick - z0) * 2 + (size_t)L.maxI + 2);
   }
   // experiments only (-DCP_EXPERIMENTS builds): CP_SWEEP_SKIP bitmask drops launches (timing of
   // the rest; results wrong).  Always 0 in the shipped library.

@@ -27,12 +27,52 @@ enum StreamOp { OP_MTTKRP = 0, OP_RESID = 1, OP_YL = 2 };
 // Gamma^(mode) factorization job (gamma_job.cuh): Upsilon^(k) for k != mode is the sum of cnt[k]
 // R x R partials at src[k] (stride R*R, summed in order, total written to ups[k]) or, cnt[k] = 0,
 // the total at src[k]; out: L^{-1} (R x R row-major) in linv; CP_ENOTSPD + mode in status.
+// gram_rows > 0 (stream_mma.cuh gram_rows_warp, before the job): Upsilon^(gram_mode) is first
+// formed from the gram_rows rows of the row-major factor copy gram_At (row stride gram_RS) and
+// written to ups -- the Gram the previous sweep's in-pass tail solve deferred (TailSolve::fin = 0).
 struct GammaJob {
   int on, N, R, mode;
   const double *src[CP_MAX_N];
   int cnt[CP_MAX_N];
   double *ups, *linv, *status;
+  int gram_mode, gram_RS;
+  int64_t gram_rows;
+  const double *gram_At;
 };
+
+// The sweep's last solve inside the last streaming pass (N = 3 dimension-tree sweep, MMA plans;
+// stream_mma.cuh sweep_tail): the last contributor of each segment i_2 (tagged ticket) sums the
+// segment's partials into row i_2 of M^(2), solves x = L^{-T}(L^{-1}(m + f)) in one warp
+// (lane = component; eq:relaxinnersolve, reading R1) and writes the row of A^(2), At^(2) and the
+// row's <M,A>, <F,A>; the last CTA of the grid (ticket gtick) forms Upsilon^(2) over all rows in
+// a fixed order and f, f~ (readings R5, R6).  L^{-1} comes from this launch's Gamma job (CTA 0's
+// weight warp), published through the flag gjflag.  No solve launch follows.
+struct TailSolve {
+  int on;
+  int fin;                 // 1: the last CTA forms Upsilon^(2) and f, f~ (the call's last sweep);
+                           // 0: rows only -- the next sweep's Gamma^(0) job forms Upsilon^(2)
+                           // (GammaJob::gram_rows) and this sweep's f is not evaluated
+  int dot_stride;          // stride between the modes' <F,A> partial arrays
+  int nsolve[2];           // <F,A> partials of modes 0, 1 (their solves' grid sizes)
+  const double *linv;      // L^{-1} of Gamma^(2), R x R row-major (Gamma job of this launch)
+  const double *F;         // F^(2) or null
+  double *A, *At;          // A^(2) column-major; row-major copy (stride RS)
+  double *rowdot;          // workspace: per row <M,A> [0, In) and <F,A> [In, 2 In)
+  const double *dotF;      // <F,A> partials of the earlier modes
+  double *Ups;             // N x R x R Gram totals
+  const double *normZ2;
+  double *status, *out;
+  // u32 completion words, zeroed by the prep kernel and reset by their last users: one ticket
+  // per segment i_2, the grid ticket, the Gamma job's "done" flag
+  unsigned *segtick, *gtick, *gjflag;
+};
+
+// doubles of shared memory sweep_tail needs: L^{-1}, the block sums, and (after them) one
+// (8 NT)^2 Gram tile per consumer warp
+__host__ __device__ constexpr int sweep_tail_fixed_doubles(int R) { return R * (R + 1) + 24; }
+__host__ __device__ constexpr int sweep_tail_doubles(int R) {
+  return sweep_tail_fixed_doubles(R) + kConsumerWarps * (8 * ((R + 7) / 8)) * (8 * ((R + 7) / 8));
+}
 
 // Plan of one streaming pass over Z (MTTKRP of one mode, or the residual pass of cp_fit).
 // Z is viewed as an I1 x Q column-major matrix (Q = P / I1 "columns" = mode-1 fibers).
@@ -106,6 +146,7 @@ struct StreamPlan {
   double *Mout;
   unsigned long long *tick;
   unsigned tag;
+  TailSolve tail;   // the sweep's last solve + finalize inside this pass (see TailSolve)
   alignas(64) CUtensorMap tmap;
   alignas(64) CUtensorMap fmap[kMaxDigits];
 };

@@ -21,6 +21,9 @@
 //    mode >= 1 -- C contracted with the A^(1) rows, reduced over lanes and warps in a fixed
 //    order into one R-vector per (CTA, segment); mode 0 -- the CTA's I1 x R partial.
 #pragma once
+#ifdef CP_TAIL_TIMING
+#include <cstdio>
+#endif
 #include "gamma_job.cuh"
 #include "stream_kernel.cuh"
 
@@ -168,6 +171,308 @@ __device__ __forceinline__ void mttkrp_complete_segments(const StreamPlan &p, in
   }
 }
 
+// Sums of three values over the 256 consumer threads (warp xor trees, then the 8 warp sums in a
+// fixed order; sred: 24 doubles).  Every consumer calls it; all of them get the sums.
+__device__ __forceinline__ void consumer_sum3(double &a, double &b, double &c, double *sred) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, off);
+    b += __shfl_xor_sync(0xffffffffu, b, off);
+    c += __shfl_xor_sync(0xffffffffu, c, off);
+  }
+  named_bar_sync(1, kConsumers);
+  if (lane == 0) {
+    sred[w] = a;
+    sred[8 + w] = b;
+    sred[16 + w] = c;
+  }
+  named_bar_sync(1, kConsumers);
+  a = ((sred[0] + sred[1]) + (sred[2] + sred[3])) + ((sred[4] + sred[5]) + (sred[6] + sred[7]));
+  b = ((sred[8] + sred[9]) + (sred[10] + sred[11])) + ((sred[12] + sred[13]) + (sred[14] + sred[15]));
+  c = ((sred[16] + sred[17]) + (sred[18] + sred[19])) + ((sred[20] + sred[21]) + (sred[22] + sred[23]));
+}
+
+// C(8 i + m, 8 j + n) += sum_k X(k, 8 i + m) X(k, 8 j + n) over rows k in [r0, r1) of the row-major
+// X (stride RS, columns < R): one DMMA per (i, j) and 4 rows; lane (gq, tq) holds X(k0 + tq, 8 i + gq)
+// -- both the A and the B fragment.  L2 loads (the rows may have been written by this launch).
+template <int NT>
+__device__ __forceinline__ void gram_rows_dmma(double (&c)[NT][NT][2], const double *X, int RS, int R, int64_t r0,
+                                               int64_t r1, int lane) {
+  const int gq = lane >> 2, tq = lane & 3;
+  constexpr int KB = (NT <= 2) ? 8 : 4;  // k-steps loaded per batch
+  for (int64_t k0 = r0; k0 < r1; k0 += 4 * KB) {
+    double xf[KB][NT];
+#pragma unroll
+    for (int u = 0; u < KB; ++u) {
+      const int64_t row = k0 + 4 * u + tq;
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        const int col = 8 * i + gq;
+        xf[u][i] = (row < r1 && col < R) ? __ldcg(X + row * RS + col) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < KB; ++u)
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma_8x8x4(c[i][j][0], c[i][j][1], xf[u][i], xf[u][j]);
+  }
+}
+
+// The Gram a tail solve deferred (GammaJob::gram_rows): one warp (the idle weight warp of CTA 0)
+// forms Upsilon^(gram_mode) over all rows in row order and writes the total to ups.
+template <int NT>
+__device__ __noinline__ void gram_rows_warp(const GammaJob &g, int lane) {
+  if (g.status[0] != 0.0) return;
+  const int gq = lane >> 2, tq = lane & 3, R = g.R;
+  double c[NT][NT][2];
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+  gram_rows_dmma<NT>(c, g.gram_At, g.gram_RS, R, 0, g.gram_rows, lane);
+  double *u = g.ups + (int64_t)g.gram_mode * R * R;
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int r = 8 * i + gq, q = 8 * j + 2 * tq;
+      if (r < R && q < R) u[q * R + r] = c[i][j][0];
+      if (r < R && q + 1 < R) u[(q + 1) * R + r] = c[i][j][1];
+    }
+  __syncwarp();
+}
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// The sweep's last solve + finalize inside the mode-2 pass (TailSolve, cp_internal.cuh): called
+// by all consumer threads after the streaming loop; scr = the Z ring, which every consumer is
+// done with.  The chain after the last stage is a handful of L2 round trips:
+//  1. warp 0 takes the segments' tickets (u32 counters zeroed by prep and reset by their last
+//     arrival) while the other warps acquire the Gamma job's flag (CTA 0's weight warp set it at
+//     the start of the pass) and stage L^{-1};
+//  2. per segment s where this CTA arrived last: one warp sums the partials (reduce_entry_part's
+//     order), b = m + f, y = L^{-1} b, x = L^{-T} y with the lane's row / column of L^{-1} and one
+//     shuffle per term (the term order of solve_kernel_t: the same x bitwise), stores the row of
+//     A^(2), At^(2) and the row's <M,A>, <F,A>;
+//  3. grid ticket: the last CTA forms Upsilon^(2) = At^T At on the tensor cores straight from L2
+//     (warp w: rows [w, w + 1) In / 8 in k-steps of 4, A and B fragments are the same values; the
+//     warps' tiles summed in warp order), sums the row dots and the earlier modes' <F,A>
+//     partials in a fixed order and writes f, f~, status.  Which CTA runs a step varies from run
+//     to run; what it computes does not.
+template <int NT>
+__device__ __noinline__ void sweep_tail(const StreamPlan &p, int64_t v0, int64_t v1, double *scr) {
+  __shared__ int s_last[32], s_clo[32], s_nc[32];
+  __shared__ int s_fin, s_live;
+  const TailSolve &t = p.tail;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int R = p.R, RR = R * R, LS = R + 1, RS = p.RS;
+  constexpr int RP = 8 * NT;
+  const int64_t In = p.In;
+  const int64_t s0 = v0 / p.Qn, s1 = (v1 - 1) / p.Qn;  // host: s1 - s0 < 32 (slots <= 32)
+  double *sLi = scr, *sred = scr + R * LS, *tiles = scr + sweep_tail_fixed_doubles(R);
+#ifdef CP_TAIL_TIMING
+  unsigned long long tt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define TAIL_T(k) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[k])); }
+#else
+#define TAIL_T(k)
+#endif
+  TAIL_T(0)
+  __threadfence();  // the partials' stores before the tickets
+  named_bar_sync(1, kConsumers);
+  TAIL_T(1)
+  if (warp == 0) {
+    const int64_t s = s0 + lane;
+    int last = 0;
+    if (s <= s1) {
+      const int64_t clo = ((s * p.Qn + 1) * p.Gc - 1) / p.Q;
+      const int64_t chi = (((s + 1) * p.Qn) * p.Gc - 1) / p.Q;
+      const unsigned n = (unsigned)((chi - clo + 1) * p.RB);
+      s_clo[lane] = (int)clo;
+      s_nc[lane] = (int)(chi - clo + 1);
+      if (atomicAdd(t.segtick + s, 1u) == n - 1) {
+        t.segtick[s] = 0u;
+        last = 1;
+      }
+    }
+    s_last[lane] = last;
+    // (acquire for the whole CTA: this fence, then the barrier, order the other contributors'
+    // partials before every consumer's L2 loads below)
+    __threadfence();
+  } else {
+    const long long t0 = clock64();
+    while (ld_acquire_u32(t.gjflag) != 1u) {
+      if (clock64() - t0 > 20000000000LL) __trap();
+    }
+    if (tid == 32) s_live = (__ldcg(t.status) == 0.0) ? 1 : 0;
+    for (int e = tid - 32; e < RR; e += kConsumers - 32) sLi[(e / R) * LS + (e % R)] = __ldcg(t.linv + e);
+  }
+  named_bar_sync(1, kConsumers);
+  TAIL_T(2)
+  const bool live = s_live != 0;
+  for (int j = warp; j < 32; j += kConsumerWarps) {
+    if (!s_last[j] || !live) continue;
+    const int64_t s = s0 + j;
+    const int clo = s_clo[j], nc = s_nc[j];
+    const bool on = lane < R;
+    const int lr = on ? lane : 0;
+    // contributor c's slot of segment s: 32 contributors' offsets formed lane-parallel, then one
+    // shuffle each (c ascending, then rb: reduce_entry_part's order)
+    const double f = (t.F != nullptr) ? __ldg(t.F + s + In * lr) : 0.0;
+    double m = 0.0;
+    for (int cb = 0; cb < nc; cb += 32) {
+      int64_t myoff = 0;
+      if (cb + lane < nc) {
+        const int64_t c = clo + cb + lane;
+        const int64_t sf = ((c * p.Q) / p.Gc) / p.Qn;
+        myoff = ((c * p.RB) * p.slots + (s - sf)) * R;
+      }
+      const int ncb = (nc - cb) < 32 ? (nc - cb) : 32;
+      for (int cc = 0; cc < ncb; ++cc) {
+        const int64_t off = __shfl_sync(0xffffffffu, myoff, cc);
+        for (int rb = 0; rb < p.RB; ++rb) m += __ldcg(p.part + off + (int64_t)rb * p.slots * R + lr);
+      }
+    }
+    const double b = m + f;
+    // y = L^{-1} b, x = L^{-T} y: lane r walks row r / column r of L^{-1}; every term's shuffle
+    // and shared-memory load is independent of the fma chain (unrolled by 8: in flight together)
+    double y = 0.0, x = 0.0;
+    const double *lrow = sLi + lr * LS, *lcol = sLi + lr;
+#pragma unroll
+    for (int k8 = 0; k8 < RP; k8 += 8) {
+      if (k8 < R) {
+        double l8[8], b8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = k8 + u;
+          l8[u] = (k <= lr && k < R) ? lrow[k] : 0.0;
+          b8[u] = __shfl_sync(0xffffffffu, b, k & 31);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (k8 + u <= lr && k8 + u < R) y = fma(l8[u], b8[u], y);
+      }
+    }
+#pragma unroll
+    for (int k8 = 0; k8 < RP; k8 += 8) {
+      if (k8 < R) {
+        double l8[8], y8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = k8 + u;
+          l8[u] = (k >= lr && k < R) ? lcol[k * LS] : 0.0;
+          y8[u] = __shfl_sync(0xffffffffu, y, k & 31);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (k8 + u >= lr && k8 + u < R) x = fma(l8[u], y8[u], x);
+      }
+    }
+    if (on) {
+      t.A[s + In * lane] = x;
+      t.At[s * RS + lane] = x;
+    }
+    double dm = on ? m * x : 0.0, df = on ? f * x : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      dm += __shfl_xor_sync(0xffffffffu, dm, off);
+      df += __shfl_xor_sync(0xffffffffu, df, off);
+    }
+    if (lane == 0) {
+      t.rowdot[s] = dm;
+      t.rowdot[In + s] = df;
+    }
+  }
+  // ---- grid ticket: the last CTA finalizes ----
+  TAIL_T(3)
+  __threadfence();
+  named_bar_sync(1, kConsumers);
+  if (tid == 0) s_fin = (atomicAdd(t.gtick, 1u) == gridDim.x - 1) ? 1 : 0;
+  named_bar_sync(1, kConsumers);
+  TAIL_T(4)
+#ifdef CP_TAIL_TIMING
+  if (tid == 0 && (blockIdx.x % 37 == 0) && !s_fin)
+    printf("TAIL cta %d: t0 %llu fence+bar %llu tick/flag %llu solve %llu gtick %llu\n", (int)blockIdx.x,
+           tt[0], tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3]);
+#endif
+  if (!s_fin) return;
+  __threadfence();
+  if (tid == 0) {  // every CTA is past its flag wait and its arrival: reset for the next launch
+    *t.gtick = 0u;
+    *t.gjflag = 0u;
+  }
+  if (!t.fin) return;  // (Upsilon^(2) is formed by the next sweep's Gamma^(0) job; no f this sweep)
+  const double st = __ldcg(t.status);
+  if (st != 0.0) {
+    if (tid == 0) {
+      t.out[0] = nan("");
+      t.out[1] = nan("");
+      t.out[2] = st;
+      t.out[3] = __ldcg(t.status + 1);
+    }
+    return;
+  }
+  // row dots and the earlier modes' <F,A> partials (loads in flight during the Gram)
+  double in = 0.0, fl = 0.0;
+  for (int64_t i = tid; i < In; i += kConsumers) {
+    in += __ldcg(t.rowdot + i);
+    fl += __ldcg(t.rowdot + In + i);
+  }
+  for (int n = 0; n < 2; ++n)
+    for (int c = tid; c < t.nsolve[n]; c += kConsumers) fl += __ldcg(t.dotF + (int64_t)n * t.dot_stride + c);
+  // Upsilon^(2) = At^T At on the tensor cores: warp w takes the rows [w, w + 1) rpw
+  {
+    const int gq = lane >> 2, tq = lane & 3;
+    const int64_t rpw = (((In + kConsumerWarps - 1) / kConsumerWarps) + 3) & ~(int64_t)3;
+    const int64_t r0 = warp * rpw, r1 = (r0 + rpw < In) ? r0 + rpw : In;
+    double c[NT][NT][2];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+    gram_rows_dmma<NT>(c, t.At, RS, R, r0, r1, lane);
+    double *tw = tiles + (size_t)warp * RP * RP;
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        tw[(8 * i + gq) * RP + 8 * j + 2 * tq] = c[i][j][0];
+        tw[(8 * i + gq) * RP + 8 * j + 2 * tq + 1] = c[i][j][1];
+      }
+  }
+  TAIL_T(5)
+  named_bar_sync(1, kConsumers);
+  double m2 = 0.0;
+  for (int e = tid; e < RR; e += kConsumers) {
+    const int r = e % R, q = e / R;
+    double u = 0.0;
+#pragma unroll
+    for (int w8 = 0; w8 < kConsumerWarps; ++w8) u += tiles[(size_t)w8 * RP * RP + r * RP + q];
+    t.Ups[(int64_t)2 * RR + e] = u;
+    m2 = fma(u, __ldcg(t.Ups + e) * __ldcg(t.Ups + RR + e), m2);
+  }
+  consumer_sum3(m2, in, fl, sred);
+  if (tid == 0) {
+    const double f = 0.5 * t.normZ2[0] - in + 0.5 * m2;
+    t.out[0] = f;
+    t.out[1] = f - fl;
+    t.out[2] = 0.0;
+    t.out[3] = -1.0;
+  }
+#ifdef CP_TAIL_TIMING
+  TAIL_T(6)
+  if (tid == 0)
+    printf("TAIL final cta %d: t0 %llu fence+bar %llu tick/flag %llu solve %llu gtick %llu dots+gram %llu reduce+out %llu\n",
+           (int)blockIdx.x, tt[0], tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4], tt[6] - tt[5]);
+#endif
+}
+
 // sum of n values at stride, 8 independent accumulators combined in a fixed tree (the order of
 // small_kernels.cu sum_strided), L2 loads (the values were written by this launch)
 __device__ __forceinline__ double sum_strided_cg(const double *q, int64_t stride, int n) {
@@ -271,7 +576,16 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   if (warp == kConsumerWarps + 1) {
     // weight rows (returns at once when direct_w), then the optional Gamma job of CTA 0
     form_weights(p, lane, sm);
-    if (p.gj.on && blockIdx.x == 0) gamma_job_run(p.gj, sm.gjbuf, lane, 32, false);
+    if (p.gj.on && blockIdx.x == 0) {
+      if (p.gj.gram_rows > 0) gram_rows_warp<NT>(p.gj, lane);
+      gamma_job_run(p.gj, sm.gjbuf, lane, 32, false);
+    }
+    if (OP == OP_MTTKRP && p.tail.on && blockIdx.x == 0) {
+      // publish the job's L^{-1}, Gram totals and status to the tail solves of every CTA
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicExch(p.tail.gjflag, 1u);
+    }
     return;
   }
 
@@ -535,7 +849,8 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #ifdef CP_CTA_TIMELINE
   tl_loop = cta_gtimer();
 #endif
-  if (OP == OP_MTTKRP && p.mode != 0 && p.Mout != nullptr) mttkrp_complete_segments(p, v0, v1);
+  if (OP == OP_MTTKRP && p.mode != 0 && p.tail.on) sweep_tail<NT>(p, v0, v1, sm.zbuf);
+  else if (OP == OP_MTTKRP && p.mode != 0 && p.Mout != nullptr) mttkrp_complete_segments(p, v0, v1);
 
   if (OP == OP_RESID) {
     // ---- this CTA's sum of (z - x)^2: lanes, then warps in order ----

@@ -297,7 +297,9 @@ def test_multi_sweep_steady_state_vs_oracle(dims, R, F, monkeypatch):
     n4 = cp.last_launch_count()
     cp.als_sweep(Zd, dims, [a.clone() for a in Ad], nzd, F=Fd)
     n1 = cp.last_launch_count()
-    assert n4 == 4 * n1 - 3  # the prep launch of sweeps 2..4 is gone
+    # the prep launch of sweeps 2..4 is gone; N = 3 tensor-core plans also solve the last mode of
+    # sweeps 1..3 inside the pass (tests/test_gpu_sweep_tail.py)
+    assert n4 == 4 * n1 - 3 or (len(dims) == 3 and n4 == 4 * n1 - 6)
     Ao = [a.copy(order="F") for a in A]
     for _ in range(4):
         Ao, oo = oracle.als_sweep(Z, dims, Ao, F=Fh, normZ2=nz2)

@@ -13,6 +13,7 @@ import paper_1111_6091_b200 as cp  # noqa: E402
 
 name = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+nsw = int(os.environ.get("NSW", "1"))  # sweeps per call (cp_als_sweeps steady state when > 1)
 _, dims, R, *_ = cpsynth.CONFIGS[name]
 rng = np.random.default_rng(0)
 Zd = torch.randn(tuple(reversed(dims)), dtype=torch.float64, device="cuda")
@@ -28,8 +29,9 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 import time
 e0.record()
 th = time.perf_counter()
-for _ in range(reps):
-    cp.als_sweep(Zd, dims, A, nz, out=out, ws=ws)
+for _ in range(max(1, reps // nsw)):
+    cp.als_sweep(Zd, dims, A, nz, out=out, ws=ws, nsweeps=nsw)
+reps = max(1, reps // nsw) * nsw
 th = (time.perf_counter() - th) / reps * 1e3
 e1.record()
 torch.cuda.synchronize()
