@@ -74,7 +74,7 @@ static int parse_env(const char *name, int dflt) {
 }
 
 int path_flag(const char *name, int dflt) {
-  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MTTKRP_FUSED", "CP_MODEPROD_PIPE", "CP_SWEEP_TAIL",
+  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MTTKRP_FUSED", "CP_MODEPROD_PIPE", "CP_SWEEP_TAIL", "CP_TINY_SWEEP",
                                        "CP_SWEEP_TREE", "CP_YLSOLVE", "CP_MODEPROD_DMMA", "CP_MG_GRAPH",
                                        "CP_ALS_GRAPH", "CP_MG_STRUCTURED", "CP_PDL"};
   for (const char *k : kPaths)
@@ -904,6 +904,14 @@ int cp_als_sweeps(const cp_shape *s, const double *Z, const double *normZ2, doub
   if (!Lp) return CP_EINVAL;
   const Layout &L = *Lp;
   if ((st = check_ws(L, ws, ws_bytes))) return st;
+  if (use_small_sweep(*s) && path_flag("CP_TINY_SWEEP", 1) != 0 && tiny_sweep_ok(*s)) {
+    // the tiniest levels (P <= 512, R <= 4): one warp runs the whole call (tiny_sweep.cu)
+    if (launch_tiny_sweep(*s, Z, normZ2, A, F, nsweeps, out, reinterpret_cast<cudaStream_t>(stream), norm) !=
+        cudaSuccess)
+      return CP_ECUDA;
+    g_launches = 1;
+    return CP_OK;
+  }
   if (use_small_sweep(*s)) {
     if (launch_small_sweep(*s, Z, normZ2, A, F, nsweeps, out, reinterpret_cast<cudaStream_t>(stream), nullptr,
                            false, norm) != cudaSuccess)

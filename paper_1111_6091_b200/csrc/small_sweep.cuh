@@ -27,6 +27,13 @@ struct SmallSweepArgs {
   double *G[CP_MAX_N];    // gradient mode: G^(n) outputs (entries may be null)
 };
 
+// Single-warp variant for the tiniest tensors (tiny_sweep.cu): sweeps only (no gradient mode)
+constexpr int kTinySweepMaxR = 4;
+constexpr int64_t kTinySweepMaxP = 512;
+bool tiny_sweep_ok(const cp_shape &s);
+cudaError_t launch_tiny_sweep(const cp_shape &s, const double *Z, const double *normZ2, double *const *A,
+                              const double *const *F, int nsweeps, double *out, cudaStream_t st, bool normalize);
+
 // dynamic shared memory the kernel needs for shape s, or 0 if s is not small enough
 size_t small_sweep_smem_bytes(const cp_shape &s);
 cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double *normZ2, double *const *A,

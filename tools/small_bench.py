@@ -27,7 +27,7 @@ def timed(fn, n=20):
     return e[0].elapsed_time(e[1]) / n * 1e3  # us
 
 
-for s, R in ((4, 3), (7, 3), (13, 3), (25, 3), (50, 3), (20, 3), (100, 5)):
+for s, R in ((4, 3), (5, 3), (7, 3), (13, 3), (25, 3), (50, 3), (20, 3), (100, 5)):
     dims = (s, s, s)
     Z, A = cpsynth.random_problem(dims, R, seed=1)
     Zd = torch.from_numpy(Z).cuda()
@@ -35,15 +35,15 @@ for s, R in ((4, 3), (7, 3), (13, 3), (25, 3), (50, 3), (20, 3), (100, 5)):
     ws = cp.Workspace(dims, R)
     nz = cp.norm2(Zd, dims, ws=ws)
     row = {"dims": s, "R": R}
-    for path in ("1", "0"):
-        os.environ["CP_SMALL_SWEEP"] = path
-        os.environ["CP_MEDIUM_SWEEP"] = path
+    for name, small, tiny in (("tiny", "1", "1"), ("fused", "1", "0"), ("general", "0", "0")):
+        if name == "tiny" and s > 5:
+            continue
+        os.environ["CP_SMALL_SWEEP"] = small
+        os.environ["CP_TINY_SWEEP"] = tiny
         A2 = [a.clone() for a in Ad]
-        row["sweeps50_" + ("fused" if path == "1" else "general")] = timed(
-            lambda: cp.als_sweep(Zd, dims, A2, nz, ws=ws, nsweeps=50), n=5)
-        row["sweep1_" + ("fused" if path == "1" else "general")] = timed(
-            lambda: cp.als_sweep(Zd, dims, A2, nz, ws=ws), n=20)
+        row["sweeps50_" + name] = timed(lambda: cp.als_sweep(Zd, dims, A2, nz, ws=ws, nsweeps=50), n=5)
+        row["sweep1_" + name] = timed(lambda: cp.als_sweep(Zd, dims, A2, nz, ws=ws), n=20)
     os.environ["CP_SMALL_SWEEP"] = "1"
-    os.environ["CP_MEDIUM_SWEEP"] = "1"
+    os.environ["CP_TINY_SWEEP"] = "1"
     row["gradient"] = timed(lambda: cp.gradient(Zd, dims, Ad, nz, ws=ws), n=20)
     print({k: (round(v, 1) if isinstance(v, float) else v) for k, v in row.items()})
