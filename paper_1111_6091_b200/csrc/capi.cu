@@ -74,7 +74,7 @@ static int parse_env(const char *name, int dflt) {
 }
 
 int path_flag(const char *name, int dflt) {
-  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MTTKRP_FUSED", "CP_MODEPROD_PIPE", "CP_SWEEP_TAIL", "CP_TINY_SWEEP",
+  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MTTKRP_FUSED", "CP_MODEPROD_PIPE", "CP_SWEEP_TAIL", "CP_TINY_SWEEP", "CP_STREAM_PREFETCH",
                                        "CP_SWEEP_TREE", "CP_YLSOLVE", "CP_MODEPROD_DMMA", "CP_MG_GRAPH",
                                        "CP_ALS_GRAPH", "CP_MG_STRUCTURED", "CP_PDL"};
   for (const char *k : kPaths)
@@ -1099,6 +1099,10 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
     // Gamma^(0) (Grams of the old factors only) rides in the Y_L pass's idle weight warp
     const bool job0 = jobs && p1.mma && p1.direct_w;
     if (job0) p1.gj = gamma_job(0);
+    // the pass's predecessor is this call's prep kernel or the previous sweep's last kernel:
+    // neither writes Z, so the first stages' Z loads may precede the PDL wait
+    const bool zpre = path_flag("CP_STREAM_PREFETCH", 1) != 0;
+    p1.prefetch = (zpre && p1.mma && p1.V >= 2) ? 1 : 0;
     if (!(skip & 128) && launch_stream(p1, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
     YLGeom yg;
@@ -1203,6 +1207,7 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
     // 419.0 us, c3 80.7 -> 75.9, c2 50.5 -> 46.9, c1 45.0 -> 41.0, tools/tail_ab.sh);
     // 2: every sweep (fin = 1 on a call's last sweep: measured 2-5 us slower than the solve launch it
     // replaces -- the last CTA's Gram and sums are a chain of L2 round trips -- so not the default).
+    p2.prefetch = (zpre && p2.mma && p2.V >= 2) ? 1 : 0;  // (predecessor: the mode-1 solve)
     const int tail_sel = path_flag("CP_SWEEP_TAIL", 1);
     const bool defer = defer_ok && deferred != nullptr && jobs && L.yl_plan.mma && L.yl_plan.direct_w;
     const bool tail = N == 3 && job2 && R <= 32 && p2.slots <= 32 && (tail_sel >= 2 || (tail_sel == 1 && defer)) &&

@@ -121,6 +121,8 @@ struct StreamPlan {
   int gjsm;         // shared-memory doubles reserved for it
   int64_t keep_q;   // L2 residency across passes: Z columns q < keep_q are fetched with an
                     // evict_last policy, the rest evict_first (0: no hints).  See DESIGN 6.8.
+  int prefetch;     // the launch's predecessor does not write Z: the producer issues the Z part of
+                    // its first nstages stages before the PDL wait (stream_kernel.cuh produce)
   int dbg;          // experiments only (knob CP_STREAM_DBG, -DCP_EXPERIMENTS builds): 1 = consumers skip the FMAs
   // MMA plans whose row block is the whole column (RB = 1): one 3-D tensor-map TMA per full
   // stage instead of one bulk copy per column.  View {I1, qsd[0], Q / qsd[0]} of Z, box
@@ -201,13 +203,17 @@ size_t stream_part_doubles(const StreamPlan &p);
 cudaError_t launch_stream(const StreamPlan &p, cudaStream_t st);
 
 // Programmatic dependent launch (PDL): the sweep's kernels are launched with programmatic
-// stream serialization, so a kernel's blocks are scheduled while its predecessor drains.  Every
-// kernel launched that way starts with griddep(): allow the next kernel to launch, then wait
-// until the predecessor grid has completed and its writes are visible (before any global
-// access and before any early return, so completion stays transitive along the stream).
+// stream serialization, so a kernel's blocks are scheduled while its predecessor runs.  Every
+// kernel launched that way starts with griddep(): wait until the predecessor grid has completed
+// and its writes are visible (before any global access to data a predecessor may write and before
+// any early return, so completion stays transitive along the stream), THEN allow the next kernel
+// to launch.  Because the trigger follows the wait, a kernel's blocks only start once everything
+// up to its predecessor's predecessor is complete: code before griddep() may read data that the
+// immediate predecessor does not write (the Z prefetch of the streaming kernels,
+// StreamPlan::prefetch).
 __device__ __forceinline__ void griddep() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 // Timing builds only (-DCP_CTA_TIMELINE, tools/sweep_timeline.py): every block's thread 0 prints
 // its entry time, the time its griddep() wait returned and its exit time (globaltimer, ns).

@@ -94,34 +94,52 @@ __device__ __forceinline__ void load_rows(const double *zc, int u, int Wb, doubl
 // Stage boundaries: a stage never crosses an i_m segment, the CTA's range end, or a wrap of
 // the fastest column digit -- so the fastest factor's rows of a stage are contiguous in At
 // (one bulk copy) and every slower digit is constant over the stage.
+// prefetch (StreamPlan::prefetch, TMA plans): the kernel's predecessor does not write Z, so the Z
+// part of the first nstages stages is issued BEFORE the programmatic-dependent-launch wait (the
+// HBM latency of the first stages overlaps the predecessor's tail), and their factor rows --
+// which the predecessor does write -- after it.  The stage barrier completes only with the
+// producer's arrival, which follows both parts.
+struct ProducerState {
+  int64_t v, seg_left;
+  int seg_slot, stage;
+  uint32_t eph;
+  int B[kMaxDigits];
+};
 template <int R, int V>
 __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, int64_t row0, int Wb,
-                        const StreamSmem &sm) {
+                        const StreamSmem &sm, bool prefetch = false) {
   const int nd = p.nd;
   const bool has_f0 = (p.ord[0] != p.mode);
   const double *A0 = p.At[p.ord[0]];
-  int B[kMaxDigits];
+  ProducerState st0;
   {
     int64_t t = v0;
 #pragma unroll
     for (int j = 0; j < kMaxDigits; ++j) {
-      B[j] = 0;
+      st0.B[j] = 0;
       if (j < nd) {
-        B[j] = (int)(t % p.rad[j]);
+        st0.B[j] = (int)(t % p.rad[j]);
         t /= p.rad[j];
       }
     }
   }
-  int64_t seg_left = p.Qn - (v0 % p.Qn);
-  int seg_slot = 0;
+  st0.seg_left = p.Qn - (v0 % p.Qn);
+  st0.seg_slot = 0;
+  st0.stage = 0;
+  st0.eph = 1;
+  st0.v = v0;
 #ifdef CP_STREAM_TIMING
   long long tm_wait = 0, tm_n = 0, tm0 = clock64();
 #endif
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
-  int stage = 0;
-  uint32_t eph = 1;
-  int64_t v = v0;
-  while (v < v1) {
+  // part 0: whole stages; 1: Z only (before the wait); 2: the factor rows, header and arrival of
+  // the stages part 1 started
+  auto run = [&](ProducerState &st, const int part, int max_stages) {
+  int (&B)[kMaxDigits] = st.B;
+  int64_t &seg_left = st.seg_left, &v = st.v;
+  int &seg_slot = st.seg_slot, &stage = st.stage;
+  uint32_t &eph = st.eph;
+  while (v < v1 && max_stages-- > 0) {
     int64_t lim = (seg_left < v1 - v) ? seg_left : (v1 - v);
     if (lim > p.rad[0] - B[0]) lim = p.rad[0] - B[0];
     const int ncols = (int)(lim < p.cps ? lim : p.cps);
@@ -134,7 +152,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
 #ifdef CP_STREAM_TIMING
     long long tw0 = clock64();
 #endif
-    mbar_wait(&sm.empty[stage], eph);
+    if (part != 2) mbar_wait(&sm.empty[stage], eph);
 #ifdef CP_STREAM_TIMING
     tm_wait += clock64() - tw0;
     ++tm_n;
@@ -150,11 +168,11 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       }
       const bool tstage = p.use_tmap && ncols == p.cps;  // full stage: one tensor-map TMA
       const uint32_t zbytes = tstage ? (uint32_t)(p.zcs * p.cps * 8) : (uint32_t)(ncols * Wb * 8);
-      if (lane == 0)
-        mbar_expect_tx(&sm.full[stage], zbytes + (has_f0 ? (p.fcm ? p.fs * p.R * 8 : ncols * p.RS * 8) : 0) +
-                                            nslow * (p.fcm ? 2 * p.R : p.RS) * 8);
+      const uint32_t fbytes = (has_f0 ? (p.fcm ? p.fs * p.R * 8 : ncols * p.RS * 8) : 0) +
+                              nslow * (p.fcm ? 2 * p.R : p.RS) * 8;
+      if (lane == 0) mbar_expect_tx(&sm.full[stage], (part != 2 ? zbytes : 0u) + (part != 1 ? fbytes : 0u));
       __syncwarp();
-      if (p.srows) {
+      if (p.srows && part != 1) {
         // the factor rows of the slow digits (constant over the stage), one copy each (fcm: a
         // {2, R} box of the column-major factor's tensor map: rank r at 2r, p.sstr)
 #pragma unroll
@@ -169,7 +187,9 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       }
       // Z columns: q advances by qsd[0] per column within a stage (digit 0 only).  Strided
       // columns are issued by all 32 lanes (one bulk copy per column).
-      if (tstage) {
+      if (part == 2) {
+        // (Z issued by part 1)
+      } else if (tstage) {
         if (lane == 0) {
           const int64_t qs = p.qsd[0];
           const int c1 = (int)(q0 % qs), c2 = (int)(q0 / qs);
@@ -197,7 +217,9 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
             bulk_g2s(zs + (size_t)col * zstride, p.Z + q * p.I1 + row0, (uint32_t)(Wb * 8), &sm.full[stage]);
         }
       }
-      if (has_f0 && p.fcm) {
+      if (part == 1) {
+        // (factor rows by part 2, after the wait)
+      } else if (has_f0 && p.fcm) {
         // rows B0 .. B0 + fs - 1 of the column-major factor as one {fs, R} box: rank-major
         // [R][fs] in shared memory (rows past I_k zero-filled)
         // (the innermost TMA coordinate must be 16-byte aligned: the box starts at the even row
@@ -224,7 +246,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
         for (int e = lane; e < ncols * p.RS; e += 32) as[e] = __ldg(A0 + (int64_t)B[0] * p.RS + e);
       __syncwarp();
     }
-    if (lane == 0) {
+    if (lane == 0 && part != 1) {
       int *h = sm.hdr + stage * kHdrInts;
       h[0] = ncols;
       h[1] = (eos ? 1 : 0) | (last ? 2 : 0);
@@ -254,6 +276,14 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       eph ^= 1u;
     }
   }
+  };
+  if (prefetch && V >= 2) {
+    ProducerState pre = st0;
+    run(pre, 1, p.nstages);
+    griddep();
+    run(st0, 2, p.nstages);
+  }
+  run(st0, 0, 0x7fffffff);
 #ifdef CP_STREAM_TIMING
   if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 101))
     printf("[cta %d] producer: total %lld wait_empty %lld stages %lld\n", blockIdx.x, clock64() - tm0, tm_wait, tm_n);

@@ -564,13 +564,16 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   }
   __syncthreads();
   CTL_BEGIN
-  griddep();  // (PDL) predecessor's At / factor writes visible from here on
+  // (PDL) predecessor's At / factor writes visible from here on; with p.prefetch the producer
+  // warp first issues the Z part of its first stages and waits inside produce()
+  const bool prefetch = p.prefetch != 0 && p.Mout == nullptr;
+  if (!(prefetch && (tid >> 5) == kConsumerWarps)) griddep();
   CTL_AFTER_WAIT
   // one-launch cp_mttkrp, mode 0: CTA 0 claims the grid barrier's words for this launch
   if (OP == OP_MTTKRP && p.mode == 0 && p.Mout != nullptr && blockIdx.x == 0 && tid == 0) grid_claim(p.tick, p.tag);
 
   if (warp == kConsumerWarps) {
-    produce<8, 2>(p, lane, v0, v1, row0, Wb, sm);  // (template args only select the TMA path)
+    produce<8, 2>(p, lane, v0, v1, row0, Wb, sm, prefetch);  // (template args only select the TMA path)
     return;
   }
   if (warp == kConsumerWarps + 1) {

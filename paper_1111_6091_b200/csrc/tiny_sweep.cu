@@ -92,6 +92,9 @@ __device__ __noinline__ void tiny_mttkrp(const double *sZ, const double *sWL, co
   }
 }
 
+// (The mode loops are unrolled with the per-mode sizes in registers.  A rolled variant with the
+// sizes in shared memory -- one copy of the per-mode code -- measured slower: 4^3 R = 3 357 vs
+// 272 us per 50 sweeps; the rolled Gamma product alone went from ~400 to ~2350 cycles per mode.)
 template <int R>
 __global__ void __launch_bounds__(32) tiny_sweep_kernel(const SmallSweepArgs a) {
   griddep();
