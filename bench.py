@@ -519,6 +519,13 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P, peaks64):
         t = flushed(lambda: cp.als_sweep(Z3, d3, A3, nz3, out=out3, ws=ws3))
         rows["c3_sweep"] = {"ms": t, "sweeps_per_s": 1e3 / t, "z_passes": 2,
                             "alg_GBps_2pass": 2 * 8.0 * P3 / t / 1e6, "l2": "flushed before each rep"}
+        # the ALS loop itself: K sweeps in one cp_als_sweeps call (steady state: no prep launch, the
+        # last mode solved inside the pass; Z = 128 MiB stays partly L2-resident between passes)
+        cp.als_sweep(Z3, d3, A3, nz3, out=out3, ws=ws3, nsweeps=50)
+        t = timed(lambda: cp.als_sweep(Z3, d3, A3, nz3, out=out3, ws=ws3, nsweeps=50), n=4) / 50
+        rows["c3_sweep_steady"] = {"ms": t, "sweeps_per_s": 1e3 / t, "z_passes": 2,
+                                   "alg_GBps_2pass": 2 * 8.0 * P3 / t / 1e6,
+                                   "l2": "not flushed: one cp_als_sweeps(50) call, device-resident loop"}
         M3 = [empty_factor(I, R3, dev) for I in d3]
         for n in range(3):
             t = flushed(lambda: cp.mttkrp(Z3, d3, A3, n, M=M3[n], ws=ws3))
@@ -600,8 +607,13 @@ def time_rows(cp, torch, d, Zd, A, nz, ws, dev, stream, dims, R, P, peaks64):
         e1.record()
         torch.cuda.synchronize()
         us = 1e3 * e0.elapsed_time(e1) / (4 * K)
+        # the same K sweeps as ONE cp_als_sweeps(K) call (steady-state sweeps)
+        cp.als_sweep(Zc, dd, Ac, nzc, out=outc, ws=wsc, nsweeps=K)
+        nls = cp.last_launch_count()
+        us_steady = 1e3 * timed(lambda: cp.als_sweep(Zc, dd, Ac, nzc, out=outc, ws=wsc, nsweeps=K), n=4) / K
         rows[f"{name}_sweep_latency"] = {
             "us_per_sweep": us, "sweeps_per_s": 1e6 / us, "launches_per_sweep": nl,
+            "us_per_sweep_one_call": us_steady, "launches_per_sweep_one_call": nls / K,
             "launch_floor_us": floor, "launch_floor_frac": (nl * floor / us) if floor else None,
             "path": "fused single-CTA kernel (small_sweep.cu)" if nl == 1 else "general dimension-tree sweep",
             "timing": f"{K} sweeps in one CUDA graph, 4 replays, L2-resident (no flush)"}
