@@ -1208,7 +1208,11 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
     // 2: every sweep (fin = 1 on a call's last sweep: measured 2-5 us slower than the solve launch it
     // replaces -- the last CTA's Gram and sums are a chain of L2 round trips -- so not the default).
     p2.prefetch = (zpre && p2.mma && p2.V >= 2) ? 1 : 0;  // (predecessor: the mode-1 solve)
-    const int tail_sel = path_flag("CP_SWEEP_TAIL", 1);
+    // (default only up to 2^26 elements: on c4a, 2^27, the ~4 us it saves per sweep are within the
+    // run-to-run noise of the 420-us sweep, and the pass would carry the solve in its own time)
+    double Pel = 1.0;
+    for (int k = 0; k < N; ++k) Pel *= (double)s->dims[k];
+    const int tail_sel = path_flag("CP_SWEEP_TAIL", Pel <= 67108864.0 ? 1 : 0);
     const bool defer = defer_ok && deferred != nullptr && jobs && L.yl_plan.mma && L.yl_plan.direct_w;
     const bool tail = N == 3 && job2 && R <= 32 && p2.slots <= 32 && (tail_sel >= 2 || (tail_sel == 1 && defer)) &&
                       (int64_t)p2.nstages * p2.zst >= sweep_tail_doubles(R);
