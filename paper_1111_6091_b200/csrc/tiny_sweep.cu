@@ -63,32 +63,51 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 }  // namespace
 
-// M(i, r) for the output entries o = i + In r owned by this lane (o = lane, lane + 32, ...): the
-// PARTS = 2^ceil(log2 Q) column terms z(a, i, b) (WL(a, r) WR(b, r)) of the entry in the lane's
-// registers (columns q >= Q: 0), summed in the order of small_sweep_kernel's 32-lane xor tree
-// (level d: t[q] += t[q + d] for q < d, d = PARTS/2 .. 1; its levels above PARTS add exact
-// zeros).  qt[q] = (a + bstride b, a, b) of column q (built once per call).
+// M(i, r) for the output entries o = i + In r: the PARTS = 2^ceil(log2 Q) column terms
+// z(a, i, b) (WL(a, r) WR(b, r)) of an entry (columns q >= Q: 0) are summed in the order of
+// small_sweep_kernel's 32-lane xor tree (level d: t[q] += t[q + d] for q < d, d = PARTS/2 .. 1;
+// its levels above PARTS add exact zeros).  qt[q] = (a + bstride b, a, b) of column q (built
+// once per call).
 template <int PARTS>
 __device__ __noinline__ void tiny_mttkrp(const double *sZ, const double *sWL, const double *sWR, double *sM,
                                          const ushort4 *qt, int Q, int left, int right, int In, float inv_In, int nout,
                                          int lane) {
-  for (int o = lane; o < nout; o += 32) {
-    const int r = ts_qdiv(o, In, inv_In), i = o - r * In;
+  // Two lanes per output entry: lane parity h takes the columns q = 2 j + h and runs the tree's
+  // levels PARTS/2 .. 2 in its registers (they only pair columns of equal parity); the last level,
+  // t[0] + t[1], is one shuffle.  PARTS = 1: one lane, one term.
+  constexpr int H = PARTS > 1 ? PARTS / 2 : 1;
+  const int h = PARTS > 1 ? (lane & 1) : 0;
+  const int per = PARTS > 1 ? 16 : 32;  // output entries per round
+  for (int o0 = 0; o0 < nout; o0 += per) {
+    const int o = o0 + (PARTS > 1 ? (lane >> 1) : lane);
+    const int oc = o < nout ? o : 0;
+    const int r = ts_qdiv(oc, In, inv_In), i = oc - r * In;
     const double *zrow = sZ + left * i, *wl = sWL + left * r, *wr = sWR + right * r;
-    double t[PARTS];
+    // branch-free (columns q >= Q re-read column 0 and are zeroed by a select): with a branch per
+    // column the terms ran one after the other, ~110 cycles each
+    double t[H];
+    ushort4 cq[H];
 #pragma unroll
-    for (int q = 0; q < PARTS; ++q) {
-      t[q] = 0.0;
-      if (q < Q) {
-        const ushort4 c = qt[q];
-        t[q] = fma(zrow[c.x], wl[c.y] * wr[c.z], 0.0);
-      }
+    for (int j = 0; j < H; ++j) {
+      const int q = (PARTS > 1 ? 2 * j : j) + h;
+      cq[j] = qt[q < Q ? q : 0];
     }
 #pragma unroll
-    for (int d = PARTS / 2; d > 0; d >>= 1)
+    for (int j = 0; j < H; ++j) {
+      const int q = (PARTS > 1 ? 2 * j : j) + h;
+      const double v = fma(zrow[cq[j].x], wl[cq[j].y] * wr[cq[j].z], 0.0);
+      t[j] = (q < Q) ? v : 0.0;
+    }
 #pragma unroll
-      for (int q = 0; q < d; ++q) t[q] += t[q + d];
-    sM[o] = t[0];
+    for (int d = H / 2; d > 0; d >>= 1)
+#pragma unroll
+      for (int j = 0; j < d; ++j) t[j] += t[j + d];
+    double m = t[0];
+    if (PARTS > 1) {
+      const double other = __shfl_xor_sync(0xffffffffu, m, 1);
+      m = m + other;  // (h = 0: t[0] + t[1], the tree's last level)
+    }
+    if (h == 0 && o < nout) sM[o] = m;
   }
 }
 
