@@ -184,6 +184,19 @@ int cp_gradient(const cp_shape *s, const double *Z, const double *normZ2, const 
                 const double *const *F, double *out, double *const *G, void *ws, size_t ws_bytes,
                 cp_stream_t stream);
 
+/* cp_als_sweeps followed by cp_gradient(F = gF) at the new iterate -- the pair every level of a
+ * CP-FAS V-cycle issues (Algorithm 2: relax, then H(A) for eq:FASrhs).  The results
+ * (A, out, gout, G) are bitwise those of the two separate calls; on tensors that run the fused
+ * shared-memory sweep kernel the gradient pass runs in the same launch (Z and the factors are
+ * loaded once).
+ *   out   as cp_als_sweeps (4 doubles);  gout, G, gF as out, G, F of cp_gradient (gout: 2 + N
+ *   doubles; if the sweeps fail with CP_ENOTSPD in out, gout[0..1] are NaN)
+ *   Errors: as cp_als_sweeps. */
+int cp_als_sweeps_then_gradient(const cp_shape *s, const double *Z, const double *normZ2,
+                                double *const *A, const double *const *F, int32_t nsweeps,
+                                int32_t flags, double *out, const double *const *gF, double *gout,
+                                double *const *G, void *ws, size_t ws_bytes, cp_stream_t stream);
+
 /* Number of kernel launches the last successful call on this thread enqueued (for the
  * benchmark's gpu_launches count). */
 int cp_last_launch_count(void);

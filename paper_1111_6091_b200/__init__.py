@@ -23,7 +23,7 @@ from ._lib import (CP_ECUDA, CP_EDIM, CP_EINVAL, CP_ENOTSPD, CP_EWORKSPACE, CP_M
                    CP_OK, CPError, lib, lib_path)
 
 __all__ = ["colmajor", "empty_factor", "Workspace", "norm2", "mttkrp", "als_sweep",
-           "mode_product", "restrict_structured", "fit", "workspace_bytes", "lib", "lib_path", "last_launch_count",
+           "mode_product", "restrict_structured", "fit", "als_sweeps_then_gradient", "workspace_bytes", "lib", "lib_path", "last_launch_count",
            "CPError", "CP_OK", "CP_EINVAL", "CP_EDIM", "CP_ENOTSPD", "CP_ECUDA", "CP_EWORKSPACE"]
 
 
@@ -344,6 +344,35 @@ def fit(Z, dims, A, normZ2, F=None, want_G=False, out=None, ws=None, stream=None
                         _ptr(out), _ptr_array(G) if G else None, _ptr(ws.buf),
                         ctypes.c_size_t(ws.nbytes), _stream(stream)), "cp_fit")
     return out, G
+
+
+def als_sweeps_then_gradient(Z, dims, A, normZ2, F=None, gF=None, nsweeps=1, normalize=False, want_G=True,
+                             ws=None, stream=None):
+    """cp_als_sweeps followed by cp_gradient(F = gF) at the new iterate in one call
+    (cp_als_sweeps_then_gradient; one launch on small tensors).  Returns (out, gout, G list or None)."""
+    _check_Z(Z, dims)
+    N = len(dims)
+    R = A[0].shape[1]
+    for k, a in enumerate(A):
+        _check_cm(a, dims[k], R, f"A[{k}]")
+
+    def parr(Fs):
+        if Fs is None:
+            return None
+        for k, f in enumerate(Fs):
+            if f is not None:
+                _check_cm(f, dims[k], R, f"F[{k}]")
+        return _ptr_array(list(Fs))
+
+    G = [empty_factor(dims[k], R, Z.device) for k in range(N)] if want_G else None
+    out = torch.empty(4, dtype=torch.float64, device=Z.device)
+    gout = torch.empty(2 + N, dtype=torch.float64, device=Z.device)
+    ws = _ws(ws, dims, R, Z.device)
+    _check(lib().cp_als_sweeps_then_gradient(
+        ctypes.byref(_shape(dims, R)), _ptr(Z), _ptr(normZ2), _ptr_array(A), parr(F), ctypes.c_int32(int(nsweeps)),
+        ctypes.c_int32(1 if normalize else 0), _ptr(out), parr(gF), _ptr(gout), _ptr_array(G) if G else None,
+        _ptr(ws.buf), ctypes.c_size_t(ws.nbytes), _stream(stream)), "cp_als_sweeps_then_gradient")
+    return out, gout, G
 
 
 def gradient(Z, dims, A, normZ2, F=None, want_G=False, out=None, ws=None, stream=None):

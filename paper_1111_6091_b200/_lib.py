@@ -12,6 +12,7 @@ _lib = None
 
 # every symbol include/cp.h declares (checked by tests/test_capi_symbols.py)
 EXPORTS = ["cp_workspace_bytes", "cp_norm2", "cp_mttkrp", "cp_als_sweep", "cp_als_sweeps",
+           "cp_als_sweeps_then_gradient",
            "cp_mode_product_workspace_bytes", "cp_mode_product", "cp_fit", "cp_gradient",
            "cp_restrict_workspace_bytes", "cp_restrict_structured",
            "cp_last_launch_count", "cp_profile_enable", "cp_profile_read", "cp_normalize_sort",
@@ -51,6 +52,8 @@ def lib():
         L.cp_mttkrp.argtypes = [vp, vp, vp, i32, vp, vp, sz, vp]
         L.cp_als_sweep.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, vp]
         L.cp_als_sweeps.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, vp, sz, vp]
+        L.cp_als_sweeps_then_gradient.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, sz, vp]
+        L.cp_als_sweeps_then_gradient.restype = ctypes.c_int
         L.cp_mode_product_workspace_bytes.argtypes = [i32, vp, i32, i64]
         L.cp_mode_product_workspace_bytes.restype = sz
         L.cp_mode_product.argtypes = [i32, vp, vp, i32, vp, i64, vp, vp, sz, vp]

@@ -74,7 +74,7 @@ static int parse_env(const char *name, int dflt) {
 }
 
 int path_flag(const char *name, int dflt) {
-  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MTTKRP_FUSED", "CP_MODEPROD_PIPE", "CP_SWEEP_TAIL", "CP_TINY_SWEEP", "CP_STREAM_PREFETCH",
+  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MTTKRP_FUSED", "CP_MODEPROD_PIPE", "CP_SWEEP_TAIL", "CP_TINY_SWEEP", "CP_STREAM_PREFETCH", "CP_SWEEPS_GRAD_FUSED",
                                        "CP_SWEEP_TREE", "CP_YLSOLVE", "CP_MODEPROD_DMMA", "CP_MG_GRAPH",
                                        "CP_ALS_GRAPH", "CP_MG_STRUCTURED", "CP_PDL"};
   for (const char *k : kPaths)
@@ -1514,6 +1514,37 @@ int cp_gradient(const cp_shape *s, const double *Z, const double *normZ2, const 
                 const double *const *F, double *out, double *const *G, void *ws, size_t ws_bytes,
                 cp_stream_t stream) {
   return fit_impl(s, Z, normZ2, A, F, out, G, ws, ws_bytes, stream, false);
+}
+
+int cp_als_sweeps_then_gradient(const cp_shape *s, const double *Z, const double *normZ2,
+                                double *const *A, const double *const *F, int32_t nsweeps,
+                                int32_t flags, double *out, const double *const *gF, double *gout,
+                                double *const *G, void *ws, size_t ws_bytes, cp_stream_t stream) {
+  g_launches = 0;
+  if (!gout) return CP_EINVAL;
+  int st = check_shape(s, 2);
+  if (st) return st;
+  // small tensors beyond the tiny kernel's shapes: sweeps and the gradient pass in one launch of
+  // the fused kernel
+  if (Z && normZ2 && A && out && aligned(Z, 16) && nsweeps >= 1 && !(flags & ~CP_SWEEPS_NORMALIZE) &&
+      use_small_sweep(*s) && !(path_flag("CP_TINY_SWEEP", 1) != 0 && tiny_sweep_ok(*s)) &&
+      path_flag("CP_SWEEPS_GRAD_FUSED", 1) != 0) {
+    for (int k = 0; k < s->N; ++k)
+      if (A[k] == nullptr) return CP_EINVAL;
+    const auto Lp = get_layout(*s);
+    if (!Lp) return CP_EINVAL;
+    if ((st = check_ws(*Lp, ws, ws_bytes))) return st;
+    if (launch_small_sweep(*s, Z, normZ2, A, F, nsweeps, out, reinterpret_cast<cudaStream_t>(stream), G, false,
+                           (flags & CP_SWEEPS_NORMALIZE) != 0, gout, gF) != cudaSuccess)
+      return CP_ECUDA;
+    g_launches = 1;
+    return CP_OK;
+  }
+  if ((st = cp_als_sweeps(s, Z, normZ2, A, F, nsweeps, flags, out, ws, ws_bytes, stream))) return st;
+  const int n1 = g_launches;
+  if ((st = cp_gradient(s, Z, normZ2, A, gF, gout, G, ws, ws_bytes, stream))) return st;
+  g_launches += n1;
+  return CP_OK;
 }
 
 int cp_normalize_sort(const cp_shape *s, double *const *A, int32_t sort, double *lambda, void *ws,

@@ -451,10 +451,18 @@ struct MG {
       relax_fas(l, v.A, F, prm.nuc_solve);
       return;
     }
-    relax_fas(l, v.A, F, prm.nu1_solve);
     Level &nx = lv[l + 1];
-    restrict_(l, v.A, nx.Atil);     // A~_c
-    grad(l, v.A, v.H);              // H(A)
+    if (l > 0 && prm.nu1_solve > 0) {
+      // pre-relaxation and H(A) at the relaxed iterate as one call (one launch on small levels;
+      // bitwise the two calls)
+      ok(cp_als_sweeps_then_gradient(&v.s, v.Z, v.nz2, v.A, F, prm.nu1_solve, 0, next_out(), nullptr, out_fit, v.H,
+                                     ws, ws_bytes, cst));
+      restrict_(l, v.A, nx.Atil);   // A~_c
+    } else {
+      relax_fas(l, v.A, F, prm.nu1_solve);
+      restrict_(l, v.A, nx.Atil);   // A~_c
+      grad(l, v.A, v.H);            // H(A)
+    }
     grad(l + 1, nx.Atil, nx.H);     // H_c(A~_c)
     {                               // F_c = H_c(A~_c) + R (F - H(A))  (eq:FASrhs);  A_c = A~_c
       XferArgs a = xfer_args(l, kXferFasRhs, true);

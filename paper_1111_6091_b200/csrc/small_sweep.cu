@@ -124,11 +124,15 @@ __global__ void __launch_bounds__(KT) small_sweep_kernel(const SmallSweepArgs a)
   }
   __syncthreads();
 
-  double inner_last = 0.0, gsum = 0.0, model2_last = 0.0, fa_last = 0.0;
+  double inner_last = 0.0, inner_grad = 0.0, gsum = 0.0, model2_last = 0.0, fa_last = 0.0;
+  // passes: the nsweeps sweeps, then (grad_after) one gradient pass at the new iterate; pure
+  // gradient mode (a.grad) is that pass alone
+  const int npass = a.grad ? 1 : a.nsweeps + (a.grad_after ? 1 : 0);
 #ifdef CP_SMALL_TIMING
   long long tst[16] = {0};
 #endif
-  for (int sweep = 0; sweep < a.nsweeps && s_status == 0; ++sweep) {
+  for (int sweep = 0; sweep < npass && s_status == 0; ++sweep) {
+    const bool gpass = a.grad || sweep == a.nsweeps;
     for (int n = 0; n < N; ++n) {
       // Z viewed as left x I_n x right (left = prod_{k<n} I_k); the Khatri-Rao row of column
       // (a, b) is WL(a, :) * WR(b, :) with WL = the left modes' rows (P:110 order), WR the right
@@ -197,9 +201,9 @@ __global__ void __launch_bounds__(KT) small_sweep_kernel(const SmallSweepArgs a)
       }
       __syncthreads();
       if (n == 0) ST(3);
-      if (a.grad) {
+      if (gpass) {
         // ---- cp_gradient: G = -M + A Gamma - F at this iterate (eq:gradEqn), ||G||^2 ----
-        const double *Fg = a.F[n];
+        const double *Fg = a.gF[n];
         double *G = a.G[n];
         const double *An = sm + s_aoff[n];
         double g2 = 0.0, d = 0.0;
@@ -213,9 +217,9 @@ __global__ void __launch_bounds__(KT) small_sweep_kernel(const SmallSweepArgs a)
           if (n == N - 1) d = fma(sM[o], An[o], d);
         }
         const double g2s = block_sum_fixed<KT>(g2, red);
-        if (tid == 0) a.out[2 + n] = g2s;
+        if (tid == 0) a.gout[2 + n] = g2s;
         gsum += g2s;
-        if (n == N - 1) inner_last = block_sum_fixed<KT>(d, red);
+        if (n == N - 1) inner_grad = block_sum_fixed<KT>(d, red);
         continue;
       }
       // ---- Gamma = L L^T, lower, no pivoting; pivot <= 0 -> CP_ENOTSPD ----
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(KT) small_sweep_kernel(const SmallSweepArgs a)
       __syncthreads();
       if (n == 0) ST(6);
     }
-    if (a.grad || s_status != 0) continue;
+    if (gpass || s_status != 0) continue;
     if (sweep == a.nsweeps - 1) {
       // f pieces of the last sweep, before any normalization (as cp_als_sweep then
       // cp_normalize_sort): ||[[A]]||^2 = 1^T (*_k Upsilon^(k)) 1 and sum_n <F^(n), A^(n)>
@@ -455,7 +459,7 @@ __global__ void __launch_bounds__(KT) small_sweep_kernel(const SmallSweepArgs a)
     printf("small sweep phases (clk, mode 0 of sweep 1): wlwr %lld mttkrp %lld msum+gamma %lld chol %lld solve %lld gram %lld\n",
            tst[1] - tst[0], tst[2] - tst[1], tst[3] - tst[2], tst[4] - tst[3], tst[5] - tst[4], tst[6] - tst[5]);
 #endif
-  if (a.grad) {
+  if (a.grad || (a.grad_after && s_status == 0)) {
     // f by the expansion (reading R6), g = (sum_n ||G^(n)||^2)^{1/2} / ||Z|| (eq:gradConv)
     double m2 = 0.0;
     for (int e = tid; e < RR; e += KT) {
@@ -465,10 +469,13 @@ __global__ void __launch_bounds__(KT) small_sweep_kernel(const SmallSweepArgs a)
     }
     const double model2 = block_sum_fixed<KT>(m2, red);
     if (tid == 0) {
-      a.out[0] = 0.5 * a.normZ2[0] - inner_last + 0.5 * model2;
-      a.out[1] = sqrt(gsum) / sqrt(a.normZ2[0]);
+      a.gout[0] = 0.5 * a.normZ2[0] - inner_grad + 0.5 * model2;
+      a.gout[1] = sqrt(gsum) / sqrt(a.normZ2[0]);
     }
-    return;
+    if (a.grad) return;
+  } else if (a.grad_after && tid == 0) {
+    a.gout[0] = nan("");  // the sweeps failed (CP_ENOTSPD in out): no gradient
+    a.gout[1] = nan("");
   }
   // ---- write back, f and f~ (readings R6, R5) ----
   for (int k = 0; k < N; ++k)
@@ -517,12 +524,19 @@ size_t small_sweep_smem_bytes(const cp_shape &s) {
 
 cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double *normZ2, double *const *A,
                                const double *const *F, int nsweeps, double *out, cudaStream_t st,
-                               double *const *G, bool grad, bool normalize) {
+                               double *const *G, bool grad, bool normalize, double *gout,
+                               const double *const *gF) {
   SmallSweepArgs a;
   memset(&a, 0, sizeof(a));
   a.grad = grad ? 1 : 0;
   a.normalize = normalize ? 1 : 0;
-  for (int k = 0; k < s.N; ++k) a.G[k] = (G != nullptr) ? G[k] : nullptr;
+  // pure gradient mode: F enters G, results in out; sweeps + gradient: separate F / outputs
+  a.grad_after = (!grad && gout != nullptr) ? 1 : 0;
+  a.gout = grad ? out : gout;
+  for (int k = 0; k < s.N; ++k) {
+    a.G[k] = (G != nullptr) ? G[k] : nullptr;
+    a.gF[k] = grad ? ((F != nullptr) ? F[k] : nullptr) : ((gF != nullptr) ? gF[k] : nullptr);
+  }
   a.N = s.N;
   a.R = s.R;
   a.nsweeps = nsweeps;

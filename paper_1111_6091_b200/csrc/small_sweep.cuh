@@ -22,9 +22,13 @@ struct SmallSweepArgs {
   double *A[CP_MAX_N];
   const double *F[CP_MAX_N];
   double *out;
-  int grad;               // 1: cp_gradient at this iterate (no updates): out = f, g, ||G^(n)||^2
+  int grad;               // 1: cp_gradient at this iterate (no updates): gout = f, g, ||G^(n)||^2
   int normalize;          // 1: eq:ALSnorm (no sort) after every sweep (CP_SWEEPS_NORMALIZE)
-  double *G[CP_MAX_N];    // gradient mode: G^(n) outputs (entries may be null)
+  int grad_after;         // 1: after the nsweeps sweeps, the gradient pass at the new iterate in the
+                          // same launch (cp_als_sweeps_then_gradient): out as the sweeps, gout as cp_gradient
+  double *G[CP_MAX_N];    // gradient pass: G^(n) outputs (entries may be null)
+  const double *gF[CP_MAX_N];  // gradient pass: F entering G (R21), or null
+  double *gout;           // gradient pass: 2 + N doubles
 };
 
 // Single-warp variant for the tiniest tensors (tiny_sweep.cu): sweeps only (no gradient mode)
@@ -38,6 +42,7 @@ cudaError_t launch_tiny_sweep(const cp_shape &s, const double *Z, const double *
 size_t small_sweep_smem_bytes(const cp_shape &s);
 cudaError_t launch_small_sweep(const cp_shape &s, const double *Z, const double *normZ2, double *const *A,
                                const double *const *F, int nsweeps, double *out, cudaStream_t st,
-                               double *const *G = nullptr, bool grad = false, bool normalize = false);
+                               double *const *G = nullptr, bool grad = false, bool normalize = false,
+                               double *gout = nullptr, const double *const *gF = nullptr);
 
 }  // namespace cpk
