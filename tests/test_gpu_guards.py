@@ -84,12 +84,18 @@ def run_all(dims, R, fill, small, use_F):
         cp.mttkrp(Zd, dims, Ad, n, M=gM.factor(dims[n], R), ws=ws)
         guards.append(gM)
         res.append(gM.view())
+    # (nsw = 3 on the general path of an N = 3 tensor-core shape: sweeps 1, 2 solve their last
+    # mode inside the pass and leave its Gram to the next sweep's Gamma job)
     for nsw, norm in ((1, False), (3, False), (2, True)):
         go = Guarded(4)
         cp.als_sweep(Zd, dims, Ad, nz, F=None if norm else Fd, out=go.view(), ws=ws, nsweeps=nsw, normalize=norm)
         guards.append(go)
         res.append(go.view().clone())
         res += [a.clone() for a in Ad]
+    # relaxation + H(A) in one call (one launch of the fused kernel on small tensors)
+    _, gout, G = cp.als_sweeps_then_gradient(Zd, dims, Ad, nz, F=Fd, nsweeps=2, ws=ws)
+    res.append(gout.clone())
+    res += [g.clone() for g in G] + [a.clone() for a in Ad]
     for fn in (cp.fit, cp.gradient):
         go = Guarded(2 + len(dims))
         out, G = fn(Zd, dims, Ad, nz, F=Fd, want_G=True, out=go.view(), ws=ws)
@@ -101,7 +107,9 @@ def run_all(dims, R, fill, small, use_F):
     return [r.cpu() for r in res], all(g.intact() for g in guards), ws_tail_intact(ws), ok_inputs
 
 
-SHAPES = [((20, 20, 20), 3, "1", True),     # fused small-sweep kernel
+SHAPES = [((4, 4, 4), 3, "1", True),        # two-warp tiny kernel (coarsest multigrid level)
+          ((6, 5, 4), 4, "1", False),       # tiny kernel, R = 4, 20 / 24 / 30 columns
+          ((20, 20, 20), 3, "1", True),     # fused small-sweep kernel
           ((20, 20, 20), 3, "0", True),     # general path, tensor-map stage loads
           ((50, 48, 46), 8, "1", True),     # general path (P > 16384), MMA consumers
           ((9, 8, 7, 6), 5, "0", False),    # 4-way: Y_R path
