@@ -15,7 +15,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("no CUDA device", allow_module_level=True)
 
 import paper_1111_6091_b200 as cp  # noqa: E402
-from gpu_util import dev_factor, dev_tensor, host_factor, relerr  # noqa: E402
+from gpu_util import dev_factor, dev_tensor, host_factor  # noqa: E402
 
 
 def _bits(t):
@@ -54,8 +54,11 @@ def test_equals_the_two_calls_bitwise(dims, R, nu, normalize):
     # and the gradient itself against the oracle at the new iterate
     Ah = [host_factor(a) for a in A2]
     fo, Go = oracle.gradient(Z, dims, Ah, want_G=True)
+    # (G = A Gamma - M is a difference of two O(|M|) terms: after a sweep without F the last
+    # mode's gradient is zero up to rounding, so the error is measured against |M|)
     for k in range(N):
-        assert relerr(host_factor(G2[k]), Go[k]) <= 1e-9
+        Mk = np.linalg.norm(oracle.mttkrp(Z, dims, Ah, k))
+        assert np.linalg.norm(host_factor(G2[k]) - Go[k]) <= 1e-9 * np.linalg.norm(Go[k]) + 1e-12 * Mk
     assert abs(g2.cpu().numpy()[1] - fo[1]) <= 1e-10 * fo[1] + 1e-13
 
 
