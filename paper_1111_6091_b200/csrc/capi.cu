@@ -39,12 +39,20 @@ const StreamEntry &stream_entry(int R, int V, int op) {
   return g_table[stream_index(R, V, op)];
 }
 
-static StreamEntry g_mma_table[kMmaTableSize];
+static StreamEntry g_mma_table[2][kMmaTableSize];  // [0]: lean kernels, [1]: full-feature kernels
 static std::once_flag g_mma_once;
 
-const StreamEntry &stream_mma_entry(int nt, int mt, int op) {
-  std::call_once(g_mma_once, [] { register_stream_mma(g_mma_table); });
-  return g_mma_table[mma_index(nt, mt, op)];
+const StreamEntry &stream_mma_entry(int nt, int mt, int op, bool feat) {
+  std::call_once(g_mma_once, [] {
+    register_stream_mma(g_mma_table[0]);
+    register_stream_mma_f(g_mma_table[1]);
+  });
+  return g_mma_table[feat ? 1 : 0][mma_index(nt, mt, op)];
+}
+
+// Does the plan use anything the lean instantiation leaves out (stream_kernel.cuh, P_FCM)?
+static bool stream_mma_feat(const StreamPlan &p) {
+  return p.fcm != 0 || p.prefetch != 0 || p.tail.on != 0 || p.Mout != nullptr || (p.gj.on && p.gj.gram_rows > 0);
 }
 
 int current_device() {
@@ -74,7 +82,7 @@ static int parse_env(const char *name, int dflt) {
 }
 
 int path_flag(const char *name, int dflt) {
-  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MTTKRP_FUSED", "CP_MODEPROD_PIPE", "CP_SWEEP_TAIL", "CP_TINY_SWEEP", "CP_STREAM_PREFETCH", "CP_SWEEPS_GRAD_FUSED",
+  static const char *const kPaths[] = {"CP_STREAM_MMA", "CP_RESID_MMA", "CP_STREAM_TMAP", "CP_SMALL_SWEEP", "CP_MTTKRP_FCM", "CP_MTTKRP_FUSED", "CP_MODEPROD_PIPE", "CP_SWEEP_TAIL", "CP_TINY_SWEEP", "CP_STREAM_PREFETCH", "CP_STREAM_LEAN", "CP_SWEEPS_GRAD_FUSED",
                                        "CP_SWEEP_TREE", "CP_YLSOLVE", "CP_MODEPROD_DMMA", "CP_MG_GRAPH",
                                        "CP_ALS_GRAPH", "CP_MG_STRUCTURED", "CP_PDL"};
   for (const char *k : kPaths)
@@ -534,7 +542,8 @@ cudaError_t launch_stream(const StreamPlan &p0, cudaStream_t st) {
   p.use_tmap = 0;
   if (p.mma && path_flag("CP_STREAM_TMAP", 1)) p.use_tmap = encode_stage_tmap(p) ? 1 : 0;
   if (p.fcm && !encode_factor_maps(p)) return cudaErrorInvalidValue;
-  const StreamEntry &e = p.mma ? stream_mma_entry(p.nt, p.mt, p.op) : stream_entry(p.R, p.V, p.op);
+  const StreamEntry &e = p.mma ? stream_mma_entry(p.nt, p.mt, p.op, stream_mma_feat(p) || path_flag("CP_STREAM_LEAN", 1) == 0)
+                              : stream_entry(p.R, p.V, p.op);
   ++g_launches;
   const bool prof = g_prof_on && g_prof_n < kProfMax;
   if (prof) cudaEventRecord(g_prof_ev[2 * g_prof_n], st);
@@ -1101,7 +1110,11 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
     if (job0) p1.gj = gamma_job(0);
     // the pass's predecessor is this call's prep kernel or the previous sweep's last kernel:
     // neither writes Z, so the first stages' Z loads may precede the PDL wait
-    const bool zpre = path_flag("CP_STREAM_PREFETCH", 1) != 0;
+    // (default only up to 2^26 elements: on c4a / c4b the prefetch changes nothing measurable and
+    // the passes run the lean kernel instantiation instead, 5 us faster per c4a pass)
+    double Pel = 1.0;
+    for (int k = 0; k < N; ++k) Pel *= (double)s->dims[k];
+    const bool zpre = path_flag("CP_STREAM_PREFETCH", Pel <= 67108864.0 ? 1 : 0) != 0;
     p1.prefetch = (zpre && p1.mma && p1.V >= 2) ? 1 : 0;
     if (!(skip & 128) && launch_stream(p1, cs) != cudaSuccess) return CP_ECUDA;
     ++launches;
@@ -1210,8 +1223,6 @@ static int sweep_impl(const cp_shape *s, const double *Z, const double *normZ2, 
     p2.prefetch = (zpre && p2.mma && p2.V >= 2) ? 1 : 0;  // (predecessor: the mode-1 solve)
     // (default only up to 2^26 elements: on c4a, 2^27, the ~4 us it saves per sweep are within the
     // run-to-run noise of the 420-us sweep, and the pass would carry the solve in its own time)
-    double Pel = 1.0;
-    for (int k = 0; k < N; ++k) Pel *= (double)s->dims[k];
     const int tail_sel = path_flag("CP_SWEEP_TAIL", Pel <= 67108864.0 ? 1 : 0);
     const bool defer = defer_ok && deferred != nullptr && jobs && L.yl_plan.mma && L.yl_plan.direct_w;
     const bool tail = N == 3 && job2 && R <= 32 && p2.slots <= 32 && (tail_sel >= 2 || (tail_sel == 1 && defer)) &&

@@ -181,8 +181,9 @@ constexpr int mma_index(int nt, int mt, int op) {
   return ((nt - 1) * 8 + (mt - 1)) * 3 + (op == OP_YL ? 1 : (op == OP_RESID ? 2 : 0));
 }
 constexpr int kMmaTableSize = mma_index(4, 8, OP_RESID) + 1;
-void register_stream_mma(StreamEntry *t);
-const StreamEntry &stream_mma_entry(int nt, int mt, int op);
+void register_stream_mma(StreamEntry *t);    // lean kernels (FEAT = false)
+void register_stream_mma_f(StreamEntry *t);  // full-feature kernels
+const StreamEntry &stream_mma_entry(int nt, int mt, int op, bool feat = true);
 
 // ---------------------------------------------------------------- host configuration
 // Path selectors (documented in include/cp.h): environment switches between result-equivalent

@@ -15,7 +15,9 @@
   CPK_STREAM_REG_R(R0 + 4) CPK_STREAM_REG_R(R0 + 5) CPK_STREAM_REG_R(R0 + 6) CPK_STREAM_REG_R(R0 + 7)
 
 // FP64 tensor-core consumers: NT = 1, 2 with MT = 1..8; NT = 3, 4 with MT = 1..4; every op
-#define CPK_MMA_REG(NT, MT, OP) t[mma_index(NT, MT, OP)] = {launch_stream_mma_t<NT, MT, OP>, (const void *)stream_mma_kernel<NT, MT, OP>};
+// (CPK_MMA_FEAT: the translation unit's feature flag -- stream_mma_inst.cu lean, stream_mma_inst_f.cu full)
+#define CPK_MMA_REG(NT, MT, OP) \
+  t[mma_index(NT, MT, OP)] = {launch_stream_mma_t<NT, MT, OP, CPK_MMA_FEAT>, (const void *)stream_mma_kernel<NT, MT, OP, CPK_MMA_FEAT>};
 #define CPK_MMA_REG_OPS(NT, MT) CPK_MMA_REG(NT, MT, 0) CPK_MMA_REG(NT, MT, 2) CPK_MMA_REG(NT, MT, 1)
 #define CPK_MMA_REG_MT4(NT) CPK_MMA_REG_OPS(NT, 1) CPK_MMA_REG_OPS(NT, 2) CPK_MMA_REG_OPS(NT, 3) CPK_MMA_REG_OPS(NT, 4)
 #define CPK_MMA_REG_MT8(NT) \

@@ -25,6 +25,12 @@
 
 namespace cpk {
 
+// Feature-free instantiations (FEAT = false) of the producer and of stream_mma_kernel: without
+// the column-major-factor staging (fcm), the pre-wait Z prefetch and the in-pass completion code
+// (sweep_tail, one-launch cp_mttkrp, deferred Gram) the same pass measured 5 us faster on c4a
+// (191.3 -> 186.1 us; each feature alone costs 0.9-1.8 us: registers and code around the hot
+// loop), so plans that use none of them run the lean kernel (launch_stream).
+#define P_FCM(p) (FEAT && (p).fcm != 0)
 constexpr int kHdrInts = 16;  // per-stage header: ncols, flags, slot, fcm row offset, digits[kMaxDigits]
 
 // Register budget: up to this many accumulators per thread (V rows x R ranks) the kernel is
@@ -105,7 +111,7 @@ struct ProducerState {
   uint32_t eph;
   int B[kMaxDigits];
 };
-template <int R, int V>
+template <int R, int V, bool FEAT = true>
 __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, int64_t row0, int Wb,
                         const StreamSmem &sm, bool prefetch = false) {
   const int nd = p.nd;
@@ -168,8 +174,8 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       }
       const bool tstage = p.use_tmap && ncols == p.cps;  // full stage: one tensor-map TMA
       const uint32_t zbytes = tstage ? (uint32_t)(p.zcs * p.cps * 8) : (uint32_t)(ncols * Wb * 8);
-      const uint32_t fbytes = (has_f0 ? (p.fcm ? p.fs * p.R * 8 : ncols * p.RS * 8) : 0) +
-                              nslow * (p.fcm ? 2 * p.R : p.RS) * 8;
+      const uint32_t fbytes = (has_f0 ? (P_FCM(p) ? p.fs * p.R * 8 : ncols * p.RS * 8) : 0) +
+                              nslow * (P_FCM(p) ? 2 * p.R : p.RS) * 8;
       if (lane == 0) mbar_expect_tx(&sm.full[stage], (part != 2 ? zbytes : 0u) + (part != 1 ? fbytes : 0u));
       __syncwarp();
       if (p.srows && part != 1) {
@@ -179,7 +185,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
         for (int j = 1; j < kMaxDigits; ++j)
           if (j < nd && p.ord[j] != p.mode && lane == j) {
             double *dst = sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.srs;
-            if (p.fcm)  // (even start row, as for digit 0: the slot holds rows B_j & ~1, +1)
+            if (P_FCM(p))  // (even start row, as for digit 0: the slot holds rows B_j & ~1, +1)
               tma_load_2d(dst, &p.fmap[j], B[j] & ~1, 0, &sm.full[stage]);
             else
               bulk_g2s(dst, p.At[p.ord[j]] + (int64_t)B[j] * p.RS, (uint32_t)(p.RS * 8), &sm.full[stage]);
@@ -219,7 +225,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       }
       if (part == 1) {
         // (factor rows by part 2, after the wait)
-      } else if (has_f0 && p.fcm) {
+      } else if (has_f0 && P_FCM(p)) {
         // rows B0 .. B0 + fs - 1 of the column-major factor as one {fs, R} box: rank-major
         // [R][fs] in shared memory (rows past I_k zero-filled)
         // (the innermost TMA coordinate must be 16-byte aligned: the box starts at the even row
@@ -277,7 +283,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
     }
   }
   };
-  if (prefetch && V >= 2) {
+  if (FEAT && prefetch && V >= 2) {
     ProducerState pre = st0;
     run(pre, 1, p.nstages);
     griddep();

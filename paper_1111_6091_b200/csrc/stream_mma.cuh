@@ -520,7 +520,7 @@ __device__ __forceinline__ unsigned long long cta_gtimer() {
 }
 #endif
 
-template <int NT, int MT, int OP>
+template <int NT, int MT, int OP, bool FEAT>
 __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __grid_constant__ StreamPlan p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
 #ifdef CP_CTA_TIMELINE
@@ -566,24 +566,24 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   CTL_BEGIN
   // (PDL) predecessor's At / factor writes visible from here on; with p.prefetch the producer
   // warp first issues the Z part of its first stages and waits inside produce()
-  const bool prefetch = p.prefetch != 0 && p.Mout == nullptr;
+  const bool prefetch = FEAT && p.prefetch != 0 && p.Mout == nullptr;
   if (!(prefetch && (tid >> 5) == kConsumerWarps)) griddep();
   CTL_AFTER_WAIT
   // one-launch cp_mttkrp, mode 0: CTA 0 claims the grid barrier's words for this launch
-  if (OP == OP_MTTKRP && p.mode == 0 && p.Mout != nullptr && blockIdx.x == 0 && tid == 0) grid_claim(p.tick, p.tag);
+  if (FEAT && OP == OP_MTTKRP && p.mode == 0 && p.Mout != nullptr && blockIdx.x == 0 && tid == 0) grid_claim(p.tick, p.tag);
 
   if (warp == kConsumerWarps) {
-    produce<8, 2>(p, lane, v0, v1, row0, Wb, sm, prefetch);  // (template args only select the TMA path)
+    produce<8, 2, FEAT>(p, lane, v0, v1, row0, Wb, sm, prefetch);  // (template args only select the TMA path)
     return;
   }
   if (warp == kConsumerWarps + 1) {
     // weight rows (returns at once when direct_w), then the optional Gamma job of CTA 0
     form_weights(p, lane, sm);
     if (p.gj.on && blockIdx.x == 0) {
-      if (p.gj.gram_rows > 0) gram_rows_warp<NT>(p.gj, lane);
+      if (FEAT && p.gj.gram_rows > 0) gram_rows_warp<NT>(p.gj, lane);
       gamma_job_run(p.gj, sm.gjbuf, lane, 32, false);
     }
-    if (OP == OP_MTTKRP && p.tail.on && blockIdx.x == 0) {
+    if (FEAT && OP == OP_MTTKRP && p.tail.on && blockIdx.x == 0) {
       // publish the job's L^{-1}, Gram totals and status to the tail solves of every CTA
       __threadfence();
       __syncwarp();
@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   const int wstride = p.direct_w ? p.ars : p.wstr;
   // B-fragment strides: (column, rank) at col * bcs + rank * brs -- staged rows [col][rank], or
   // (fcm) the rank-major [rank][fs] box of the column-major factor
-  const int bcs = p.fcm ? 1 : wstride;
+  const int bcs = P_FCM(p) ? 1 : wstride;
   const int bstage = p.direct_w ? p.astage : p.cps * p.wstr;
   const int arow0 = wi * MT * 8 + gq;  // first A row of this lane (m-tile j adds 8 j)
 
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #pragma unroll
   for (int n = 0; n < NT; ++n) {
     nok[n] = (n * 8 + gq) < R;
-    boff[n] = (nok[n] ? n * 8 + gq : 0) * (p.fcm ? p.fs : 1);
+    boff[n] = (nok[n] ? n * 8 + gq : 0) * (P_FCM(p) ? p.fs : 1);
   }
 
   // residual pass (OP_RESID, the mode-0 plan): x(rows, cols) = A^(0)(rows, :) W(cols, :)^T on the
@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     const int flags = h[1];
     const int slot = h[2];
     const double *zs = sm.zbuf + (size_t)stage * p.zst + arow0;
-    const double *ws = (p.direct_w ? sm.abuf : sm.wbuf) + (size_t)stage * bstage + (p.fcm ? h[3] : 0);
+    const double *ws = (p.direct_w ? sm.abuf : sm.wbuf) + (size_t)stage * bstage + (P_FCM(p) ? h[3] : 0);
     // Khatri-Rao rows = staged factor rows x S, S = product of the slow digits' rows (staged by
     // the producer; S = 1 when there are none)
     double sl[NT];
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #pragma unroll
       for (int j = 1; j < kMaxDigits; ++j) {
         if (j < p.nd && p.ord[j] != p.mode) {
-          const double *sr = sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.srs + gq * p.sstr + (p.fcm ? (h[4 + j] & 1) : 0);
+          const double *sr = sm.sbuf + ((size_t)stage * kMaxDigits + j) * p.srs + gq * p.sstr + (P_FCM(p) ? (h[4 + j] & 1) : 0);
 #pragma unroll
           for (int n = 0; n < NT; ++n)
             if (nok[n]) sl[n] *= sr[8 * n * p.sstr];
@@ -806,8 +806,8 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #pragma unroll
       for (int n = 0; n < NT; ++n) pr[n][0] = pr[n][1] = 0.0;
       // A^(1) rows: the row-major copy, or (fcm) the caller's column-major factor
-      const double *a1b = p.fcm ? p.Af[0] + row0 : p.At[0] + row0 * p.RS;
-      const int64_t a1rs = p.fcm ? 1 : p.RS, a1cs = p.fcm ? p.dims[0] : 1;
+      const double *a1b = P_FCM(p) ? p.Af[0] + row0 : p.At[0] + row0 * p.RS;
+      const int64_t a1rs = P_FCM(p) ? 1 : p.RS, a1cs = P_FCM(p) ? p.dims[0] : 1;
 #pragma unroll
       for (int j = 0; j < MT; ++j) {
         const int m = arow0 + 8 * j;
@@ -852,8 +852,8 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #ifdef CP_CTA_TIMELINE
   tl_loop = cta_gtimer();
 #endif
-  if (OP == OP_MTTKRP && p.mode != 0 && p.tail.on) sweep_tail<NT>(p, v0, v1, sm.zbuf);
-  else if (OP == OP_MTTKRP && p.mode != 0 && p.Mout != nullptr) mttkrp_complete_segments(p, v0, v1);
+  if (FEAT && OP == OP_MTTKRP && p.mode != 0 && p.tail.on) sweep_tail<NT>(p, v0, v1, sm.zbuf);
+  else if (FEAT && OP == OP_MTTKRP && p.mode != 0 && p.Mout != nullptr) mttkrp_complete_segments(p, v0, v1);
 
   if (OP == OP_RESID) {
     // ---- this CTA's sum of (z - x)^2: lanes, then warps in order ----
@@ -886,7 +886,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
         }
       }
     }
-    if (p.Mout != nullptr) {
+    if (FEAT && p.Mout != nullptr) {
       // one launch: every CTA's partial stored -> grid barrier -> this CTA's slice of M
       __threadfence();
       named_bar_sync(1, kConsumers);
@@ -906,9 +906,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #endif
 }
 
-template <int NT, int MT, int OP>
+template <int NT, int MT, int OP, bool FEAT>
 cudaError_t launch_stream_mma_t(const StreamPlan &p, cudaStream_t st) {
-  auto kern = stream_mma_kernel<NT, MT, OP>;
+  auto kern = stream_mma_kernel<NT, MT, OP, FEAT>;
   if (cudaError_t e = ensure_smem_attr((const void *)kern, 200 * 1024)) return e;
   return launch_kc(kPdlStream, kern, dim3(p.Gc * p.RB), dim3(kStreamThreads), (size_t)p.smem_bytes, st, p);
 }

@@ -560,3 +560,34 @@ def test_chained_calls_without_sync_match_synced():
     for a, b in zip(chain(False), chain(True)):
         assert np.all(np.isfinite(a))
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dims,R", [((64, 48, 40), 16), ((130, 9, 6), 20), ((30, 28, 26, 12), 6), ((96, 50, 33), 3)])
+def test_lean_stream_kernels_bitwise(dims, R, monkeypatch):
+    """The feature-free instantiations of the tensor-core streaming kernel (what large tensors
+    run: no pre-wait prefetch, no in-pass tail) against the full-feature ones (CP_STREAM_LEAN=0)
+    on the same plans: the same arithmetic, so sweep, fit and gradient agree bitwise; and the
+    lean sweep against the oracle."""
+    monkeypatch.setenv("CP_SMALL_SWEEP", "0")
+    monkeypatch.setenv("CP_STREAM_PREFETCH", "0")
+    monkeypatch.setenv("CP_SWEEP_TAIL", "0")
+    Z, A = cpsynth.random_problem(dims, R, seed=77 + R)
+    nz2 = float(np.vdot(Z, Z))
+    Zd, _ = dev_problem(Z, A)
+    nzd = cp.norm2(Zd, dims)
+    res = {}
+    for lean in ("1", "0"):
+        monkeypatch.setenv("CP_STREAM_LEAN", lean)
+        Ad = [dev_factor(a) for a in A]
+        out = host_tensor(cp.als_sweep(Zd, dims, Ad, nzd, nsweeps=2))
+        fit = host_tensor(cp.fit(Zd, dims, Ad, nzd)[0])
+        g, G = cp.gradient(Zd, dims, Ad, nzd, want_G=True)
+        res[lean] = ([host_factor(a) for a in Ad], out, fit, host_tensor(g), [host_factor(x) for x in G])
+    for a, b in zip(res["1"][0] + res["1"][4], res["0"][0] + res["0"][4]):
+        assert np.array_equal(a, b)
+    for k in (1, 2, 3):
+        assert np.array_equal(res["1"][k], res["0"][k])
+    Ao = [a.copy(order="F") for a in A]
+    for _ in range(2):
+        Ao, oo = oracle.als_sweep(Z, dims, Ao, normZ2=nz2)
+    _check_sweep(res["1"][0], res["1"][1], Ao, oo, nz2)
