@@ -223,7 +223,10 @@ static bool plan_mma(StreamPlan &p, const cp_shape &s, int op) {
   if (best < 0) return false;
   p.mma = 1;
   p.V = 2;
-  p.zcs = (int)(ceil_div(W, 16) * 16 + 8);  // = 8 (mod 16) doubles: conflict-free A fragments
+  // = 4 (mod 16) doubles: conflict-free A fragments (64-bit shared loads are served per half-warp:
+  // lanes (gq, tq), gq in 0..3 or 4..7, hit the 16 distinct bank pairs 4 tq + gq; the former
+  // stride = 8 (mod 16) collided tq with tq + 2 -- 4 wavefronts per fragment instead of 2)
+  p.zcs = (int)(ceil_div(W, 16) * 16 + knob("CP_ZCS_PAD", 4));
   // residual pass: Z is read at the C-fragment positions (row gq, columns 2 tq, 2 tq + 1);
   // a column stride = 2 (mod 8) doubles makes each half-warp hit 16 distinct bank pairs
   if (op == OP_RESID) p.zcs = (int)(ceil_div(W, 8) * 8 + 2);

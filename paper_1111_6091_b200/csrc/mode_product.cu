@@ -124,7 +124,11 @@ __global__ void __launch_bounds__(256) gemm_f64_kernel(const GemmArgs g) {
 // along m, else along k; B_NC: B contiguous along n, else along k) with padded strides that make
 // the fragment reads bank-conflict free (two 128-B wavefronts per 256-B fragment).
 constexpr int TBM = 64, TBN = 128, TBK = 16;
-constexpr int AMS = TBM + 8, AKS = TBK + 4, BNS = TBN + 8, BKS = TBK + 4;
+// (strides = 4 (mod 16) doubles: a 64-bit shared load is served half-warp by half-warp, and lanes
+// (gq, tq) of a half-warp -- gq in 0..3 or 4..7, tq in 0..3 -- then hit the 16 distinct bank pairs
+// 4 tq + gq; a stride = 8 (mod 16) collides tq with tq + 2: ncu showed 4 wavefronts per A fragment
+// instead of 2 at AMS = 72, profiles/r02g_ncu_gemm_c3.md)
+constexpr int AMS = TBM + 4, AKS = TBK + 4, BNS = TBN + 4, BKS = TBK + 4;
 
 __device__ __forceinline__ void dmma_m8n8k4(double &d0, double &d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(256, 2) gemm_dmma_pipe_kernel(const GemmArgs g
   // TN: CTA n-tile (128: warp tiles 32 x 32; 64: 32 x 16 -- twice the tiles for the wave
   // quantization of problems with ~1000 tiles, e.g. the c3 restriction)
   constexpr int WF = TN / 32;  // n-fragments (of 8) per warp
-  constexpr int BNSx = TN + 8, ASZ = A_MC ? TBK * AMS : TBM * AKS, BSZ = B_NC ? TBK * BNSx : TN * BKS;
+  constexpr int BNSx = TN + 4, ASZ = A_MC ? TBK * AMS : TBM * AKS, BSZ = B_NC ? TBK * BNSx : TN * BKS;
   constexpr int BPT = TN * TBK / 2 / 256;  // B pairs per thread
   extern __shared__ __align__(16) double gsm[];
   double *As = gsm, *Bs = gsm + NS * ASZ;
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(256, 2) gemm_dmma_pipe_kernel(const GemmArgs g
 
 template <bool A_MC, bool B_NC, int NS, int TN>
 static size_t dmma_pipe_smem() {
-  return NS * sizeof(double) * (size_t)((A_MC ? TBK * AMS : TBM * AKS) + (B_NC ? TBK * (TN + 8) : TN * BKS));
+  return NS * sizeof(double) * (size_t)((A_MC ? TBK * AMS : TBM * AKS) + (B_NC ? TBK * (TN + 4) : TN * BKS));
 }
 
 template <bool A_MC, bool B_NC, int NS, int TN>

@@ -9,7 +9,7 @@
 //  * warps: KS k-groups of 8/KS warps; k-group kg takes the k-steps (4 columns) kk = kg mod KS
 //    of every stage; warp wi of a group owns m-tiles wi*MT .. wi*MT+MT-1 (8 rows each) and all
 //    NT n-tiles (8 ranks each; ranks >= R are masked to zero).
-//  * shared memory: Z columns at a padded stride zcs = 8 (mod 16) doubles -> the A-fragment
+//  * shared memory: Z columns at a padded stride zcs = 4 (mod 16) doubles -> the A-fragment
 //    reads (8 rows x 4 columns) take the minimal two 128-B wavefronts; the producer issues one
 //    bulk copy per column.  B fragments come from the staged factor rows (direct_w: the
 //    Khatri-Rao rows are the factor rows) or from the weight warp's rows.
