@@ -135,7 +135,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
   st0.eph = 1;
   st0.v = v0;
 #ifdef CP_STREAM_TIMING
-  long long tm_wait = 0, tm_n = 0, tm0 = clock64();
+  long long tm_wait = 0, tm_n = 0, tm0 = clock64(), tm_pre = 0, tm_issue = 0, tm_post = 0, tm_top = 0;
 #endif
   const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
   // part 0: whole stages; 1: Z only (before the wait); 2: the factor rows, header and arrival of
@@ -146,6 +146,9 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
   int &seg_slot = st.seg_slot, &stage = st.stage;
   uint32_t &eph = st.eph;
   while (v < v1 && max_stages-- > 0) {
+#ifdef CP_STREAM_TIMING
+    tm_top = clock64();
+#endif
     int64_t lim = (seg_left < v1 - v) ? seg_left : (v1 - v);
     if (lim > p.rad[0] - B[0]) lim = p.rad[0] - B[0];
     const int ncols = (int)(lim < p.cps ? lim : p.cps);
@@ -157,10 +160,12 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       if (j < nd) q0 += (int64_t)B[j] * p.qsd[j];
 #ifdef CP_STREAM_TIMING
     long long tw0 = clock64();
+    tm_pre += tw0 - tm_top;
 #endif
     if (part != 2) mbar_wait(&sm.empty[stage], eph);
 #ifdef CP_STREAM_TIMING
-    tm_wait += clock64() - tw0;
+    const long long tw1 = clock64();
+    tm_wait += tw1 - tw0;
     ++tm_n;
 #endif
     double *zs = sm.zbuf + (size_t)stage * p.zst;
@@ -252,6 +257,10 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
         for (int e = lane; e < ncols * p.RS; e += 32) as[e] = __ldg(A0 + (int64_t)B[0] * p.RS + e);
       __syncwarp();
     }
+#ifdef CP_STREAM_TIMING
+    const long long tw2 = clock64();
+    tm_issue += tw2 - tw1;
+#endif
     if (lane == 0 && part != 1) {
       int *h = sm.hdr + stage * kHdrInts;
       h[0] = ncols;
@@ -281,6 +290,9 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
       stage = 0;
       eph ^= 1u;
     }
+#ifdef CP_STREAM_TIMING
+    tm_post += clock64() - tw2;
+#endif
   }
   };
   if (FEAT && prefetch && V >= 2) {
@@ -292,7 +304,7 @@ __device__ void produce(const StreamPlan &p, int lane, int64_t v0, int64_t v1, i
   run(st0, 0, 0x7fffffff);
 #ifdef CP_STREAM_TIMING
   if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 101))
-    printf("[cta %d] producer: total %lld wait_empty %lld stages %lld\n", blockIdx.x, clock64() - tm0, tm_wait, tm_n);
+    printf("[cta %d] producer: total %lld wait_empty %lld stages %lld pre %lld issue %lld post %lld\n", blockIdx.x, clock64() - tm0, tm_wait, tm_n, tm_pre, tm_issue, tm_post);
 #endif
 }
 

@@ -641,8 +641,18 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 
   int stage = 0;
   uint32_t fph = 0;
+#ifdef CP_STREAM_TIMING
+  long long tc_wait = 0, tc_n = 0, tc0 = clock64();
+#endif
   for (;;) {
+#ifdef CP_STREAM_TIMING
+    const long long tcw = clock64();
+#endif
     mbar_wait(p.direct_w ? &sm.full[stage] : &sm.wready[stage], fph);
+#ifdef CP_STREAM_TIMING
+    tc_wait += clock64() - tcw;
+    ++tc_n;
+#endif
 #ifdef CP_CTA_TIMELINE
     if (tl_first == 0) tl_first = cta_gtimer();
 #endif
@@ -724,6 +734,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     }
     // full k-steps (4 landed columns): only the rank mask applies
     int k0 = 4 * kg;
+#ifdef CP_EXPERIMENTS
+    if (p.dbg & 1) k0 = ncols;  // (CP_STREAM_DBG=1: consumers only hand the stages back -- the TMA ring alone)
+#endif
     for (; k0 + 4 <= ncols; k0 += 4 * KS) {
       const int col = k0 + tq;
       const double *za = zs + col * zcs;
@@ -851,6 +864,11 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   }
 #ifdef CP_CTA_TIMELINE
   tl_loop = cta_gtimer();
+#endif
+#ifdef CP_STREAM_TIMING
+  // (timing build, tools/one_c4a_sweep.py: the consumers' share of the loop spent waiting for data)
+  if (lane == 0 && (warp == 0 || warp == 7) && (blockIdx.x == 0 || blockIdx.x == 101))
+    printf("[cta %d warp %d op %d] consumer: loop %lld wait_full %lld stages %lld\n", blockIdx.x, warp, OP, clock64() - tc0, tc_wait, tc_n);
 #endif
   if (FEAT && OP == OP_MTTKRP && p.mode != 0 && p.tail.on) sweep_tail<NT>(p, v0, v1, sm.zbuf);
   else if (FEAT && OP == OP_MTTKRP && p.mode != 0 && p.Mout != nullptr) mttkrp_complete_segments(p, v0, v1);
