@@ -643,6 +643,8 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   uint32_t fph = 0;
 #ifdef CP_STREAM_TIMING
   long long tc_wait = 0, tc_n = 0, tc0 = clock64();
+  unsigned long long tg0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg0));
 #endif
   for (;;) {
 #ifdef CP_STREAM_TIMING
@@ -867,8 +869,13 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #endif
 #ifdef CP_STREAM_TIMING
   // (timing build, tools/one_c4a_sweep.py: the consumers' share of the loop spent waiting for data)
-  if (lane == 0 && (warp == 0 || warp == 7) && (blockIdx.x == 0 || blockIdx.x == 101))
-    printf("[cta %d warp %d op %d] consumer: loop %lld wait_full %lld stages %lld\n", blockIdx.x, warp, OP, clock64() - tc0, tc_wait, tc_n);
+  if (lane == 0 && (warp == 0 || warp == 7) && (blockIdx.x == 0 || blockIdx.x == 101)) {
+    unsigned long long tg1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg1));
+    const long long cyc = clock64() - tc0;
+    printf("[cta %d warp %d op %d] consumer: loop %lld cycles in %llu ns (%.0f MHz) wait_full %lld stages %lld\n", blockIdx.x, warp, OP,
+           cyc, tg1 - tg0, 1e3 * (double)cyc / (double)(tg1 - tg0), tc_wait, tc_n);
+  }
 #endif
   if (FEAT && OP == OP_MTTKRP && p.mode != 0 && p.tail.on) sweep_tail<NT>(p, v0, v1, sm.zbuf);
   else if (FEAT && OP == OP_MTTKRP && p.mode != 0 && p.Mout != nullptr) mttkrp_complete_segments(p, v0, v1);
