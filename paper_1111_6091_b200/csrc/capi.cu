@@ -223,10 +223,12 @@ static bool plan_mma(StreamPlan &p, const cp_shape &s, int op) {
   if (best < 0) return false;
   p.mma = 1;
   p.V = 2;
-  // = 4 (mod 16) doubles: conflict-free A fragments (64-bit shared loads are served per half-warp:
-  // lanes (gq, tq), gq in 0..3 or 4..7, hit the 16 distinct bank pairs 4 tq + gq; the former
-  // stride = 8 (mod 16) collided tq with tq + 2 -- 4 wavefronts per fragment instead of 2)
-  p.zcs = (int)(ceil_div(W, 16) * 16 + knob("CP_ZCS_PAD", 4));
+  // column stride = 8 (mod 16) doubles.  (64-bit shared loads are served per half-warp, so = 4
+  // (mod 16) is what makes the A-fragment reads conflict-free -- 2 wavefronts instead of 4, as in
+  // the GEMM of mode_product.cu -- but the shared-memory pipe does not limit these kernels: with
+  // = 4 the sweeps gained 0-0.7 %, while cp_mttkrp mode 0 on c4a went from 0.208 to 0.298 ms
+  // (profiles/r02g_zcs_mode0.txt), so the stride stays; CP_ZCS_PAD in experiment builds.)
+  p.zcs = (int)(ceil_div(W, 16) * 16 + knob("CP_ZCS_PAD", 8));
   // residual pass: Z is read at the C-fragment positions (row gq, columns 2 tq, 2 tq + 1);
   // a column stride = 2 (mod 8) doubles makes each half-warp hit 16 distinct bank pairs
   if (op == OP_RESID) p.zcs = (int)(ceil_div(W, 8) * 8 + 2);

@@ -9,8 +9,8 @@
 //  * warps: KS k-groups of 8/KS warps; k-group kg takes the k-steps (4 columns) kk = kg mod KS
 //    of every stage; warp wi of a group owns m-tiles wi*MT .. wi*MT+MT-1 (8 rows each) and all
 //    NT n-tiles (8 ranks each; ranks >= R are masked to zero).
-//  * shared memory: Z columns at a padded stride zcs = 4 (mod 16) doubles -> the A-fragment
-//    reads (8 rows x 4 columns) take the minimal two 128-B wavefronts; the producer issues one
+//  * shared memory: Z columns at a padded stride zcs = 8 (mod 16) doubles (A-fragment reads of 8
+//    rows x 4 columns: 4 wavefronts; = 4 (mod 16) would give 2, see plan_mma); the producer issues one
 //    bulk copy per column.  B fragments come from the staged factor rows (direct_w: the
 //    Khatri-Rao rows are the factor rows) or from the weight warp's rows.
 //  * ragged stages (fewer than 4 columns in a k-step): A and B masked to zero in registers.
@@ -869,12 +869,18 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
 #endif
 #ifdef CP_STREAM_TIMING
   // (timing build, tools/one_c4a_sweep.py: the consumers' share of the loop spent waiting for data)
+#if CP_STREAM_TIMING >= 2  // (every CTA: the launch's distribution of loop times, tools/cta_loop_times.py)
+  if (lane == 0 && warp == 0) {
+#else
   if (lane == 0 && (warp == 0 || warp == 7) && (blockIdx.x == 0 || blockIdx.x == 101)) {
+#endif
     unsigned long long tg1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg1));
     const long long cyc = clock64() - tc0;
-    printf("[cta %d warp %d op %d] consumer: loop %lld cycles in %llu ns (%.0f MHz) wait_full %lld stages %lld\n", blockIdx.x, warp, OP,
-           cyc, tg1 - tg0, 1e3 * (double)cyc / (double)(tg1 - tg0), tc_wait, tc_n);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    printf("[cta %d warp %d op %d sm %u] consumer: loop %lld cycles in %llu ns (%.0f MHz) wait_full %lld stages %lld start %llu\n", blockIdx.x,
+           warp, OP, smid, cyc, tg1 - tg0, 1e3 * (double)cyc / (double)(tg1 - tg0), tc_wait, tc_n, tg0);
   }
 #endif
   if (FEAT && OP == OP_MTTKRP && p.mode != 0 && p.tail.on) sweep_tail<NT>(p, v0, v1, sm.zbuf);

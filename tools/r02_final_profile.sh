@@ -2,7 +2,7 @@
 # ncu --set full captures of their kernels and of the tiny-level kernel.  One GPU, one process per
 # capture, each after the same command ran clean without ncu.
 mkdir -p gpurun_out
-T=r02f
+T=${T:-r02h}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${T}_smi.txt 2>&1
 for c in c3 c4a c1 cube4; do timeout 300 python tools/prof_steady.py $c 4 || exit 1; done
 for c in c3 c4a c1; do
