@@ -44,6 +44,26 @@
  *     a zero factor column -- the Keller condition of P:362) is written into the device
  *     `out` status word as CP_ENOTSPD together with the failing mode; the factors are then
  *     unspecified.
+ *
+ * Environment
+ *   The shipped library reads a fixed list of PATH SELECTORS from the environment on each call
+ *   (path_flag() in csrc/capi.cu; everything else -- tuning and debugging knobs -- exists only in
+ *   -DCP_EXPERIMENTS builds).  A selector switches between implementations of the same operation
+ *   whose results agree bitwise or within the parity tolerance; each one is exercised by the GPU
+ *   parity tests.  Unset = the default in brackets:
+ *     CP_STREAM_MMA [1]      0: DFMA register-tile consumers instead of the FP64 tensor-core ones
+ *     CP_RESID_MMA [1]       0: DFMA residual pass in cp_fit
+ *     CP_STREAM_TMAP [1]     0: one bulk copy per Z column instead of one tensor-map TMA per stage
+ *     CP_STREAM_LEAN [1]     0: full-feature streaming kernels also for plans that need no feature
+ *     CP_STREAM_PREFETCH [1 up to 2^26 elements]  Z of the first stages issued before the PDL wait
+ *     CP_SWEEP_TREE [1]      0: one Z pass per mode instead of the two-pass dimension tree
+ *     CP_SWEEP_TAIL [1 up to 2^26 elements]  last mode solved inside the mode-2 pass (2: every sweep)
+ *     CP_YLSOLVE [1]         0: separate contraction and solve kernels for modes 0 and 1
+ *     CP_SMALL_SWEEP [1], CP_TINY_SWEEP [1], CP_SWEEPS_GRAD_FUSED [1]  fused kernels of small tensors
+ *     CP_MTTKRP_FCM [1], CP_MTTKRP_FUSED [1]  cp_mttkrp: factor rows from the caller's factors, one launch
+ *     CP_MODEPROD_DMMA [1], CP_MODEPROD_PIPE [1]  mode products: tensor-core GEMM, cp.async ring
+ *     CP_MG_GRAPH [1], CP_ALS_GRAPH [1], CP_MG_STRUCTURED [1]  host driver: CUDA graphs, structured restriction
+ *     CP_PDL [1]             0: no programmatic dependent launch
  */
 #ifndef CP_H
 #define CP_H
