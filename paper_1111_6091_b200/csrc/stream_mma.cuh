@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
   int stage = 0;
   uint32_t fph = 0;
 #ifdef CP_STREAM_TIMING
-  long long tc_wait = 0, tc_n = 0, tc0 = clock64();
+  long long tc_wait = 0, tc_n = 0, tc0 = clock64(), tc_flush = 0, tc_nflush = 0;
   unsigned long long tg0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg0));
 #endif
@@ -784,6 +784,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
       fph ^= 1u;
     }
 
+#ifdef CP_STREAM_TIMING
+    const long long tcf = clock64();
+#endif
     if (OP == OP_YL && (flags & 1)) {
       // ---- end of an i_1 segment: the CTA's I0-block x R block of Y_L(:, i_1, :) ----
       const int Wq = opaque(Wb);
@@ -862,6 +865,12 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
       }
       named_bar_sync(1, kConsumers);
     }
+#ifdef CP_STREAM_TIMING
+    if (flags & 1) {
+      tc_flush += clock64() - tcf;
+      ++tc_nflush;
+    }
+#endif
     if (flags & 2) break;
   }
 #ifdef CP_CTA_TIMELINE
@@ -879,8 +888,8 @@ __global__ void __launch_bounds__(kStreamThreads, 2) stream_mma_kernel(const __g
     const long long cyc = clock64() - tc0;
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    printf("[cta %d warp %d op %d sm %u] consumer: loop %lld cycles in %llu ns (%.0f MHz) wait_full %lld stages %lld start %llu\n", blockIdx.x,
-           warp, OP, smid, cyc, tg1 - tg0, 1e3 * (double)cyc / (double)(tg1 - tg0), tc_wait, tc_n, tg0);
+    printf("[cta %d warp %d op %d sm %u] consumer: loop %lld cycles in %llu ns (%.0f MHz) wait_full %lld stages %lld flush %lld in %lld segment ends start %llu\n", blockIdx.x,
+           warp, OP, smid, cyc, tg1 - tg0, 1e3 * (double)cyc / (double)(tg1 - tg0), tc_wait, tc_n, tc_flush, tc_nflush, tg0);
   }
 #endif
   if (FEAT && OP == OP_MTTKRP && p.mode != 0 && p.tail.on) sweep_tail<NT>(p, v0, v1, sm.zbuf);
