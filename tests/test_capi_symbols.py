@@ -127,3 +127,23 @@ def test_peaks_library_exports_header_symbols():
     assert P.cpp_fp64_peaks(ctypes.byref(a), ctypes.byref(b), 0) == -1
     assert P.cpp_fp64_peaks(None, ctypes.byref(b), 1) == -1
     assert P.cpp_launch_floor_us(0, ctypes.byref(a)) == -1
+
+
+def test_every_path_selector_is_documented_in_cp_h():
+    """The environment switches the shipped library reads (path_flag's whitelist in csrc/capi.cu)
+    are exactly the ones include/cp.h documents: no undocumented global changes a result path."""
+    import re
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "paper_1111_6091_b200", "csrc", "capi.cu")).read()
+    m = re.search(r"kPaths\[\]\s*=\s*\{(.*?)\};", src, re.S)
+    assert m, "path_flag whitelist not found"
+    names = re.findall(r'"(CP_[A-Z0-9_]+)"', m.group(1))
+    assert len(names) >= 10
+    hdr = open(os.path.join(root, "include", "cp.h")).read()
+    missing = [n for n in names if n not in hdr]
+    assert not missing, f"selectors missing from include/cp.h: {missing}"
+    # and every path_flag() call site uses a whitelisted name (others would silently return the default)
+    used = set()
+    for fn in os.listdir(os.path.join(root, "paper_1111_6091_b200", "csrc")):
+        used |= set(re.findall(r'path_flag\("(CP_[A-Z0-9_]+)"', open(os.path.join(root, "paper_1111_6091_b200", "csrc", fn)).read()))
+    assert used <= set(names), f"path_flag names not in the whitelist: {sorted(used - set(names))}"
